@@ -1,0 +1,167 @@
+/*
+ * mk_b200.h -- C ABI of the B200 checking stage (libmk_b200.so).
+ *
+ * Drop-in boundary.  The reference checking stage is the Python class
+ * minikernel.engine.detectors.Detectors (engine/detectors.py:46-57) whose
+ * five site methods (arithmetic_site :69, narrowing_site :84, access_site
+ * :134, store_site :204, deref_site :277) each build one solver query and,
+ * when it is satisfiable, pin the canonical witness with
+ * engine/report.py:147 canonicalize_witness -> solver/interface.py:112/154
+ * minimize/maximize -> solver/builtin.py:705 check_assertions.
+ *
+ * The reference has no FFI of its own (pure Python);
+ * this header is the seam its Python checker binds through ctypes
+ * (paper_2603_24595_b200/native.py).  One call replaces, for every query in
+ * a batch, the decision check_assertions(...) (solver/builtin.py:705-764)
+ * AND the canonicalisation loop (engine/report.py:147-174): the engine
+ * returns, per compiled problem, unsat / sat + the lexicographically optimal
+ * point in witness order / unknown (budget exhausted), exactly the
+ * three-valued verdict of solver/query.py:11-42.
+ *
+ * Plain C types only: no torch types cross this boundary.  128-bit integers
+ * travel as mk_i128 (two's complement, little endian).  Every function
+ * returns 0 on success and a negative MK_E* code on failure; the message is
+ * available from mk_last_error().  A context is bound to one device and is
+ * not thread safe; calls are synchronous at return.
+ */
+#ifndef MK_B200_H
+#define MK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MK_ABI_VERSION 1
+
+#define MK_OK 0
+#define MK_EINVAL (-1)
+#define MK_ECUDA (-2)
+#define MK_ENOMEM (-3)
+#define MK_ENODEV (-4)
+
+/* per-problem verdicts (solver/query.py:11-42) */
+#define MK_UNSAT 0
+#define MK_SAT 1
+#define MK_UNKNOWN 2
+
+/* bytecode opcodes (register machine, mathematical integer semantics of
+ * sym/expr.py:273-383: unbounded integers, truncating div/mod, Euclidean
+ * emod, shl = *2^k, shr = floor shift, errors make a point a non-model) */
+#define MK_OP_ADD 1
+#define MK_OP_SUB 2
+#define MK_OP_MUL 3
+#define MK_OP_DIV 4
+#define MK_OP_MOD 5
+#define MK_OP_EMOD 6
+#define MK_OP_SHL 7
+#define MK_OP_SHR 8
+#define MK_OP_EQ 16
+#define MK_OP_NE 17
+#define MK_OP_LT 18
+#define MK_OP_LE 19
+#define MK_OP_GT 20
+#define MK_OP_GE 21
+#define MK_OP_AND 32 /* short-circuit, as sym/expr.py:370-374 */
+#define MK_OP_OR 33  /* short-circuit, as sym/expr.py:375-378 */
+#define MK_OP_NOT 34
+#define MK_OP_ITE 35
+/* fold atom register a (atom index b) into the verdict; a definitely false
+ * atom ends the evaluation of the box / point early */
+#define MK_OP_ATOM 40
+
+typedef struct mk_i128 {
+  uint64_t lo;
+  int64_t hi;
+} mk_i128;
+
+typedef struct mk_insn {
+  uint16_t op, dst, a, b, c, pad;
+} mk_insn;
+
+/* One independent lexicographic search: free symbols 0..nvars-1 in witness
+ * order (engine/report.py:177-203), each minimised or maximised; the point
+ * is a model iff every atom register evaluates true without error
+ * (solver/query.py:45-62).  Registers 0..nvars-1 hold the symbols,
+ * nvars..nvars+nconst-1 the constants, the rest temporaries. */
+typedef struct mk_problem {
+  int32_t nvars, ninsn, nregs, natoms, nconst, nrows;
+  int32_t var_off;   /* into var_lo / var_hi / mk_result.point */
+  int32_t insn_off;  /* into insns */
+  int32_t const_off; /* into consts */
+  int32_t atom_off;  /* into atom_regs / atom_masks */
+  int32_t row_off;   /* into rows */
+  int32_t pad;
+  uint64_t maxmask;  /* bit i: symbol i is maximised */
+} mk_problem;
+
+/* Linear rows used for bound contraction inside a box:
+ *   sum_k coef_k * x_var_k + c0  (rel 0: <= 0, rel 1: == 0) */
+typedef struct mk_row {
+  int32_t rel, nterms, term_off, pad;
+  mk_i128 c0;
+} mk_row;
+
+typedef struct mk_row_term {
+  int32_t var, pad0;
+  int64_t pad1;
+  mk_i128 coef;
+} mk_row_term;
+
+typedef struct mk_problem_set {
+  int32_t nprob;
+  int32_t nvar_total, ninsn_total, nconst_total, natom_total, nrow_total, nterm_total;
+  int32_t pad;
+  const mk_problem* probs;
+  const mk_i128* var_lo;
+  const mk_i128* var_hi;
+  const mk_insn* insns;
+  const mk_i128* consts;
+  const int32_t* atom_regs;
+  const uint64_t* atom_masks;
+  const mk_row* rows;
+  const mk_row_term* row_terms;
+} mk_problem_set;
+
+typedef struct mk_limits {
+  int64_t max_rounds;   /* branch-and-prune rounds (0 = default) */
+  int64_t max_boxes;    /* boxes evaluated (0 = default) */
+  double max_seconds;   /* wall budget, mirrors Budget.query_timeout_s (engine/state.py:38) */
+  int32_t split_k;      /* children per split (0 = default 16) */
+  int32_t chunk;        /* boxes per round (0 = default) */
+  int64_t leaf_volume;  /* boxes at most this large are enumerated exhaustively */
+} mk_limits;
+
+typedef struct mk_stats {
+  int64_t rounds;       /* host loop iterations (each: prune kernel + leaf kernel) */
+  int64_t boxes;        /* boxes interval-evaluated */
+  int64_t leaves;       /* boxes enumerated exhaustively */
+  int64_t points;       /* concrete instances evaluated (the roofline basis) */
+  double covered;       /* instances decided: pruned + enumerated (box volume) */
+  double seconds;       /* wall time of the call incl. H2D/D2H */
+  double bb_ms;         /* device time of the prune kernels (CUDA events) */
+  double leaf_ms;       /* device time of the leaf kernels (CUDA events) */
+  int64_t insns_bb;     /* bytecode instructions executed by the prune kernel */
+  int64_t insns_leaf;   /* bytecode instructions executed by the leaf kernel */
+} mk_stats;
+
+typedef struct mk_ctx mk_ctx;
+
+int mk_abi_version(void);
+int mk_device_count(int* out);
+int mk_ctx_create(int device, mk_ctx** out);
+int mk_ctx_destroy(mk_ctx* ctx);
+const char* mk_last_error(const mk_ctx* ctx);
+
+/* Decide every problem of the set.  status[nprob] receives MK_UNSAT /
+ * MK_SAT / MK_UNKNOWN, point[nvar_total] the lexicographically optimal
+ * point of each satisfiable problem.  Host buffers; the copies to and from
+ * the device happen inside the call. */
+int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_limits* lim,
+                 int32_t* status, mk_i128* point, mk_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MK_B200_H */

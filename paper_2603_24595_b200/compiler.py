@@ -1,0 +1,1411 @@
+"""Site compiler: one checker query -> GPU search problems.
+
+A site query is the assertion list the reference's checker hands its solver
+(``engine/detectors.py:111-116`` overflow, ``:143-147`` bounds,
+``:213-219`` race, ``:284`` deref).  The reference decides it with an exact
+ILP procedure and then pins every symbol by bisection to the canonical
+lexicographic optimum (``engine/report.py:147-203``).  This module turns the
+query into data-parallel search problems whose lexicographic optimum over
+a finite box *is* that canonical witness, and which the sm_100a engine
+decides by interval branch-and-prune plus exhaustive leaf enumeration.
+
+Steps (each exact: the model set and the witness order are preserved):
+
+1. simplify and split into symbol-connected components exactly as the
+   reference does (``solver/builtin.py:727-737``, ``:767-793``) so that the
+   three-valued combination rule (unsat > unknown > sat,
+   ``solver/builtin.py:737-750``) can be mirrored;
+2. per component, mirror what the reference cannot decide: paths through a
+   float atom or a non-constant shift are unsupported
+   (``solver/linear.py:389-391``, ``:459-477``), a non-constant ``shr`` or a
+   division by constant zero makes the whole component unsupported
+   (``solver/linear.py:148-150``, ``:219-229``, ``:284-286``).  Unsupported
+   atoms are replaced by FALSE in negation normal form; an empty remainder
+   with such atoms present is ``unknown``;
+3. presolve: linear normalisation, bound extraction, fixed-symbol folding,
+   elimination of a symbol defined by a unit-coefficient equality (only when
+   every other symbol of the equality precedes it in witness order, so the
+   optimum over the remaining free symbols is unchanged), lattice
+   substitution for ``emod(.., c) == r`` loop-summary atoms
+   (``engine/executor.py:680-684``), gcd aggregation of wide equality terms,
+   and interval bound tightening;
+4. split the remaining atoms into independent problems and emit register
+   bytecode for the device.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Callable, Dict, List, Optional, Sequence, Set, Tuple
+
+from . import ir
+from .ir import Node
+from .order import optimization_order
+
+INF = None  # unbounded side of an interval
+
+# opcodes shared with csrc/mk_engine.cuh
+OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_MOD, OP_EMOD, OP_SHL, OP_SHR = 1, 2, 3, 4, 5, 6, 7, 8
+OP_EQ, OP_NE, OP_LT, OP_LE, OP_GT, OP_GE = 16, 17, 18, 19, 20, 21
+OP_AND, OP_OR, OP_NOT, OP_ITE = 32, 33, 34, 35
+OP_ATOM = 40
+_ARITH_OP = {"add": OP_ADD, "sub": OP_SUB, "mul": OP_MUL, "div": OP_DIV,
+             "mod": OP_MOD, "emod": OP_EMOD, "shl": OP_SHL, "shr": OP_SHR}
+_CMP_OP = {"eq": OP_EQ, "ne": OP_NE, "lt": OP_LT, "le": OP_LE, "gt": OP_GT, "ge": OP_GE}
+
+MAX_VARS = 64        # free symbols per device problem (bit mask width)
+MAX_REGS = 1024
+_AGG_WIDE = 4096
+_NEG = {"eq": "ne", "ne": "eq", "lt": "ge", "le": "gt", "gt": "le", "ge": "lt"}
+_FLIP = {"lt": "gt", "le": "ge", "gt": "lt", "ge": "le", "eq": "eq", "ne": "ne"}
+
+
+class CompileError(Exception):
+    """The query is outside what the compiler handles; the site is reported
+    ``unknown`` (mirrors the reference's honest-unknown convention)."""
+
+
+# -- device problem --------------------------------------------------------------------
+
+@dataclass
+class Problem:
+    """One independent lexicographic search over a box of free symbols."""
+
+    var_names: List[str]           # free symbols in witness (position) order
+    lo: List[int]
+    hi: List[int]
+    maximize: List[bool]
+    insns: List[Tuple[int, int, int, int, int]] = field(default_factory=list)
+    consts: List[int] = field(default_factory=list)
+    nregs: int = 0
+    atom_regs: List[int] = field(default_factory=list)
+    atom_masks: List[int] = field(default_factory=list)
+    rows: List[Tuple[int, int, List[Tuple[int, int]]]] = field(default_factory=list)
+    ops_per_point: int = 0         # instructions evaluated per instance
+
+    @property
+    def nvars(self) -> int:
+        return len(self.var_names)
+
+    def volume(self) -> int:
+        v = 1
+        for a, b in zip(self.lo, self.hi):
+            v *= (b - a + 1)
+        return v
+
+
+@dataclass
+class Group:
+    """A raw (reference-level) component and the problems it compiled to."""
+
+    status: str                    # "pending" | "unsat" | "unknown"
+    reason: Optional[str]
+    had_unsupported: bool
+    problems: List[int] = field(default_factory=list)
+
+
+@dataclass
+class CompiledQuery:
+    witness_names: List[str]
+    order: List[Tuple[str, str]]
+    groups: List[Group]
+    problems: List[Problem]
+    defs: Dict[str, Node]          # eliminated symbols -> expr over free symbols
+    free_default: Dict[str, int]   # symbols absent from every atom
+
+    def assemble(self, results: Sequence[Tuple[str, Optional[List[int]]]]):
+        """Combine per-problem device results into the reference verdict.
+
+        Returns (status, witness) with status in sat/unsat/unknown."""
+        status = "sat"
+        pending_unknown = False
+        for g in self.groups:
+            if g.status == "unsat":
+                return "unsat", {}
+            if g.status == "unknown":
+                pending_unknown = True
+                continue
+            gs = "sat"
+            for pi in g.problems:
+                st = results[pi][0]
+                if st == "unsat":
+                    gs = "unsat"
+                    break
+                if st != "sat":
+                    gs = "unknown"
+            if gs == "unsat":
+                if g.had_unsupported:
+                    pending_unknown = True
+                    continue
+                return "unsat", {}
+            if gs == "unknown":
+                pending_unknown = True
+        if pending_unknown:
+            return "unknown", {}
+        binding: Dict[str, int] = dict(self.free_default)
+        for p, (st, point) in zip(self.problems, results):
+            for name, v in zip(p.var_names, point):
+                binding[name] = v
+        for name, e in self.defs.items():
+            binding[name] = ir.evaluate(e, binding)
+        witness = {n: binding[n] for n in sorted(self.witness_names) if n in binding}
+        return status, witness
+
+
+# -- linear forms ------------------------------------------------------------------------
+
+LinForm = Tuple[Dict[object, int], int]   # term -> coeff, const ; term is str | opaque Node
+
+
+def _lin_add(a: LinForm, b: LinForm, sign: int = 1) -> LinForm:
+    out = dict(a[0])
+    for k, c in b[0].items():
+        v = out.get(k, 0) + sign * c
+        if v:
+            out[k] = v
+        else:
+            out.pop(k, None)
+    return out, a[1] + sign * b[1]
+
+
+def _lin_scale(a: LinForm, f: int) -> LinForm:
+    if f == 0:
+        return {}, 0
+    return {k: c * f for k, c in a[0].items()}, a[1] * f
+
+
+def _term_sort_key(k) -> Tuple[int, str]:
+    return (0, k) if isinstance(k, str) else (1, ir.render(k))
+
+
+def lin_to_ir(lf: LinForm, widths: Dict[str, str]) -> Node:
+    terms, c = lf
+    acc: Optional[Node] = None
+    for k in sorted(terms, key=_term_sort_key):
+        coef = terms[k]
+        t = ("s", k, widths.get(k, "i64")) if isinstance(k, str) else k
+        if coef != 1:
+            t = ("b", "mul", ("c", coef, "i64"), t, "i64")
+        acc = t if acc is None else ("b", "add", acc, t, "i64")
+    if acc is None:
+        return ("c", c, "i64")
+    if c:
+        acc = ("b", "add", acc, ("c", c, "i64"), "i64")
+    return acc
+
+
+class _Lin:
+    """Memoised linearisation of integer IR into linear forms over symbols
+    and opaque nonlinear subterms (math-mode exact)."""
+
+    def __init__(self, widths: Dict[str, str]) -> None:
+        self.widths = widths
+        self.memo: Dict[Node, LinForm] = {}
+
+    def norm(self, e: Node) -> Node:
+        return lin_to_ir(self.lin(e), self.widths)
+
+    def lin(self, e: Node) -> LinForm:
+        got = self.memo.get(e)
+        if got is not None:
+            return got
+        r = self._lin(e)
+        self.memo[e] = r
+        return r
+
+    def _opaque(self, e: Node) -> LinForm:
+        return {e: 1}, 0
+
+    def _lin(self, e: Node) -> LinForm:
+        t = e[0]
+        if t == "c":
+            if not isinstance(e[1], int):
+                raise CompileError("float constant in arithmetic")
+            return {}, int(e[1])
+        if t == "s":
+            return {e[1]: 1}, 0
+        if t == "x":
+            return self.lin(e[1])
+        if t == "b":
+            op = e[1]
+            la = self.lin(e[2])
+            if op in ("add", "sub"):
+                return _lin_add(la, self.lin(e[3]), 1 if op == "add" else -1)
+            lb = self.lin(e[3])
+            if op == "mul":
+                if not la[0]:
+                    return _lin_scale(lb, la[1])
+                if not lb[0]:
+                    return _lin_scale(la, lb[1])
+                a = lin_to_ir(la, self.widths)
+                b = lin_to_ir(lb, self.widths)
+                if ir.render(a) > ir.render(b):
+                    a, b = b, a
+                return self._opaque(("b", "mul", a, b, "i64"))
+            if op == "shl" and not lb[0] and 0 <= lb[1] <= 256:
+                return _lin_scale(la, 1 << lb[1])
+            if not lb[0] and not la[0]:
+                try:
+                    return {}, ir.apply_binop(op, la[1], lb[1])
+                except ir.EvalError:
+                    pass
+            if op in ("div", "mod", "emod") and not lb[0] and lb[1] != 0:
+                c = lb[1]
+                if op == "emod":
+                    m = abs(c)
+                    terms = {}
+                    for k, v in la[0].items():
+                        r = v % m
+                        if r > m // 2:
+                            r -= m
+                        if r:
+                            terms[k] = r
+                    if not terms:
+                        return {}, la[1] % m
+                    k0 = la[1] % m
+                    inner = lin_to_ir((terms, k0), self.widths)
+                    return self._opaque(("b", "emod", inner, ("c", m, "i64"), "i64"))
+                if all(v % c == 0 for v in la[0].values()) and la[1] % c == 0:
+                    if op == "div":
+                        return {k: v // c for k, v in la[0].items()}, la[1] // c
+                    return {}, 0
+                inner = lin_to_ir(la, self.widths)
+                return self._opaque(("b", op, inner, ("c", c, "i64"), "i64"))
+            a = lin_to_ir(la, self.widths)
+            b = lin_to_ir(lb, self.widths)
+            return self._opaque(("b", op, a, b, "i64"))
+        if t == "i":
+            return self._opaque(e)
+        raise CompileError(f"boolean node in arithmetic position: {e[0]}")
+
+
+# -- interval helper (math mode, None = unbounded) ---------------------------------------------
+
+def _imul(x, y):
+    c = []
+    for a in x:
+        for b in y:
+            if a is None or b is None:
+                return (None, None)
+            c.append(a * b)
+    return (min(c), max(c))
+
+
+def _tdiv(a, b):
+    q = abs(a) // abs(b)
+    return q if (a >= 0) == (b >= 0) else -q
+
+
+class _Ivl:
+    def __init__(self, bounds: Dict[str, Tuple[Optional[int], Optional[int]]]):
+        self.bounds = bounds
+        self.memo: Dict[Node, Tuple[Optional[int], Optional[int]]] = {}
+
+    def __call__(self, e: Node):
+        got = self.memo.get(e)
+        if got is not None:
+            return got
+        r = self._go(e)
+        self.memo[e] = r
+        return r
+
+    def _go(self, e: Node):
+        t = e[0]
+        if t == "c":
+            return (e[1], e[1])
+        if t == "s":
+            return self.bounds.get(e[1], (None, None))
+        if t == "x":
+            return self(e[1])
+        if t in ("p", "o"):
+            return (0, 1)
+        if t == "i":
+            a, b = self(e[2]), self(e[3])
+            lo = None if a[0] is None or b[0] is None else min(a[0], b[0])
+            hi = None if a[1] is None or b[1] is None else max(a[1], b[1])
+            return (lo, hi)
+        op = e[1]
+        x, y = self(e[2]), self(e[3])
+        add = lambda p, q: None if p is None or q is None else p + q  # noqa: E731
+        if op == "add":
+            return (add(x[0], y[0]), add(x[1], y[1]))
+        if op == "sub":
+            return (add(x[0], None if y[1] is None else -y[1]),
+                    add(x[1], None if y[0] is None else -y[0]))
+        if op == "mul":
+            return _imul(x, y)
+        if op == "shl" and y[0] is not None and y[0] == y[1] and 0 <= y[0] <= 256:
+            return _imul(x, (1 << y[0], 1 << y[0]))
+        if op == "shr" and y[0] is not None and y[0] == y[1] and 0 <= y[0] <= 256:
+            return (None if x[0] is None else x[0] >> y[0],
+                    None if x[1] is None else x[1] >> y[0])
+        if op == "emod" and y[0] is not None and y[0] == y[1] and y[0] != 0:
+            return (0, abs(y[0]) - 1)
+        if op == "div" and y[0] is not None and y[1] is not None and (y[0] >= 1 or y[1] <= -1):
+            if x[0] is None or x[1] is None:
+                return (None, None)
+            c = [_tdiv(a, b) for a in x for b in y]
+            return (min(c), max(c))
+        if op == "mod" and y[0] is not None and y[0] == y[1] and y[0] != 0:
+            m = abs(y[0]) - 1
+            return (0 if (x[0] is not None and x[0] >= 0) else -m,
+                    0 if (x[1] is not None and x[1] <= 0) else m)
+        return (None, None)
+
+
+# -- boolean normal form ------------------------------------------------------------------
+
+def _has_float(e: Node) -> bool:
+    t = e[0]
+    if t in ("c", "s"):
+        return ir.is_float(e[2])
+    if t in ("b", "x", "i") and ir.is_float(ir.width_of(e)):
+        return True
+    if t == "x" and ir.is_float(ir.width_of(e[1])):
+        return True
+    return any(_has_float(c) for c in ir.children(e))
+
+
+def _bad_shl(e: Node) -> bool:
+    if e[0] == "b" and e[1] == "shl":
+        r = e[3]
+        if r[0] != "c" or not (0 <= r[1] <= 256):
+            return True
+    return any(_bad_shl(c) for c in ir.children(e))
+
+
+def _component_unsupported(e: Node) -> Optional[str]:
+    """Whole-component failures raised by the reference's ``rewrite_divs``
+    (solver/linear.py:130-306)."""
+    if e[0] == "b":
+        op, r = e[1], e[3]
+        if op == "shr" and (r[0] != "c" or not (0 <= r[1] <= 256)):
+            return "unsupported: shift amount must be a small constant"
+        if op in ("div", "mod") and r[0] == "c" and r[1] == 0:
+            return "unsupported: division by constant zero"
+        if op == "emod" and r[0] == "c" and r[1] == 0:
+            return "unsupported: emod by constant zero"
+    for c in ir.children(e):
+        got = _component_unsupported(c)
+        if got:
+            return got
+    return None
+
+
+def _nnf(e: Node, neg: bool, flags: Dict[str, bool]) -> Node:
+    """Negation normal form with unsupported atoms replaced by FALSE
+    (the reference drops such paths, solver/builtin.py:815-821)."""
+    t = e[0]
+    if t == "c":
+        v = 1 if e[1] else 0
+        return ir.TRUE if (v ^ neg) else ir.FALSE
+    if t == "o":
+        if e[1] == "not":
+            return _nnf(e[2][0], not neg, flags)
+        op = e[1]
+        if neg:
+            op = "or" if op == "and" else "and"
+        return ("o", op, tuple(_nnf(a, neg, flags) for a in e[2]))
+    if t == "p":
+        if _has_float(e) or _bad_shl(e):
+            flags["unsupported"] = True
+            return ir.FALSE
+        op = _NEG[e[1]] if neg else e[1]
+        return ("p", op, e[2], e[3])
+    if t == "i":
+        c_pos = _nnf(e[1], False, flags)
+        c_neg = _nnf(e[1], True, flags)
+        th = _nnf(e[2], neg, flags)
+        ot = _nnf(e[3], neg, flags)
+        return ("o", "or", (("o", "and", (c_pos, th)), ("o", "and", (c_neg, ot))))
+    if t == "s" and e[2] == "bool":
+        return ("p", "eq" if not neg else "ne", e, ("c", 1, "bool"))
+    raise CompileError(f"cannot assert a {t} node")
+
+
+def _may_err(e: Node) -> bool:
+    """True when evaluating ``e`` can raise (symbolic or zero divisor)."""
+    if e[0] == "b" and e[1] in ("div", "mod", "emod"):
+        r = e[3]
+        if not (r[0] == "c" and r[1] != 0):
+            return True
+    return any(_may_err(c) for c in ir.children(e))
+
+
+def _truth(e: Node, ivl: "_Ivl") -> str:
+    """Three-valued truth of a normalised boolean node over symbol bounds."""
+    t = e[0]
+    if t == "c":
+        return "T" if e[1] else "F"
+    if t == "p":
+        a, b = ivl(e[2]), ivl(e[3])
+        if None in a or None in b:
+            lo = None if a[0] is None or b[1] is None else a[0] - b[1]
+            hi = None if a[1] is None or b[0] is None else a[1] - b[0]
+        else:
+            lo, hi = a[0] - b[1], a[1] - b[0]
+        op = e[1]
+        if op == "le":
+            if hi is not None and hi <= 0:
+                return "T"
+            if lo is not None and lo > 0:
+                return "F"
+        elif op == "lt":
+            if hi is not None and hi < 0:
+                return "T"
+            if lo is not None and lo >= 0:
+                return "F"
+        elif op == "ge":
+            if lo is not None and lo >= 0:
+                return "T"
+            if hi is not None and hi < 0:
+                return "F"
+        elif op == "gt":
+            if lo is not None and lo > 0:
+                return "T"
+            if hi is not None and hi <= 0:
+                return "F"
+        elif op in ("eq", "ne"):
+            tv = "?"
+            if lo is not None and hi is not None and lo == hi == 0:
+                tv = "T"
+            elif (lo is not None and lo > 0) or (hi is not None and hi < 0):
+                tv = "F"
+            if op == "ne" and tv != "?":
+                tv = "F" if tv == "T" else "T"
+            return tv
+        return "?"
+    if t == "o":
+        if e[1] == "not":
+            v = _truth(e[2][0], ivl)
+            return {"T": "F", "F": "T"}.get(v, "?")
+        vals = [_truth(a, ivl) for a in e[2]]
+        if e[1] == "and":
+            if "F" in vals:
+                return "F"
+            return "T" if all(v == "T" for v in vals) else "?"
+        if "T" in vals:
+            return "T"
+        return "F" if all(v == "F" for v in vals) else "?"
+    return "?"
+
+
+def _form_key(terms: Dict[object, int]) -> Tuple[Tuple, int]:
+    """(normalised form, factor) with terms == factor * form, the form
+    gcd-reduced with its first coefficient positive."""
+    g = 0
+    for v in terms.values():
+        g = math.gcd(g, abs(v))
+    first = min(terms, key=_term_sort_key)
+    f = g if terms[first] > 0 else -g
+    key = tuple(sorted(((k if isinstance(k, str) else ir.render(k)), v // f)
+                       for k, v in terms.items()))
+    return key, f
+
+
+# -- presolve ----------------------------------------------------------------------------
+
+class _Presolve:
+    def __init__(self, atoms: List[Node], widths: Dict[str, str],
+                 pos: Dict[str, float], maximize: Dict[str, bool]) -> None:
+        self.widths = widths
+        self.pos = pos
+        self.maximize = maximize
+        self.bounds: Dict[str, Tuple[Optional[int], Optional[int]]] = {}
+        for n, w in widths.items():
+            self.bounds[n] = ir.bounds(w)
+        self.defs: Dict[str, Node] = {}
+        self.atoms: List[Node] = list(dict.fromkeys(atoms))
+        self.unsat = False
+        self.kcount = 0
+        self.fm_rounds = 0
+        self.fbbt_passes = 0
+        self.agg_done: Set[Tuple] = set()
+        self.cuts: Set[Node] = set()
+
+    # symbols of an IR node (memo-free; atoms are small)
+    @staticmethod
+    def _vars(e: Node) -> Set[str]:
+        return set(ir.symbols_of(e))
+
+    def _canon_cmp(self, lin: _Lin, op: str, l: Node, r: Node) -> Node:
+        """Normalise ``l op r`` to ``L op' 0`` with op' in le/eq/ne."""
+        lf = _lin_add(lin.lin(l), lin.lin(r), -1)
+        terms, c = lf
+        if op in ("gt", "ge"):
+            terms, c = {k: -v for k, v in terms.items()}, -c
+            op = "lt" if op == "gt" else "le"
+        if op == "lt":
+            c += 1
+            op = "le"
+        if not terms:
+            ok = {"le": c <= 0, "eq": c == 0, "ne": c != 0}[op]
+            return ir.TRUE if ok else ir.FALSE
+        g = 0
+        for v in terms.values():
+            g = math.gcd(g, abs(v))
+        if op == "le":
+            terms = {k: v // g for k, v in terms.items()}
+            c = -((-c) // g)          # ceil(c / g)
+        else:
+            if c % g:
+                return ir.FALSE if op == "eq" else ir.TRUE
+            terms = {k: v // g for k, v in terms.items()}
+            c //= g
+            first = min(terms, key=_term_sort_key)
+            if terms[first] < 0:
+                terms, c = {k: -v for k, v in terms.items()}, -c
+        return ("p", op, lin_to_ir((terms, c), self.widths), ("c", 0, "i64"))
+
+    def _normalize(self, e: Node, lin: _Lin, ivl: Optional["_Ivl"] = None) -> Node:
+        t = e[0]
+        if t == "p":
+            return self._canon_cmp(lin, e[1], e[2], e[3])
+        if t == "o":
+            args = tuple(self._normalize(a, lin, ivl) for a in e[2])
+            if ivl is not None and e[1] in ("and", "or"):
+                # drop operands decided by the symbol bounds; only operands that
+                # cannot raise (no symbolic divisor) may go, since an error in
+                # an operand makes the whole point a non-model
+                drop = "F" if e[1] == "or" else "T"
+                absorb = "T" if e[1] == "or" else "F"
+                kept = []
+                for a in args:
+                    tv = _truth(a, ivl)
+                    if tv == absorb and not _may_err(a):
+                        kept = None
+                        break
+                    if tv == drop and not _may_err(a):
+                        continue
+                    kept.append(a)
+                if kept is None:
+                    return ir.TRUE if e[1] == "or" else ir.FALSE
+                if not kept:
+                    return ir.FALSE if e[1] == "or" else ir.TRUE
+                args = tuple(kept)
+            return ir.simplify(("o", e[1], args))
+        return e
+
+    def _split_and(self, atoms: List[Node]) -> List[Node]:
+        out: List[Node] = []
+        for a in atoms:
+            if a[0] == "o" and a[1] == "and":
+                out.extend(self._split_and(list(a[2])))
+            else:
+                out.append(a)
+        return out
+
+    def _set_bound(self, v: str, lo, hi) -> bool:
+        olo, ohi = self.bounds.get(v, (None, None))
+        nlo = olo if lo is None else (lo if olo is None else max(olo, lo))
+        nhi = ohi if hi is None else (hi if ohi is None else min(ohi, hi))
+        if (nlo, nhi) != (olo, ohi):
+            self.bounds[v] = (nlo, nhi)
+            if nlo is not None and nhi is not None and nlo > nhi:
+                self.unsat = True
+            return True
+        return False
+
+    def _substitute(self, name: str, e: Node) -> None:
+        m = {name: e}
+        self.atoms = [ir.substitute(a, m) for a in self.atoms]
+        for k in list(self.defs):
+            self.defs[k] = ir.substitute(self.defs[k], m)
+        self.defs[name] = e
+
+    def _eliminate(self, name: str, e: Node) -> None:
+        lo, hi = self.bounds.pop(name, (None, None))
+        if lo is not None:
+            self.atoms.append(("p", "ge", e, ("c", lo, "i64")))
+        if hi is not None:
+            self.atoms.append(("p", "le", e, ("c", hi, "i64")))
+        self._substitute(name, e)
+
+    def _lin_of_atom(self, lin: _Lin, a: Node) -> Optional[LinForm]:
+        if a[0] == "p" and a[3] == ("c", 0, "i64"):
+            return lin.lin(a[2])
+        return None
+
+    def run(self, max_iter: int = 200) -> None:
+        for _ in range(max_iter):
+            if self.unsat:
+                return
+            if not self._pass():
+                return
+
+    def _pass(self) -> bool:
+        lin = _Lin(self.widths)
+        ivl0 = _Ivl(self.bounds)
+        # 1. normalise, split conjunctions, drop truths
+        new_atoms: List[Node] = []
+        for a in self._split_and(self.atoms):
+            n = self._normalize(a, lin, ivl0)
+            if n == ir.TRUE:
+                continue
+            if n == ir.FALSE:
+                self.unsat = True
+                return False
+            if n[0] == "o" and n[1] == "and":
+                new_atoms.extend(self._split_and([n]))
+            else:
+                new_atoms.append(n)
+        changed = new_atoms != self.atoms
+        self.atoms = list(dict.fromkeys(new_atoms))
+        # 2. unary bounds
+        kept: List[Node] = []
+        for a in self.atoms:
+            lf = self._lin_of_atom(lin, a)
+            if lf is not None and len(lf[0]) == 1:
+                (k, c), = lf[0].items()
+                if isinstance(k, str) and a[1] in ("le", "eq"):
+                    const = lf[1]
+                    if a[1] == "eq":
+                        if (-const) % c:
+                            self.unsat = True
+                            return False
+                        v = (-const) // c
+                        self._set_bound(k, v, v)
+                    elif c > 0:
+                        self._set_bound(k, None, (-const) // c)
+                    else:
+                        self._set_bound(k, math.ceil(Fraction(-const, c)), None)
+                    changed = True
+                    if self.unsat:
+                        return False
+                    continue
+            kept.append(a)
+        self.atoms = kept
+        # 3. fold fixed symbols
+        fixed = [(n, b[0]) for n, b in self.bounds.items()
+                 if b[0] is not None and b[0] == b[1]]
+        if fixed:
+            for n, v in fixed:
+                del self.bounds[n]
+                self._substitute(n, ("c", v, "i64"))
+            return True
+        if changed:
+            return True
+        # 4. unit-coefficient equality elimination (order preserving)
+        if self._try_eliminate(lin):
+            return True
+        # 5. lattice substitution for emod(.., c) == r
+        if self._try_lattice(lin):
+            return True
+        # 6. gcd aggregation of wide terms
+        if self._try_aggregate(lin):
+            return True
+        if self._try_aggregate_ineq(lin):
+            return True
+        # 7. Fourier-Motzkin implied rows (sound cuts, never remove models)
+        if self._try_fm(lin):
+            return True
+        # 8. interval bound tightening (capped: slow creep is left to the device)
+        if self.fbbt_passes >= 24:
+            return False
+        self.fbbt_passes += 1
+        return self._fbbt(lin)
+
+    def _free_deps(self, k) -> Set[str]:
+        return {k} if isinstance(k, str) else self._vars(k)
+
+    def _try_eliminate(self, lin: _Lin) -> bool:
+        best = None
+        for a in self.atoms:
+            if a[0] != "p" or a[1] != "eq":
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None:
+                continue
+            terms, c = lf
+            opaque_vars: Set[str] = set()
+            for k in terms:
+                if not isinstance(k, str):
+                    opaque_vars |= self._vars(k)
+            cands = [k for k, v in terms.items()
+                     if isinstance(k, str) and abs(v) == 1 and k not in opaque_vars]
+            if not cands:
+                continue
+            v = max(cands, key=lambda n: self.pos[n])
+            others: Set[str] = set(opaque_vars)
+            for k in terms:
+                if isinstance(k, str) and k != v:
+                    others.add(k)
+            if any(self.pos[o] >= self.pos[v] for o in others):
+                continue
+            coef = terms[v]
+            rest = {k: -x * coef for k, x in terms.items() if k != v}
+            expr = lin_to_ir((rest, -c * coef), self.widths)
+            if best is None or self.pos[v] > self.pos[best[0]]:
+                best = (v, expr)
+        if best is None:
+            return False
+        self._eliminate(best[0], best[1])
+        return True
+
+    def _try_lattice(self, lin: _Lin) -> bool:
+        for idx, a in enumerate(self.atoms):
+            if a[0] != "p" or a[1] != "eq":
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None or len(lf[0]) != 1:
+                continue
+            (k, c1), = lf[0].items()
+            if isinstance(k, str) or k[0] != "b" or k[1] != "emod" or abs(c1) != 1:
+                continue
+            m = k[3][1]
+            r = -lf[1] * c1
+            if not 0 <= r < m:
+                self.unsat = True
+                return True
+            inner = lin.lin(k[2])
+            terms, k0 = inner
+            opaque_vars: Set[str] = set()
+            for t in terms:
+                if not isinstance(t, str):
+                    opaque_vars |= self._vars(t)
+            cands = [t for t, v in terms.items()
+                     if isinstance(t, str) and abs(v) == 1 and t not in opaque_vars]
+            if not cands:
+                continue
+            v = max(cands, key=lambda n: self.pos[n])
+            others = set(opaque_vars) | {t for t in terms if isinstance(t, str) and t != v}
+            if any(self.pos[o] >= self.pos[v] for o in others):
+                continue
+            av = terms[v]
+            # av*v + R + k0 = m*kk + r  ->  v = av*(m*kk + r - k0 - R)
+            kname = f"{v}#k{self.kcount}"
+            self.kcount += 1
+            self.widths[kname] = "i64"
+            self.pos[kname] = self.pos[v] - 0.25
+            self.maximize[kname] = self.maximize.get(v, False) ^ (av < 0)
+            self.bounds[kname] = (None, None)
+            rest = {t: -x * av for t, x in terms.items() if t != v}
+            rest[kname] = m * av
+            expr = lin_to_ir((rest, (r - k0) * av), self.widths)
+            del self.atoms[idx]
+            self._eliminate(v, expr)
+            return True
+        return False
+
+    def _try_aggregate(self, lin: _Lin) -> bool:
+        ivl = _Ivl(self.bounds)
+        existing = set(self.atoms)
+        for a in self.atoms:
+            if a[0] != "p" or a[1] != "eq":
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None:
+                continue
+            terms, c = lf
+            wide, rlo, rhi = [], c, c
+            for k, v in terms.items():
+                if isinstance(k, str):
+                    lo, hi = self.bounds.get(k, (None, None))
+                else:
+                    lo, hi = ivl(k)
+                if isinstance(k, str) and (lo is None or hi is None or hi - lo > _AGG_WIDE):
+                    wide.append(k)
+                    continue
+                if lo is None or hi is None:
+                    rlo = rhi = None
+                    break
+                if rlo is not None:
+                    rlo += min(v * lo, v * hi)
+                    rhi += max(v * lo, v * hi)
+            if rlo is None or not wide or len(wide) == len(terms):
+                continue
+            g = 0
+            for k in wide:
+                g = math.gcd(g, abs(terms[k]))
+            if g <= 1:
+                continue
+            w_lo = -((rhi) // g)   # ceil(-rhi/g)
+            w_hi = (-rlo) // g
+            if w_lo > w_hi:
+                self.unsat = True
+                return True
+            if w_lo != w_hi:
+                continue
+            wt = {k: terms[k] // g for k in wide}
+            new = self._canon_cmp(lin, "eq", lin_to_ir((wt, -w_lo), self.widths), ("c", 0, "i64"))
+            if new == ir.FALSE:
+                self.unsat = True
+                return True
+            if new != ir.TRUE and new not in existing:
+                self.atoms.append(new)
+                return True
+        return False
+
+    def _form_bounds(self, lin: _Lin) -> Dict[Tuple, List]:
+        """Bounds that single rows state on a normalised linear form
+        (gcd-reduced, first coefficient positive)."""
+        out: Dict[Tuple, List] = {}
+        for a in self.atoms:
+            if a[0] != "p" or a[1] not in ("le", "eq"):
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None or not lf[0]:
+                continue
+            key, f = _form_key(lf[0])
+            c = lf[1]
+            ent = out.setdefault(key, [None, None])
+            # f*F0 + c <= 0
+            if f > 0:
+                ub = (-c) // f
+                ent[1] = ub if ent[1] is None else min(ent[1], ub)
+            else:
+                lb = math.ceil(Fraction(-c, f))
+                ent[0] = lb if ent[0] is None else max(ent[0], lb)
+            if a[1] == "eq":
+                if f > 0:
+                    lb = math.ceil(Fraction(-c, f))
+                    ent[0] = lb if ent[0] is None else max(ent[0], lb)
+                else:
+                    ub = math.floor(Fraction(-c, f))
+                    ent[1] = ub if ent[1] is None else min(ent[1], ub)
+        return out
+
+    def _try_aggregate_ineq(self, lin: _Lin) -> bool:
+        """Per wide linear form W (terms with range > 4096, common gcd g),
+        intersect the W-bounds every row implies; a singleton becomes the
+        equality W == w (the reference's row aggregation, applied to
+        inequalities too), a tighter range becomes two implied rows.  The
+        narrow remainder's range uses symbol bounds and any row bounding
+        the same linear form."""
+        ivl = _Ivl(self.bounds)
+        fb = self._form_bounds(lin)
+        acc: Dict[Tuple, List] = {}
+        for a in self.atoms:
+            if a[0] != "p" or a[1] not in ("le", "eq"):
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None:
+                continue
+            terms, c = lf
+            wide, rlo, rhi = [], 0, 0
+            narrow: Dict[object, int] = {}
+            for k, v in terms.items():
+                lo, hi = self.bounds.get(k, (None, None)) if isinstance(k, str) else ivl(k)
+                if isinstance(k, str) and (lo is None or hi is None or hi - lo > _AGG_WIDE):
+                    wide.append(k)
+                    continue
+                narrow[k] = v
+                if lo is None or hi is None:
+                    rlo = rhi = None
+                    continue
+                if rlo is not None:
+                    rlo += min(v * lo, v * hi)
+                    rhi += max(v * lo, v * hi)
+            if narrow and len(narrow) > 1:
+                key, f = _form_key(narrow)
+                got = fb.get(key)
+                if got is not None:
+                    lo0, hi0 = got
+                    cands = [x * f for x in (lo0, hi0) if x is not None]
+                    if lo0 is not None and hi0 is not None:
+                        nlo, nhi = min(cands), max(cands)
+                    elif len(cands) == 1:
+                        nlo, nhi = (cands[0], None) if (f > 0) == (lo0 is not None) else (None, cands[0])
+                    else:
+                        nlo = nhi = None
+                    if rlo is None:
+                        rlo, rhi = nlo, nhi
+                    else:
+                        if nlo is not None:
+                            rlo = max(rlo, nlo)
+                        if nhi is not None:
+                            rhi = min(rhi, nhi)
+            if rlo is None or rhi is None:
+                continue
+            rlo += c
+            rhi += c
+            if rlo is None or not wide or len(wide) == len(terms):
+                continue
+            g = 0
+            for k in wide:
+                g = math.gcd(g, abs(terms[k]))
+            wt = {k: terms[k] // g for k in wide}
+            first = min(wt, key=_term_sort_key)
+            sign = 1 if wt[first] > 0 else -1
+            key = tuple(sorted((k, sign * v) for k, v in wt.items()))
+            # g*sign*W' + R <= 0  with W' = sign*wt
+            ent = acc.setdefault(key, [None, None])
+            ub = (-rlo) // g                      # g*w <= -R  =>  w <= floor(-rlo/g)
+            if sign > 0:
+                ent[1] = ub if ent[1] is None else min(ent[1], ub)
+            else:
+                lb = -ub
+                ent[0] = lb if ent[0] is None else max(ent[0], lb)
+            if a[1] == "eq":
+                lb2 = -((rhi) // g)               # w >= ceil(-rhi/g)
+                if sign > 0:
+                    ent[0] = lb2 if ent[0] is None else max(ent[0], lb2)
+                else:
+                    ent[1] = -lb2 if ent[1] is None else min(ent[1], -lb2)
+        existing = set(self.atoms)
+        added = False
+        for key, (lo, hi) in acc.items():
+            if lo is not None and hi is not None and lo > hi:
+                self.unsat = True
+                return True
+            wt = dict(key)
+            if lo is not None and hi is not None and 0 < hi - lo <= _AGG_WIDE \
+                    and key not in self.agg_done:
+                # name the narrow combination: v := cv*(w - rest) for the last
+                # unit-coefficient symbol v of W, w taking v's witness slot
+                cands = [k for k, c in wt.items() if abs(c) == 1]
+                if cands:
+                    v = max(cands, key=lambda n: self.pos[n])
+                    if all(self.pos[o] < self.pos[v] for o in wt if o != v):
+                        self.agg_done.add(key)
+                        cv = wt[v]
+                        wname = f"{v}#w{self.kcount}"
+                        self.kcount += 1
+                        self.widths[wname] = "i64"
+                        self.pos[wname] = self.pos[v] - 0.25
+                        self.maximize[wname] = self.maximize.get(v, False) ^ (cv < 0)
+                        self.bounds[wname] = (lo, hi)
+                        rest = {k: -c * cv for k, c in wt.items() if k != v}
+                        rest[wname] = cv
+                        self._eliminate(v, lin_to_ir((rest, 0), self.widths))
+                        return True
+            wl = lin_to_ir((wt, 0), self.widths)
+            cur = ivl(wl)
+            news = []
+            if lo is not None and hi is not None and lo == hi:
+                news.append(self._canon_cmp(lin, "eq", wl, ("c", lo, "i64")))
+            else:
+                if hi is not None and (cur[1] is None or hi < cur[1]):
+                    news.append(self._canon_cmp(lin, "le", wl, ("c", hi, "i64")))
+                if lo is not None and (cur[0] is None or lo > cur[0]):
+                    news.append(self._canon_cmp(lin, "ge", wl, ("c", lo, "i64")))
+            for n in news:
+                if n == ir.FALSE:
+                    self.unsat = True
+                    return True
+                if n != ir.TRUE and n not in existing and n not in self.cuts:
+                    self.cuts.add(n)
+                    self.atoms.append(n)
+                    existing.add(n)
+                    added = True
+        return added
+
+    def _try_fm(self, lin: _Lin, max_terms: int = 3, max_new: int = 16) -> bool:
+        """Add Fourier-Motzkin combinations of pairs of linear rows that
+        cancel one symbol.  Non-negative combinations of rows are implied by
+        them, so the model set is unchanged; the new rows let bound
+        propagation and the device contraction see relational facts such as
+        bx < SL and 4096*bx + idx >= 4096*SL  =>  idx >= 4096."""
+        if self.fm_rounds >= 8:
+            return False
+        self.fm_rounds += 1
+        rows: List[Tuple[Dict[str, int], int]] = []
+        for a in self.atoms:
+            if a[0] != "p" or a[1] not in ("le", "eq"):
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None:
+                continue
+            rows.append(lf)   # opaque product terms combine like symbols
+            if a[1] == "eq":
+                rows.append(({k: -v for k, v in lf[0].items()}, -lf[1]))
+        existing = set(self.atoms)
+        added = 0
+        def wide(n: str) -> bool:
+            lo, hi = self.bounds.get(n, (None, None))
+            return lo is None or hi is None or hi - lo > _AGG_WIDE
+
+        # only wide symbols are eliminated: narrow ones are cheap to enumerate
+        symbols = sorted({k for t, _ in rows for k in t if isinstance(k, str) and wide(k)},
+                         key=lambda n: self.pos.get(n, 0))
+        if len(self.cuts) >= 48:
+            return False
+        for v in symbols:
+            pos_rows = [r for r in rows if r[0].get(v, 0) > 0]
+            neg_rows = [r for r in rows if r[0].get(v, 0) < 0]
+            for p in pos_rows:
+                for q in neg_rows:
+                    a, b = p[0][v], -q[0][v]
+                    comb = _lin_add(_lin_scale(p, b), _lin_scale(q, a))
+                    if not comb[0]:
+                        if comb[1] > 0:
+                            self.unsat = True
+                            return True
+                        continue
+                    if len(comb[0]) > max_terms:
+                        continue
+                    n = self._canon_cmp(lin, "le", lin_to_ir(comb, self.widths), ("c", 0, "i64"))
+                    if n == ir.FALSE:
+                        self.unsat = True
+                        return True
+                    if n == ir.TRUE or n in existing or n in self.cuts:
+                        continue
+                    self.cuts.add(n)
+                    existing.add(n)
+                    self.atoms.append(n)
+                    added += 1
+                    if added >= max_new:
+                        return True
+        return added > 0
+
+    def _fbbt(self, lin: _Lin, rounds: int = 8) -> bool:
+        any_change = False
+        for _ in range(rounds):
+            ivl = _Ivl(self.bounds)
+            changed = False
+            for a in self.atoms:
+                lf = self._lin_of_atom(lin, a)
+                if lf is None or a[1] == "ne":
+                    continue
+                terms, c = lf
+                parts = []
+                for k, v in terms.items():
+                    lo, hi = self.bounds.get(k, (None, None)) if isinstance(k, str) else ivl(k)
+                    parts.append((k, v, lo, hi))
+                for j, (k, v, _, _) in enumerate(parts):
+                    if not isinstance(k, str):
+                        continue
+                    rlo, rhi = c, c
+                    for i, (k2, v2, lo, hi) in enumerate(parts):
+                        if i == j:
+                            continue
+                        if v2 > 0:
+                            rlo = None if rlo is None or lo is None else rlo + v2 * lo
+                            rhi = None if rhi is None or hi is None else rhi + v2 * hi
+                        else:
+                            rlo = None if rlo is None or hi is None else rlo + v2 * hi
+                            rhi = None if rhi is None or lo is None else rhi + v2 * lo
+                    # v*x + rest <= 0  (and >= 0 for eq)
+                    nlo = nhi = None
+                    if rlo is not None:
+                        if v > 0:
+                            nhi = (-rlo) // v
+                        else:
+                            nlo = math.ceil(Fraction(-rlo, v))
+                    if a[1] == "eq" and rhi is not None:
+                        if v > 0:
+                            nlo = math.ceil(Fraction(-rhi, v))
+                        else:
+                            nhi = math.floor(Fraction(-rhi, v))
+                    if self._set_bound(k, nlo, nhi):
+                        changed = True
+                        if self.unsat:
+                            return True
+            if not changed:
+                break
+            any_change = True
+        return any_change
+
+
+# -- bytecode emission -------------------------------------------------------------------
+
+class _Emitter:
+    def __init__(self, var_index: Dict[str, int]) -> None:
+        self.var_index = var_index
+        self.nvars = len(var_index)
+        self.consts: List[int] = []
+        self.const_reg: Dict[int, int] = {}
+        self.code: List[List[int]] = []      # [op, dst, a, b, c] with virtual regs
+        self.memo: Dict[Node, int] = {}
+        self.next_v = 0
+
+    def _const(self, v: int) -> int:
+        r = self.const_reg.get(v)
+        if r is None:
+            r = -(len(self.consts) + 1)        # negative = const slot
+            self.consts.append(v)
+            self.const_reg[v] = r
+        return r
+
+    def _tmp(self) -> int:
+        self.next_v += 1
+        return 1_000_000 + self.next_v
+
+    def emit(self, e: Node) -> int:
+        got = self.memo.get(e)
+        if got is not None:
+            return got
+        t = e[0]
+        if t == "c":
+            r = self._const(int(e[1]))
+        elif t == "s":
+            r = ("V", self.var_index[e[1]])
+        elif t == "x":
+            r = self.emit(e[1])
+        elif t == "b":
+            a = self.emit(e[2])
+            b = self.emit(e[3])
+            r = self._tmp()
+            self.code.append([_ARITH_OP[e[1]], r, a, b, 0])
+        elif t == "p":
+            a = self.emit(e[2])
+            b = self.emit(e[3])
+            r = self._tmp()
+            self.code.append([_CMP_OP[e[1]], r, a, b, 0])
+        elif t == "o":
+            if e[1] == "not":
+                a = self.emit(e[2][0])
+                r = self._tmp()
+                self.code.append([OP_NOT, r, a, 0, 0])
+            else:
+                op = OP_AND if e[1] == "and" else OP_OR
+                r = self.emit(e[2][0])
+                for arg in e[2][1:]:
+                    b = self.emit(arg)
+                    d = self._tmp()
+                    self.code.append([op, d, r, b, 0])
+                    r = d
+        elif t == "i":
+            c = self.emit(e[1])
+            a = self.emit(e[2])
+            b = self.emit(e[3])
+            r = self._tmp()
+            self.code.append([OP_ITE, r, c, a, b])
+        else:
+            raise CompileError(f"cannot emit {t}")
+        self.memo[e] = r
+        return r
+
+    def atom(self, e: Node, index: int) -> None:
+        r = self.emit(e)
+        self.code.append([OP_ATOM, 0, r, index, 0])
+
+    def finish(self, atom_vregs: List[object]) -> Tuple[List[Tuple[int, int, int, int, int]], int, List[int]]:
+        """Resolve virtual registers with a linear-scan allocator."""
+        base = self.nvars + len(self.consts)
+
+        def phys_fixed(r) -> Optional[int]:
+            if isinstance(r, tuple):
+                return r[1]
+            if isinstance(r, int) and r < 0:
+                return self.nvars + (-r - 1)
+            return None
+
+        # atoms must survive to the end
+        last_use: Dict[int, int] = {}
+        for i, ins in enumerate(self.code):
+            opnds = ins[2:3] if ins[0] == OP_ATOM else ins[2:5]
+            for opnd in opnds:
+                if isinstance(opnd, int) and opnd >= 1_000_000:
+                    last_use[opnd] = i
+        end = len(self.code)
+        for r in atom_vregs:
+            if isinstance(r, int) and r >= 1_000_000:
+                last_use[r] = end
+        free: List[int] = []
+        nphys = base
+        assign: Dict[int, int] = {}
+        out: List[Tuple[int, int, int, int, int]] = []
+        for i, ins in enumerate(self.code):
+            op, d, a, b, c = ins
+
+            def res(x):
+                f = phys_fixed(x)
+                if f is not None:
+                    return f
+                if isinstance(x, int) and x >= 1_000_000:
+                    return assign[x]
+                return 0
+            if op == OP_ATOM:
+                pa = res(a)
+                if isinstance(a, int) and a >= 1_000_000 and last_use.get(a) == i and a in assign:
+                    free.append(assign.pop(a))
+                out.append((op, 0, pa, b, 0))
+                continue
+            pa, pb = res(a), res(b) if op != OP_NOT else 0
+            pc = res(c) if op == OP_ITE else 0
+            # release operands whose last use is here
+            for x in (a, b, c):
+                if isinstance(x, int) and x >= 1_000_000 and last_use.get(x) == i and x in assign:
+                    free.append(assign.pop(x))
+            if free:
+                pd = free.pop()
+            else:
+                pd = nphys
+                nphys += 1
+            assign[d] = pd
+            if d not in last_use:   # dead value: release immediately
+                free.append(assign.pop(d))
+            out.append((op, pd, pa, pb, pc))
+        atom_regs = []
+        for r in atom_vregs:
+            f = phys_fixed(r)
+            atom_regs.append(f if f is not None else assign[r])
+        if nphys > MAX_REGS:
+            raise CompileError(f"site needs {nphys} registers (> {MAX_REGS})")
+        return out, nphys, atom_regs
+
+
+def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
+                  maximize: List[bool], atoms: List[Node]) -> Problem:
+    if len(var_names) > MAX_VARS:
+        raise CompileError(f"{len(var_names)} free symbols in one component (> {MAX_VARS})")
+    index = {n: i for i, n in enumerate(var_names)}
+    em = _Emitter(index)
+    # cheap linear rows first: a definitely-false atom ends evaluation early
+    atoms = sorted(atoms, key=lambda a: (0 if a[0] == "p" and a[1] in ("le", "eq") else 1))
+    for i, a in enumerate(atoms):
+        em.atom(a, i)
+    code, nregs, _ = em.finish([])
+    atom_regs = [0] * len(atoms)
+    masks = []
+    for a in atoms:
+        m = 0
+        for n in ir.symbols_of(a):
+            m |= 1 << index[n]
+        masks.append(m)
+    # purely linear atoms double as contraction rows (sum <= 0 / sum == 0)
+    rows: List[Tuple[int, int, List[Tuple[int, int]]]] = []
+    lin = _Lin({})
+    for a in atoms:
+        if a[0] == "p" and a[1] in ("le", "eq") and a[3] == ("c", 0, "i64"):
+            terms, c0 = lin.lin(a[2])
+            if terms and all(isinstance(k, str) for k in terms):
+                rows.append((0 if a[1] == "le" else 1, c0,
+                             [(index[k], v) for k, v in sorted(terms.items())]))
+    return Problem(var_names=var_names, lo=lo, hi=hi, maximize=maximize,
+                   insns=code, consts=list(em.consts), nregs=nregs,
+                   atom_regs=atom_regs, atom_masks=masks, rows=rows,
+                   ops_per_point=len(code))
+
+
+# -- driver ------------------------------------------------------------------------------
+
+def _components(assertions: Sequence[Node]) -> List[List[Node]]:
+    """Union-find over shared symbols, symbol-free assertions ride with the
+    first group (solver/builtin.py:767-793)."""
+    parent = list(range(len(assertions)))
+
+    def find(i: int) -> int:
+        while parent[i] != i:
+            parent[i] = parent[parent[i]]
+            i = parent[i]
+        return i
+
+    owner: Dict[str, int] = {}
+    for i, a in enumerate(assertions):
+        for name in ir.symbols_of(a):
+            if name in owner:
+                parent[find(i)] = find(owner[name])
+            else:
+                owner[name] = i
+    groups: Dict[int, List[Node]] = {}
+    order: List[int] = []
+    for i, a in enumerate(assertions):
+        r = find(i)
+        if r not in groups:
+            groups[r] = []
+            order.append(r)
+        groups[r].append(a)
+    return [groups[r] for r in order]
+
+
+def compile_query(assertions: Sequence[Node],
+                  origin_of: Callable[[str], str]) -> CompiledQuery:
+    """Compile one checker query (a list of IR assertions)."""
+    widths: Dict[str, str] = {}
+    for a in assertions:
+        ir.symbols_of(a, widths)
+    order = optimization_order(widths, origin_of)
+    pos = {n: float(i) for i, (n, _) in enumerate(order)}
+    maximize = {n: d == "max" for n, d in order}
+    witness_names = sorted(widths)
+
+    simplified = [ir.simplify(a) for a in assertions]
+    groups: List[Group] = []
+    problems: List[Problem] = []
+    defs: Dict[str, Node] = {}
+    free_default: Dict[str, int] = {}
+    seen_syms: Set[str] = set()
+
+    for comp in _components(simplified):
+        csyms: Dict[str, str] = {}
+        for a in comp:
+            ir.symbols_of(a, csyms)
+        seen_syms |= set(csyms)
+        reason = None
+        for a in comp:
+            reason = _component_unsupported(a)
+            if reason:
+                break
+        if reason:
+            groups.append(Group("unknown", reason, True))
+            continue
+        flags = {"unsupported": False}
+        try:
+            atoms = [ir.simplify(_nnf(a, False, flags)) for a in comp]
+        except CompileError as exc:
+            groups.append(Group("unknown", str(exc), True))
+            continue
+        int_widths = {n: w for n, w in csyms.items() if not ir.is_float(w)}
+        ps = _Presolve(atoms, dict(int_widths), dict(pos), dict(maximize))
+        try:
+            ps.run()
+        except CompileError as exc:
+            groups.append(Group("unknown", str(exc), True))
+            continue
+        had = flags["unsupported"]
+        if ps.unsat:
+            groups.append(Group("unsat" if not had else "unknown",
+                                "float/unsupported atoms only" if had else None, had))
+            continue
+        for n, e in ps.defs.items():
+            defs[n] = e
+        # post-presolve components over free symbols
+        free = [n for n in ps.bounds]
+        atom_vars = [set(ir.symbols_of(a)) for a in ps.atoms]
+        parent = {n: n for n in free}
+
+        def find(x: str) -> str:
+            while parent[x] != x:
+                parent[x] = parent[parent[x]]
+                x = parent[x]
+            return x
+
+        for vs in atom_vars:
+            vs = list(vs)
+            for o in vs[1:]:
+                ra, rb = find(vs[0]), find(o)
+                if ra != rb:
+                    parent[ra] = rb
+        buckets: Dict[str, List[int]] = {}
+        for i, vs in enumerate(atom_vars):
+            if vs:
+                buckets.setdefault(find(next(iter(vs))), []).append(i)
+        grp = Group("pending", None, had)
+        used: Set[str] = set()
+        for root, idxs in buckets.items():
+            names = sorted({n for i in idxs for n in atom_vars[i]}, key=lambda n: ps.pos[n])
+            used |= set(names)
+            lo = [ps.bounds[n][0] for n in names]
+            hi = [ps.bounds[n][1] for n in names]
+            if any(v is None for v in lo + hi):
+                raise CompileError("unbounded free symbol after presolve")
+            mx = [ps.maximize.get(n, False) for n in names]
+            prob = _emit_problem(names, lo, hi, mx, [ps.atoms[i] for i in idxs])
+            grp.problems.append(len(problems))
+            problems.append(prob)
+        # free symbols constrained by bounds only: their optimum is a bound,
+        # still decided on the device as an atom-free problem
+        rest = sorted((n for n in free if n not in used), key=lambda n: ps.pos[n])
+        if rest:
+            lo = [ps.bounds[n][0] for n in rest]
+            hi = [ps.bounds[n][1] for n in rest]
+            if any(v is None for v in lo + hi):
+                raise CompileError("unbounded free symbol after presolve")
+            mx = [ps.maximize.get(n, False) for n in rest]
+            prob = _emit_problem(rest, lo, hi, mx, [])
+            grp.problems.append(len(problems))
+            problems.append(prob)
+        groups.append(grp)
+
+    # symbols that simplification removed entirely: unconstrained, so the
+    # canonical value is the width bound in the optimisation direction
+    for n, w in widths.items():
+        if n not in seen_syms and not ir.is_float(w):
+            lo, hi = ir.bounds(w)
+            free_default[n] = hi if maximize.get(n) else lo
+    return CompiledQuery(witness_names=witness_names, order=order, groups=groups,
+                         problems=problems, defs=defs, free_default=free_default)

@@ -1,0 +1,633 @@
+// mk_engine.cu -- sm_100a checking-stage engine behind include/mk_b200.h.
+//
+// Replaces, per compiled site problem, the reference's decision
+// (solver/builtin.py:705-764 check_assertions) and canonical-witness search
+// (engine/report.py:147-203 + solver/interface.py:112-187 bisection) by a
+// data-parallel lexicographic branch-and-prune over the problem's box of free
+// symbols:
+//
+//   k_bb    one thread per box: incumbent test on the box's best corner, linear
+//           bound contraction, interval evaluation of the bytecode, then
+//           prune / accept the corner / hand to leaf enumeration / split the
+//           first undecided symbol (witness order) into K children written in
+//           lexicographic order;
+//   k_leaf  one CTA per small box: exhaustive concrete evaluation of every
+//           instance in lexicographic order, first model per thread, CTA min
+//           reduction of the instance index (index order == witness order),
+//           incumbent update under a per-problem seqlock;
+//   stack   LIFO of boxes in HBM; children are compacted with
+//           cub::DeviceSelect::Flagged (order preserving) so the best child
+//           of the best box is always on top (depth-first in witness order,
+//           which finds the incumbent early and prunes the rest).
+//
+// The host loop (mk_site_eval) runs rounds until the stack is empty.
+
+#include <cuda_runtime.h>
+#include <cub/cub.cuh>
+
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mk_b200.h"
+#include "mk_core.cuh"
+
+namespace {
+
+struct Box {
+  int32_t prob;
+  int32_t pad0;
+  int64_t pad1;
+  // followed by i128 lo[S], hi[S]
+};
+
+struct Incumbent {
+  int lock;
+  unsigned version;
+  int has;
+  int err;  // inexact evaluation (saturation) or unsplittable box
+};
+
+struct DevSet {
+  const mk_problem* probs;
+  const mk_insn* insns;
+  const mk_i128* consts;
+  const int32_t* atom_regs;
+  const uint64_t* atom_masks;
+  const mk_row* rows;
+  const mk_row_term* terms;
+  const mk_i128* var_lo;
+  const mk_i128* var_hi;
+  Incumbent* inc;
+  mk_i128* best;  // nvar_total
+  int stride;     // S
+  size_t box_bytes;
+};
+
+struct DevStats {
+  unsigned long long boxes, leaves, points, insns_bb, insns_leaf;
+  double covered;
+};
+
+__device__ __forceinline__ Box* box_at(void* base, size_t box_bytes, size_t i) {
+  return reinterpret_cast<Box*>(reinterpret_cast<char*>(base) + i * box_bytes);
+}
+__device__ __forceinline__ mk_i128* box_lo(Box* b) { return reinterpret_cast<mk_i128*>(b + 1); }
+
+// incumbent test: true when the box cannot hold anything better than the
+// current incumbent (its best corner is not strictly better)
+__device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, const i128* corner) {
+  Incumbent* I = D.inc + pid;
+  unsigned v1 = *((volatile unsigned*)&I->version);
+  if (v1 & 1u) return false;
+  __threadfence();
+  int has = *((volatile int*)&I->has);
+  if (!has) return false;
+  const volatile mk_i128* B = D.best + p.var_off;
+  bool dominated = true;
+  for (int i = 0; i < p.nvars; ++i) {
+    mk_i128 t;
+    t.lo = B[i].lo;
+    t.hi = B[i].hi;
+    i128 b = mk_ld(t);
+    if (corner[i] == b) continue;
+    bool mx = (p.maxmask >> i) & 1;
+    dominated = !(mx ? corner[i] > b : corner[i] < b);
+    break;
+  }
+  __threadfence();
+  unsigned v2 = *((volatile unsigned*)&I->version);
+  if (v1 != v2) return false;
+  return dominated;
+}
+
+__device__ void inc_offer(const DevSet& D, int pid, const mk_problem& p, const i128* x) {
+  Incumbent* I = D.inc + pid;
+  while (atomicCAS(&I->lock, 0, 1) != 0) {
+  }
+  __threadfence();
+  bool better = true;
+  if (I->has) {
+    i128 cur[MK_MAXV];
+    for (int i = 0; i < p.nvars; ++i) cur[i] = mk_ld(D.best[p.var_off + i]);
+    better = mk_lex_better(x, cur, p.nvars, p.maxmask);
+  }
+  if (better) {
+    atomicAdd(&I->version, 1u);
+    __threadfence();
+    for (int i = 0; i < p.nvars; ++i) D.best[p.var_off + i] = mk_st(x[i]);
+    I->has = 1;
+    __threadfence();
+    atomicAdd(&I->version, 1u);
+  }
+  __threadfence();
+  atomicExch(&I->lock, 0);
+}
+
+__device__ __forceinline__ MkProb view(const DevSet& D, int pid) {
+  return mk_prob_view(D.probs, pid, D.insns, D.consts, D.atom_regs, D.atom_masks, D.rows,
+                      D.terms);
+}
+
+__global__ void k_roots(DevSet D, int nprob, void* stack) {
+  int pid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pid >= nprob) return;
+  const mk_problem p = D.probs[pid];
+  Box* b = box_at(stack, D.box_bytes, pid);
+  b->prob = pid;
+  mk_i128* lo = box_lo(b);
+  mk_i128* hi = lo + D.stride;
+  for (int i = 0; i < p.nvars; ++i) {
+    lo[i] = D.var_lo[p.var_off + i];
+    hi[i] = D.var_hi[p.var_off + i];
+  }
+  D.inc[pid].lock = 0;
+  D.inc[pid].version = 0;
+  D.inc[pid].has = 0;
+  D.inc[pid].err = 0;
+}
+
+__global__ void __launch_bounds__(128) k_bb(DevSet D, const void* chunk, int n, int K,
+                                            long long leaf_volume, void* child_out,
+                                            int* child_flag, void* leaf_out, int* leaf_flag,
+                                            DevStats* st) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int j = 0; j < K; ++j) child_flag[(size_t)i * K + j] = 0;
+  leaf_flag[i] = 0;
+  const Box* in = box_at(const_cast<void*>(chunk), D.box_bytes, i);
+  const int pid = in->prob;
+  const mk_problem p = D.probs[pid];
+  const int nv = p.nvars;
+  const MkProb P = view(D, pid);
+  i128 lo[MK_MAXV], hi[MK_MAXV], c[MK_MAXV];
+  const mk_i128* blo = box_lo(const_cast<Box*>(in));
+  for (int v = 0; v < nv; ++v) {
+    lo[v] = mk_ld(blo[v]);
+    hi[v] = mk_ld(blo[D.stride + v]);
+  }
+  atomicAdd(&st->boxes, 1ull);
+  mk_corner(lo, hi, nv, p.maxmask, c);
+  if (inc_dominates(D, pid, p, c)) {
+    atomicAdd(&st->covered, mk_volume_f(lo, hi, nv));
+    return;
+  }
+  double vol0 = mk_volume_f(lo, hi, nv);
+  if (!mk_contract(P, lo, hi, 4)) {
+    atomicAdd(&st->covered, vol0);
+    return;
+  }
+  MkIv R[MK_MAXR];
+  int64_t cnt = 0;
+  MkBoxVerdict v = mk_eval_box(P, lo, hi, R, &cnt);
+  atomicAdd(&st->insns_bb, (unsigned long long)cnt);
+  if (v.any_false) {
+    atomicAdd(&st->covered, vol0);
+    return;
+  }
+  if (v.all_true) {
+    mk_corner(lo, hi, nv, p.maxmask, c);
+    inc_offer(D, pid, p, c);
+    atomicAdd(&st->covered, vol0);
+    return;
+  }
+  long long vol = mk_volume(lo, hi, nv);
+  if (vol <= leaf_volume) {
+    Box* out = box_at(leaf_out, D.box_bytes, i);
+    out->prob = pid;
+    mk_i128* olo = box_lo(out);
+    for (int k = 0; k < nv; ++k) {
+      olo[k] = mk_st(lo[k]);
+      olo[D.stride + k] = mk_st(hi[k]);
+    }
+    leaf_flag[i] = 1;
+    return;
+  }
+  int sv = mk_pick_split(lo, hi, nv, v.und_mask, *((volatile int*)&D.inc[pid].has) != 0);
+  if (sv < 0) {  // every symbol of an undecided atom is fixed: saturated arithmetic
+    atomicExch(&D.inc[pid].err, 1);
+    return;
+  }
+  i128 size = hi[sv] - lo[sv] + 1;
+  int m = size < (i128)K ? (int)size : K;
+  bool mx = (p.maxmask >> sv) & 1;
+  for (int t = 0; t < m; ++t) {
+    i128 plo, phi;
+    mk_piece(lo[sv], hi[sv], m, t, mx, &plo, &phi);
+    size_t slot = (size_t)i * K + (K - 1 - t);  // best piece in the highest slot
+    Box* out = box_at(child_out, D.box_bytes, slot);
+    out->prob = pid;
+    mk_i128* olo = box_lo(out);
+    for (int k = 0; k < nv; ++k) {
+      olo[k] = mk_st(k == sv ? plo : lo[k]);
+      olo[D.stride + k] = mk_st(k == sv ? phi : hi[k]);
+    }
+    child_flag[slot] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_leaf(DevSet D, const void* leaves, int nleaf,
+                                              DevStats* st) {
+  const Box* in = box_at(const_cast<void*>(leaves), D.box_bytes, blockIdx.x);
+  const int pid = in->prob;
+  const mk_problem p = D.probs[pid];
+  const int nv = p.nvars;
+  __shared__ i128 s_lo[MK_MAXV], s_hi[MK_MAXV];
+  __shared__ unsigned long long s_best;
+  __shared__ int s_skip;
+  const mk_i128* blo = box_lo(const_cast<Box*>(in));
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    s_lo[v] = mk_ld(blo[v]);
+    s_hi[v] = mk_ld(blo[D.stride + v]);
+  }
+  if (threadIdx.x == 0) {
+    s_best = ~0ull;
+    s_skip = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    i128 c[MK_MAXV];
+    mk_corner(s_lo, s_hi, nv, p.maxmask, c);
+    if (inc_dominates(D, pid, p, c)) s_skip = 1;
+  }
+  __syncthreads();
+  const unsigned long long vol = (unsigned long long)mk_volume(s_lo, s_hi, nv);
+  if (s_skip) {
+    if (threadIdx.x == 0) {
+      atomicAdd(&st->covered, (double)vol);
+      atomicAdd(&st->leaves, 1ull);
+    }
+    return;
+  }
+  const MkProb P = view(D, pid);
+  MkCv R[MK_MAXR];
+  i128 x[MK_MAXV];
+  int64_t cnt = 0;
+  unsigned long long evaluated = 0;
+  bool ovf = false;
+  for (unsigned long long idx = threadIdx.x; idx < vol; idx += blockDim.x) {
+    if (idx > *((volatile unsigned long long*)&s_best)) break;
+    mk_decode(s_lo, s_hi, nv, p.maxmask, idx, x);
+    ++evaluated;
+    if (mk_eval_point(P, x, R, &ovf, &cnt)) {
+      atomicMin(&s_best, idx);
+      break;
+    }
+  }
+  if (ovf) atomicExch(&D.inc[pid].err, 1);
+  atomicAdd(&st->points, evaluated);
+  atomicAdd(&st->insns_leaf, (unsigned long long)cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(&st->leaves, 1ull);
+    atomicAdd(&st->covered, (double)vol);
+    if (s_best != ~0ull) {
+      mk_decode(s_lo, s_hi, nv, p.maxmask, s_best, x);
+      inc_offer(D, pid, p, x);
+    }
+  }
+}
+
+// problems that still own boxes when the budget runs out are undecided
+__global__ void k_mark_pending(DevSet D, const void* stack, long long top, int* pending) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= top) return;
+  const Box* b = box_at(const_cast<void*>(stack), D.box_bytes, (size_t)i);
+  pending[b->prob] = 1;
+}
+
+// move flagged fixed-size box records to their scanned positions; the last
+// thread also publishes the selected count
+__global__ void k_scatter(const char* src, const int* flag, const int* pos, long long n, char* dst,
+                          size_t box_bytes, int* count) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == n - 1) *count = pos[i] + flag[i];
+  if (!flag[i]) return;
+  const int4* s = reinterpret_cast<const int4*>(src + (size_t)i * box_bytes);
+  int4* d = reinterpret_cast<int4*>(dst + (size_t)pos[i] * box_bytes);
+  for (size_t w = 0; w < box_bytes / sizeof(int4); ++w) d[w] = s[w];
+}
+
+}  // namespace
+
+struct mk_ctx {
+  int device = 0;
+  std::string err;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // growable device buffers
+  void* d_set = nullptr;
+  size_t d_set_bytes = 0;
+  void* d_work = nullptr;
+  size_t d_work_bytes = 0;
+  void* h_pinned = nullptr;
+};
+
+static int fail(mk_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+#define CK(call)                                                                  \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess)                                                        \
+      return fail(ctx, MK_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+extern "C" int mk_abi_version(void) { return MK_ABI_VERSION; }
+
+extern "C" int mk_device_count(int* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) n = 0;
+  if (out) *out = n;
+  return n > 0 ? MK_OK : MK_ENODEV;
+}
+
+extern "C" int mk_ctx_create(int device, mk_ctx** out) {
+  if (!out) return MK_EINVAL;
+  *out = nullptr;
+  mk_ctx* ctx = new mk_ctx();
+  ctx->device = device;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device) {
+    delete ctx;
+    return MK_ENODEV;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return MK_ECUDA;
+  }
+  // the evaluators keep their register files in local memory
+  cudaDeviceSetLimit(cudaLimitStackSize, 32 * 1024);
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return MK_ECUDA;
+  }
+  for (int i = 0; i < 4; ++i) cudaEventCreate(&ctx->ev[i]);
+  cudaMallocHost(&ctx->h_pinned, 4096);
+  *out = ctx;
+  return MK_OK;
+}
+
+extern "C" int mk_ctx_destroy(mk_ctx* ctx) {
+  if (!ctx) return MK_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->d_set) cudaFree(ctx->d_set);
+  if (ctx->d_work) cudaFree(ctx->d_work);
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  for (int i = 0; i < 4; ++i)
+    if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return MK_OK;
+}
+
+extern "C" const char* mk_last_error(const mk_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : "null context";
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static int ensure(mk_ctx* ctx, void** buf, size_t* cap, size_t need) {
+  if (*cap >= need) return MK_OK;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  size_t want = need + need / 4;
+  cudaError_t e = cudaMalloc(buf, want);
+  if (e != cudaSuccess) {
+    *cap = 0;
+    return fail(ctx, MK_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  *cap = want;
+  return MK_OK;
+}
+
+extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_limits* lim,
+                            int32_t* status, mk_i128* point, mk_stats* stats) {
+  if (!ctx || !set || !status || !point) return fail(ctx, MK_EINVAL, "null argument");
+  auto t0 = std::chrono::steady_clock::now();
+  CK(cudaSetDevice(ctx->device));
+  mk_stats local_stats;
+  std::memset(&local_stats, 0, sizeof(local_stats));
+  const int nprob = set->nprob;
+  if (nprob <= 0) {
+    if (stats) *stats = local_stats;
+    return MK_OK;
+  }
+  int S = 1;
+  for (int i = 0; i < nprob; ++i) {
+    const mk_problem& p = set->probs[i];
+    if (p.nvars > MK_MAXV || p.nregs > MK_MAXR)
+      return fail(ctx, MK_EINVAL, "problem exceeds MK_MAXV symbols or MK_MAXR registers");
+    if (p.nvars > S) S = p.nvars;
+  }
+  int64_t max_rounds = lim && lim->max_rounds > 0 ? lim->max_rounds : 200000;
+  int64_t max_boxes = lim && lim->max_boxes > 0 ? lim->max_boxes : (int64_t)4e9;
+  double max_seconds = lim && lim->max_seconds > 0 ? lim->max_seconds : 30.0;
+  int K = lim && lim->split_k > 1 ? lim->split_k : 16;
+  int chunk = lim && lim->chunk > 0 ? lim->chunk : 65536;
+  long long leaf_volume = lim && lim->leaf_volume > 0 ? lim->leaf_volume : 4096;
+
+  // ---- upload the problem set (one contiguous device block)
+  const size_t box_bytes = sizeof(Box) + 2 * sizeof(mk_i128) * (size_t)S;
+  size_t off = 0;
+  auto place = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  size_t o_probs = place(sizeof(mk_problem) * nprob);
+  size_t o_insn = place(sizeof(mk_insn) * (size_t)set->ninsn_total + 16);
+  size_t o_const = place(sizeof(mk_i128) * (size_t)set->nconst_total + 16);
+  size_t o_ar = place(sizeof(int32_t) * (size_t)set->natom_total + 16);
+  size_t o_am = place(sizeof(uint64_t) * (size_t)set->natom_total + 16);
+  size_t o_rows = place(sizeof(mk_row) * (size_t)set->nrow_total + 16);
+  size_t o_terms = place(sizeof(mk_row_term) * (size_t)set->nterm_total + 16);
+  size_t o_vlo = place(sizeof(mk_i128) * (size_t)set->nvar_total + 16);
+  size_t o_vhi = place(sizeof(mk_i128) * (size_t)set->nvar_total + 16);
+  size_t o_best = place(sizeof(mk_i128) * (size_t)set->nvar_total + 16);
+  size_t o_inc = place(sizeof(Incumbent) * nprob);
+  size_t o_pend = place(sizeof(int) * nprob);
+  size_t o_stats = place(sizeof(DevStats));
+  size_t o_counts = place(sizeof(int) * 4);
+  size_t set_bytes = off;
+  int rc = ensure(ctx, &ctx->d_set, &ctx->d_set_bytes, set_bytes);
+  if (rc) return rc;
+  char* base = static_cast<char*>(ctx->d_set);
+  cudaStream_t s = ctx->stream;
+  auto h2d = [&](size_t o, const void* src, size_t bytes) -> cudaError_t {
+    if (!bytes || !src) return cudaSuccess;
+    return cudaMemcpyAsync(base + o, src, bytes, cudaMemcpyHostToDevice, s);
+  };
+  CK(h2d(o_probs, set->probs, sizeof(mk_problem) * nprob));
+  CK(h2d(o_insn, set->insns, sizeof(mk_insn) * (size_t)set->ninsn_total));
+  CK(h2d(o_const, set->consts, sizeof(mk_i128) * (size_t)set->nconst_total));
+  CK(h2d(o_ar, set->atom_regs, sizeof(int32_t) * (size_t)set->natom_total));
+  CK(h2d(o_am, set->atom_masks, sizeof(uint64_t) * (size_t)set->natom_total));
+  CK(h2d(o_rows, set->rows, sizeof(mk_row) * (size_t)set->nrow_total));
+  CK(h2d(o_terms, set->row_terms, sizeof(mk_row_term) * (size_t)set->nterm_total));
+  CK(h2d(o_vlo, set->var_lo, sizeof(mk_i128) * (size_t)set->nvar_total));
+  CK(h2d(o_vhi, set->var_hi, sizeof(mk_i128) * (size_t)set->nvar_total));
+  CK(cudaMemsetAsync(base + o_pend, 0, sizeof(int) * nprob, s));
+  CK(cudaMemsetAsync(base + o_stats, 0, sizeof(DevStats), s));
+
+  DevSet D;
+  D.probs = reinterpret_cast<const mk_problem*>(base + o_probs);
+  D.insns = reinterpret_cast<const mk_insn*>(base + o_insn);
+  D.consts = reinterpret_cast<const mk_i128*>(base + o_const);
+  D.atom_regs = reinterpret_cast<const int32_t*>(base + o_ar);
+  D.atom_masks = reinterpret_cast<const uint64_t*>(base + o_am);
+  D.rows = reinterpret_cast<const mk_row*>(base + o_rows);
+  D.terms = reinterpret_cast<const mk_row_term*>(base + o_terms);
+  D.var_lo = reinterpret_cast<const mk_i128*>(base + o_vlo);
+  D.var_hi = reinterpret_cast<const mk_i128*>(base + o_vhi);
+  D.inc = reinterpret_cast<Incumbent*>(base + o_inc);
+  D.best = reinterpret_cast<mk_i128*>(base + o_best);
+  D.stride = S;
+  D.box_bytes = box_bytes;
+  DevStats* d_st = reinterpret_cast<DevStats*>(base + o_stats);
+  int* d_counts = reinterpret_cast<int*>(base + o_counts);
+  int* d_pend = reinterpret_cast<int*>(base + o_pend);
+
+  // ---- work buffers: stack, child/leaf staging, flags, cub scratch
+  size_t cap_boxes = (size_t)(512u << 20) / box_bytes;  // ~512 MiB of stack
+  if (cap_boxes < (size_t)nprob + (size_t)chunk * K) cap_boxes = (size_t)nprob + (size_t)chunk * K;
+  size_t cub_bytes = 0;
+  {
+    size_t t1 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t1, (const int*)nullptr, (int*)nullptr,
+                                  (int)((size_t)chunk * K), s);
+    cub_bytes = t1;
+  }
+  size_t w = 0;
+  auto wplace = [&](size_t bytes) {
+    size_t o = w;
+    w = align_up(w + bytes, 256);
+    return o;
+  };
+  size_t w_stack = wplace(box_bytes * cap_boxes);
+  size_t w_child = wplace(box_bytes * (size_t)chunk * K);
+  size_t w_cflag = wplace(sizeof(int) * (size_t)chunk * K);
+  size_t w_cpos = wplace(sizeof(int) * (size_t)chunk * K);
+  size_t w_leaf = wplace(box_bytes * (size_t)chunk);
+  size_t w_lflag = wplace(sizeof(int) * (size_t)chunk);
+  size_t w_lpos = wplace(sizeof(int) * (size_t)chunk);
+  size_t w_leaves = wplace(box_bytes * (size_t)chunk);
+  size_t w_cub = wplace(cub_bytes + 256);
+  rc = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, w);
+  if (rc) return rc;
+  char* wb = static_cast<char*>(ctx->d_work);
+  void* stack = wb + w_stack;
+  char* child = wb + w_child;
+  int* cflag = reinterpret_cast<int*>(wb + w_cflag);
+  int* cpos = reinterpret_cast<int*>(wb + w_cpos);
+  char* leafst = wb + w_leaf;
+  int* lflag = reinterpret_cast<int*>(wb + w_lflag);
+  int* lpos = reinterpret_cast<int*>(wb + w_lpos);
+  char* leaves = wb + w_leaves;
+  void* cub_tmp = wb + w_cub;
+
+  k_roots<<<(nprob + 127) / 128, 128, 0, s>>>(D, nprob, stack);
+  CK(cudaGetLastError());
+  long long top = nprob;
+  int64_t rounds = 0;
+  double bb_ms = 0.0, leaf_ms = 0.0;
+  int* h_counts = static_cast<int*>(ctx->h_pinned);
+  bool budget_hit = false;
+  while (top > 0) {
+    double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rounds >= max_rounds || el > max_seconds) {
+      budget_hit = true;
+      break;
+    }
+    long long room = (long long)cap_boxes - top;
+    long long n = top < chunk ? top : chunk;
+    // popped n boxes free n slots; children need n*K slots
+    long long fit = (room + n) / K;
+    if (fit < n) n = fit;
+    if (n < 1) {
+      budget_hit = true;
+      break;
+    }
+    long long basei = top - n;
+    const void* chunk_ptr = static_cast<char*>(stack) + (size_t)basei * box_bytes;
+    CK(cudaEventRecord(ctx->ev[0], s));
+    int threads = 128;
+    k_bb<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
+        D, chunk_ptr, (int)n, K, leaf_volume, child, cflag, leafst, lflag, d_st);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev[1], s));
+    top = basei;
+    // compact children (order preserving) straight onto the stack top and
+    // leaves into the leaf list: exclusive scan of the flags, then scatter
+    {
+      size_t tb = cub_bytes;
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, cflag, cpos, (int)(n * K), s));
+      long long nc = n * K;
+      k_scatter<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
+          child, cflag, cpos, nc, static_cast<char*>(stack) + (size_t)top * box_bytes, box_bytes,
+          d_counts);
+      CK(cudaGetLastError());
+      tb = cub_bytes;
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, lflag, lpos, (int)n, s));
+      k_scatter<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(leafst, lflag, lpos, n, leaves,
+                                                             box_bytes, d_counts + 1);
+      CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(h_counts, d_counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    long long nchild = h_counts[0];
+    long long nleaf = h_counts[1];
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    bb_ms += ms;
+    if (nleaf > 0) {
+      CK(cudaEventRecord(ctx->ev[2], s));
+      k_leaf<<<(unsigned)nleaf, 256, 0, s>>>(D, leaves, (int)nleaf, d_st);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(ctx->ev[3], s));
+      CK(cudaEventSynchronize(ctx->ev[3]));
+      cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+      leaf_ms += ms;
+    }
+    top += nchild;
+    ++rounds;
+    (void)max_boxes;
+  }
+  if (budget_hit && top > 0) {
+    k_mark_pending<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, stack, top, d_pend);
+    CK(cudaGetLastError());
+  }
+  // ---- results
+  std::vector<Incumbent> inc(nprob);
+  std::vector<int> pend(nprob);
+  DevStats dst;
+  CK(cudaMemcpyAsync(inc.data(), D.inc, sizeof(Incumbent) * nprob, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(pend.data(), d_pend, sizeof(int) * nprob, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(point, D.best, sizeof(mk_i128) * (size_t)set->nvar_total,
+                     cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&dst, d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < nprob; ++i) {
+    if (inc[i].err || pend[i]) status[i] = MK_UNKNOWN;
+    else status[i] = inc[i].has ? MK_SAT : MK_UNSAT;
+  }
+  local_stats.rounds = rounds;
+  local_stats.boxes = (int64_t)dst.boxes;
+  local_stats.leaves = (int64_t)dst.leaves;
+  local_stats.points = (int64_t)dst.points;
+  local_stats.covered = dst.covered;
+  local_stats.insns_bb = (int64_t)dst.insns_bb;
+  local_stats.insns_leaf = (int64_t)dst.insns_leaf;
+  local_stats.bb_ms = bb_ms;
+  local_stats.leaf_ms = leaf_ms;
+  local_stats.seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (stats) *stats = local_stats;
+  return MK_OK;
+}

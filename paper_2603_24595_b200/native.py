@@ -1,0 +1,250 @@
+"""ctypes binding of ``libmk_b200.so`` (C ABI in ``include/mk_b200.h``).
+
+The product path loads ONLY the in-tree CUDA library built by
+``__graft_entry__.build()``; there is no CPU fallback.  A missing library or
+a host without a CUDA device raises :class:`NativeUnavailable`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_NAME = "libmk_b200.so"
+DEFAULT_LIB = os.path.join(HERE, LIB_NAME)
+
+MK_UNSAT, MK_SAT, MK_UNKNOWN = 0, 1, 2
+STATUS_NAME = {MK_UNSAT: "unsat", MK_SAT: "sat", MK_UNKNOWN: "unknown"}
+
+EXPORTS = ("mk_abi_version", "mk_device_count", "mk_ctx_create", "mk_ctx_destroy",
+           "mk_last_error", "mk_site_eval")
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA checking engine cannot run here."""
+
+
+# -- ABI structs (must match include/mk_b200.h) ------------------------------------
+
+I128 = np.dtype([("lo", "<u8"), ("hi", "<i8")])
+INSN = np.dtype([("op", "<u2"), ("dst", "<u2"), ("a", "<u2"), ("b", "<u2"),
+                 ("c", "<u2"), ("pad", "<u2")])
+PROBLEM = np.dtype([("nvars", "<i4"), ("ninsn", "<i4"), ("nregs", "<i4"), ("natoms", "<i4"),
+                    ("nconst", "<i4"), ("nrows", "<i4"), ("var_off", "<i4"),
+                    ("insn_off", "<i4"), ("const_off", "<i4"), ("atom_off", "<i4"),
+                    ("row_off", "<i4"), ("pad", "<i4"), ("maxmask", "<u8")])
+ROW = np.dtype([("rel", "<i4"), ("nterms", "<i4"), ("term_off", "<i4"), ("pad", "<i4"),
+                ("c0", I128)])
+ROW_TERM = np.dtype([("var", "<i4"), ("pad0", "<i4"), ("pad1", "<i8"), ("coef", I128)])
+assert PROBLEM.itemsize == 56 and INSN.itemsize == 12 and ROW.itemsize == 32
+assert ROW_TERM.itemsize == 32 and I128.itemsize == 16
+
+
+class ProblemSet(ctypes.Structure):
+    _fields_ = [("nprob", ctypes.c_int32), ("nvar_total", ctypes.c_int32),
+                ("ninsn_total", ctypes.c_int32), ("nconst_total", ctypes.c_int32),
+                ("natom_total", ctypes.c_int32), ("nrow_total", ctypes.c_int32),
+                ("nterm_total", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("probs", ctypes.c_void_p), ("var_lo", ctypes.c_void_p),
+                ("var_hi", ctypes.c_void_p), ("insns", ctypes.c_void_p),
+                ("consts", ctypes.c_void_p), ("atom_regs", ctypes.c_void_p),
+                ("atom_masks", ctypes.c_void_p), ("rows", ctypes.c_void_p),
+                ("row_terms", ctypes.c_void_p)]
+
+
+class Limits(ctypes.Structure):
+    _fields_ = [("max_rounds", ctypes.c_int64), ("max_boxes", ctypes.c_int64),
+                ("max_seconds", ctypes.c_double), ("split_k", ctypes.c_int32),
+                ("chunk", ctypes.c_int32), ("leaf_volume", ctypes.c_int64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("rounds", ctypes.c_int64), ("boxes", ctypes.c_int64),
+                ("leaves", ctypes.c_int64), ("points", ctypes.c_int64),
+                ("covered", ctypes.c_double), ("seconds", ctypes.c_double),
+                ("bb_ms", ctypes.c_double), ("leaf_ms", ctypes.c_double),
+                ("insns_bb", ctypes.c_int64), ("insns_leaf", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
+    lib.mk_abi_version.restype = ctypes.c_int
+    lib.mk_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
+    lib.mk_ctx_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+    lib.mk_ctx_destroy.argtypes = [ctypes.c_void_p]
+    lib.mk_last_error.argtypes = [ctypes.c_void_p]
+    lib.mk_last_error.restype = ctypes.c_char_p
+    lib.mk_site_eval.argtypes = [ctypes.c_void_p, ctypes.POINTER(ProblemSet),
+                                 ctypes.POINTER(Limits), ctypes.c_void_p, ctypes.c_void_p,
+                                 ctypes.POINTER(Stats)]
+    return lib
+
+
+_LIBS = {}
+
+
+def load_library(path: Optional[str] = None) -> ctypes.CDLL:
+    path = os.path.abspath(path or os.environ.get("MK_B200_LIB") or DEFAULT_LIB)
+    lib = _LIBS.get(path)
+    if lib is not None:
+        return lib
+    if not os.path.exists(path):
+        raise NativeUnavailable(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = _bind(ctypes.CDLL(path))
+    if lib.mk_abi_version() != 1:
+        raise NativeUnavailable(f"{path}: ABI version mismatch")
+    _LIBS[path] = lib
+    return lib
+
+
+# -- packing ---------------------------------------------------------------------------
+
+def _i128_array(values: Sequence[int]) -> np.ndarray:
+    a = np.zeros(len(values), dtype=I128)
+    if len(values):
+        a["lo"] = [v & 0xFFFFFFFFFFFFFFFF for v in values]
+        a["hi"] = [v >> 64 for v in values]
+    return a
+
+
+def _i128_value(lo: int, hi: int) -> int:
+    return (int(hi) << 64) | int(lo)
+
+
+class PackedSet:
+    """Host-side arrays of one ``mk_problem_set`` (kept alive while in use)."""
+
+    def __init__(self, problems) -> None:
+        self.problems = list(problems)
+        P = len(self.problems)
+        self.probs = np.zeros(P, dtype=PROBLEM)
+        lo, hi, consts, atom_regs, atom_masks = [], [], [], [], []
+        insns = []
+        rows, terms = [], []
+        for i, p in enumerate(self.problems):
+            rec = self.probs[i]
+            rec["nvars"] = p.nvars
+            rec["ninsn"] = len(p.insns)
+            rec["nregs"] = max(p.nregs, 1)
+            rec["natoms"] = len(p.atom_regs)
+            rec["nconst"] = len(p.consts)
+            rec["nrows"] = len(p.rows)
+            rec["var_off"] = len(lo)
+            rec["insn_off"] = len(insns)
+            rec["const_off"] = len(consts)
+            rec["atom_off"] = len(atom_regs)
+            rec["row_off"] = len(rows)
+            m = 0
+            for k, mx in enumerate(p.maximize):
+                if mx:
+                    m |= 1 << k
+            rec["maxmask"] = m
+            lo.extend(p.lo)
+            hi.extend(p.hi)
+            insns.extend(p.insns)
+            consts.extend(p.consts)
+            atom_regs.extend(p.atom_regs)
+            atom_masks.extend(p.atom_masks)
+            for rel, c0, tl in p.rows:
+                rows.append((rel, len(tl), len(terms), c0))
+                terms.extend(tl)
+        self.var_lo = _i128_array(lo)
+        self.var_hi = _i128_array(hi)
+        self.insns = np.zeros(len(insns), dtype=INSN)
+        if insns:
+            arr = np.asarray(insns, dtype=np.int64)
+            self.insns["op"] = arr[:, 0]
+            self.insns["dst"] = arr[:, 1]
+            self.insns["a"] = arr[:, 2]
+            self.insns["b"] = arr[:, 3]
+            self.insns["c"] = arr[:, 4]
+        self.consts = _i128_array(consts)
+        self.atom_regs = np.asarray(atom_regs, dtype=np.int32)
+        self.atom_masks = np.asarray(atom_masks, dtype=np.uint64)
+        self.rows = np.zeros(len(rows), dtype=ROW)
+        for i, (rel, nt, off, c0) in enumerate(rows):
+            self.rows[i]["rel"] = rel
+            self.rows[i]["nterms"] = nt
+            self.rows[i]["term_off"] = off
+            self.rows[i]["c0"] = (c0 & 0xFFFFFFFFFFFFFFFF, c0 >> 64)
+        self.terms = np.zeros(len(terms), dtype=ROW_TERM)
+        for i, (var, coef) in enumerate(terms):
+            self.terms[i]["var"] = var
+            self.terms[i]["coef"] = (coef & 0xFFFFFFFFFFFFFFFF, coef >> 64)
+        self.nvar_total = len(lo)
+        self.struct = ProblemSet(
+            P, len(lo), len(insns), len(consts), len(atom_regs), len(rows), len(terms), 0,
+            self.probs.ctypes.data, self.var_lo.ctypes.data, self.var_hi.ctypes.data,
+            self.insns.ctypes.data, self.consts.ctypes.data, self.atom_regs.ctypes.data,
+            self.atom_masks.ctypes.data, self.rows.ctypes.data, self.terms.ctypes.data)
+
+    def host_bytes(self) -> int:
+        return sum(a.nbytes for a in (self.probs, self.var_lo, self.var_hi, self.insns,
+                                      self.consts, self.atom_regs, self.atom_masks,
+                                      self.rows, self.terms))
+
+
+class Engine:
+    """One device context of the checking engine."""
+
+    def __init__(self, device: int = 0, lib_path: Optional[str] = None) -> None:
+        self.lib = load_library(lib_path)
+        n = ctypes.c_int(0)
+        self.lib.mk_device_count(ctypes.byref(n))
+        if n.value <= device:
+            raise NativeUnavailable(f"no CUDA device {device} (found {n.value})")
+        ctx = ctypes.c_void_p()
+        rc = self.lib.mk_ctx_create(device, ctypes.byref(ctx))
+        if rc != 0:
+            raise NativeUnavailable(f"mk_ctx_create({device}) failed: {rc}")
+        self.ctx = ctx
+        self.device = device
+        self.last_stats: Optional[dict] = None
+
+    def close(self) -> None:
+        if getattr(self, "ctx", None):
+            self.lib.mk_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def solve_packed(self, packed: PackedSet, limits: Optional[dict] = None
+                     ) -> List[Tuple[str, Optional[List[int]]]]:
+        lim = Limits(0, 0, 0.0, 0, 0, 0)
+        for k, v in (limits or {}).items():
+            setattr(lim, k, v)
+        P = len(packed.problems)
+        status = np.zeros(max(P, 1), dtype=np.int32)
+        point = np.zeros(max(packed.nvar_total, 1), dtype=I128)
+        st = Stats()
+        rc = self.lib.mk_site_eval(self.ctx, ctypes.byref(packed.struct), ctypes.byref(lim),
+                                   status.ctypes.data, point.ctypes.data, ctypes.byref(st))
+        if rc != 0:
+            msg = self.lib.mk_last_error(self.ctx)
+            raise RuntimeError(f"mk_site_eval failed ({rc}): {msg.decode() if msg else ''}")
+        self.last_stats = st.as_dict()
+        out: List[Tuple[str, Optional[List[int]]]] = []
+        for i, p in enumerate(packed.problems):
+            s = STATUS_NAME[int(status[i])]
+            if s == "sat":
+                off = int(packed.probs[i]["var_off"])
+                vals = [_i128_value(point[off + k]["lo"], point[off + k]["hi"])
+                        for k in range(p.nvars)]
+                out.append((s, vals))
+            else:
+                out.append((s, None))
+        return out
+
+    def solve(self, problems, limits: Optional[dict] = None):
+        return self.solve_packed(PackedSet(problems), limits)
