@@ -495,7 +495,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   int* d_pend = reinterpret_cast<int*>(base + o_pend);
 
   // ---- work buffers: stack, child/leaf staging, flags, cub scratch
-  size_t cap_boxes = (size_t)(512u << 20) / box_bytes;  // ~512 MiB of stack
+  size_t cap_boxes = ((size_t)4 << 30) / box_bytes;  // 4 GiB of box stack in HBM
   if (cap_boxes < (size_t)nprob + (size_t)chunk * K) cap_boxes = (size_t)nprob + (size_t)chunk * K;
   size_t cub_bytes = 0;
   {
@@ -547,8 +547,10 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
     }
     long long room = (long long)cap_boxes - top;
     long long n = top < chunk ? top : chunk;
-    // popped n boxes free n slots; children need n*K slots
-    long long fit = (room + n) / K;
+    // popping n boxes frees n slots and their children need up to n*K:
+    // n*(K-1) <= room.  A nearly full stack therefore processes fewer, deeper
+    // boxes (LIFO top), which drains it.
+    long long fit = room / (K - 1);
     if (fit < n) n = fit;
     if (n < 1) {
       budget_hit = true;
@@ -597,7 +599,14 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
     }
     top += nchild;
     ++rounds;
-    (void)max_boxes;
+    if (rounds % 64 == 0) {
+      unsigned long long nb = 0;
+      CK(cudaMemcpy(&nb, &d_st->boxes, sizeof(nb), cudaMemcpyDeviceToHost));
+      if ((int64_t)nb > max_boxes) {
+        budget_hit = true;
+        break;
+      }
+    }
   }
   if (budget_hit && top > 0) {
     k_mark_pending<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, stack, top, d_pend);

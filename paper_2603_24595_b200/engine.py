@@ -78,7 +78,11 @@ class SiteChecker:
         if packed is None:
             packed, offsets = self.pack(cqs)
         t0 = time.perf_counter()
-        results = self.engine.solve_packed(packed, self.limits) if packed.problems else []
+        # the reference grants every query its own timeout (engine/state.py:38);
+        # a batch gets the sum, capped
+        lim = dict(self.limits)
+        lim["max_seconds"] = min(self.limits["max_seconds"] * max(len(compiled), 1), 3600.0)
+        results = self.engine.solve_packed(packed, lim) if packed.problems else []
         t1 = time.perf_counter()
         out: List[QueryResult] = []
         for (cq, err), off in zip(compiled, offsets):
