@@ -48,6 +48,10 @@ struct Incumbent {
   unsigned version;
   int has;
   int err;  // inexact evaluation (saturation) or unsplittable box
+  // lexicographic key of the best offered model: each symbol's offset from
+  // its best root bound packed into bit fields in witness order (a monotone
+  // prefix of the full order when the fields exceed 64 bits)
+  unsigned long long key;
 };
 
 struct DevSet {
@@ -76,10 +80,39 @@ __device__ __forceinline__ Box* box_at(void* base, size_t box_bytes, size_t i) {
 }
 __device__ __forceinline__ mk_i128* box_lo(Box* b) { return reinterpret_cast<mk_i128*>(b + 1); }
 
+// 64-bit lexicographic key of a point (see Incumbent::key)
+__device__ unsigned long long lex_key(const DevSet& D, const mk_problem& p, const i128* x) {
+  unsigned long long key = 0;
+  int left = 64;
+  for (int i = 0; i < p.nvars && left > 0; ++i) {
+    i128 rlo = mk_ld(D.var_lo[p.var_off + i]), rhi = mk_ld(D.var_hi[p.var_off + i]);
+    u128 span = (u128)(rhi - rlo);
+    int bits = mk_bitlen(span);
+    if (bits == 0) continue;
+    u128 d = ((p.maxmask >> i) & 1) ? (u128)(rhi - x[i]) : (u128)(x[i] - rlo);
+    if (bits <= left) {
+      key = (bits == 64 ? 0ull : (key << bits)) | (unsigned long long)d;
+      left -= bits;
+    } else {  // keep the top `left` bits of this field, then stop
+      key = (key << left) | (unsigned long long)(d >> (bits - left));
+      left = 0;
+    }
+  }
+  if (left > 0 && left < 64) key <<= left;
+  return key;
+}
+
 // incumbent test: true when the box cannot hold anything better than the
 // current incumbent (its best corner is not strictly better)
 __device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, const i128* corner) {
   Incumbent* I = D.inc + pid;
+  {
+    unsigned long long kmin = *((volatile unsigned long long*)&I->key);
+    if (kmin != ~0ull) {
+      unsigned long long k = lex_key(D, p, corner);
+      if (k > kmin) return true;   // a strictly better model was offered
+    }
+  }
   unsigned v1 = *((volatile unsigned*)&I->version);
   if (v1 & 1u) return false;
   __threadfence();
@@ -105,7 +138,18 @@ __device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, con
 
 __device__ void inc_offer(const DevSet& D, int pid, const mk_problem& p, const i128* x) {
   Incumbent* I = D.inc + pid;
+  // lock-free filter: a candidate whose key prefix is worse than the best
+  // offered key loses without touching the lock
+  {
+    unsigned long long k = lex_key(D, p, x);
+    unsigned long long old = atomicMin(&I->key, k);
+    if (k > old) return;
+  }
+  if (inc_dominates(D, pid, p, x)) return;
+  unsigned ns = 32;
   while (atomicCAS(&I->lock, 0, 1) != 0) {
+    __nanosleep(ns);
+    if (ns < 2048) ns <<= 1;
   }
   __threadfence();
   bool better = true;
@@ -147,6 +191,142 @@ __global__ void k_roots(DevSet D, int nprob, void* stack) {
   D.inc[pid].version = 0;
   D.inc[pid].has = 0;
   D.inc[pid].err = 0;
+  D.inc[pid].key = ~0ull;
+}
+
+// ---------------------------------------------------------------------------
+// per-box step shared by the round kernel (k_bb) and the persistent search
+// kernel (k_search)
+
+enum { ACT_DONE = 0, ACT_LEAF = 1, ACT_SPLIT = 2 };
+
+struct Act {
+  int kind;
+  int sv;  // split symbol
+  int m;   // number of children
+};
+
+// lo/hi: the box (contracted in place).  Prunes, accepts the best corner of an
+// all-true box, hands small boxes to enumeration, or chooses a split.
+__device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, i128* lo, i128* hi,
+                           int K, long long leaf_volume, DevStats* st) {
+  const int nv = p.nvars;
+  const MkProb P = view(D, pid);
+  Act a;
+  a.kind = ACT_DONE;
+  a.sv = -1;
+  a.m = 0;
+  i128 c[MK_MAXV];
+  atomicAdd(&st->boxes, 1ull);
+  mk_corner(lo, hi, nv, p.maxmask, c);
+  double vol0 = mk_volume_f(lo, hi, nv);
+  if (inc_dominates(D, pid, p, c)) {
+    atomicAdd(&st->covered, vol0);
+    return a;
+  }
+  if (!mk_contract(P, lo, hi, 4)) {
+    atomicAdd(&st->covered, vol0);
+    return a;
+  }
+  MkIv R[MK_MAXR];
+  int64_t cnt = 0;
+  MkBoxVerdict v = mk_eval_box(P, lo, hi, R, &cnt);
+  atomicAdd(&st->insns_bb, (unsigned long long)cnt);
+  if (v.any_false) {
+    atomicAdd(&st->covered, vol0);
+    return a;
+  }
+  if (v.all_true) {
+    mk_corner(lo, hi, nv, p.maxmask, c);
+    inc_offer(D, pid, p, c);
+    atomicAdd(&st->covered, vol0);
+    return a;
+  }
+  if (mk_volume(lo, hi, nv) <= leaf_volume) {
+    a.kind = ACT_LEAF;
+    return a;
+  }
+  int sv = mk_pick_split(lo, hi, nv, v.und_mask, *((volatile int*)&D.inc[pid].has) != 0);
+  if (sv < 0) {  // every symbol of an undecided atom is fixed: saturated arithmetic
+    atomicExch(&D.inc[pid].err, 1);
+    return a;
+  }
+  i128 size = hi[sv] - lo[sv] + 1;
+  a.kind = ACT_SPLIT;
+  a.sv = sv;
+  a.m = size < (i128)K ? (int)size : K;
+  return a;
+}
+
+__device__ __forceinline__ void write_box(Box* out, int pid, const i128* lo, const i128* hi,
+                                          int nv, int stride, int sv, i128 plo, i128 phi) {
+  out->prob = pid;
+  mk_i128* olo = box_lo(out);
+  for (int k = 0; k < nv; ++k) {
+    olo[k] = mk_st(k == sv ? plo : lo[k]);
+    olo[stride + k] = mk_st(k == sv ? phi : hi[k]);
+  }
+}
+
+__device__ __forceinline__ void load_box(const Box* in, int nv, int stride, i128* lo, i128* hi) {
+  const mk_i128* blo = box_lo(const_cast<Box*>(in));
+  for (int v = 0; v < nv; ++v) {
+    lo[v] = mk_ld(blo[v]);
+    hi[v] = mk_ld(blo[stride + v]);
+  }
+}
+
+// Exhaustive enumeration of one small box by the whole CTA: every instance in
+// lexicographic index order (== witness order), each thread stops at its
+// first model, CTA min of the index, incumbent update.  s_lo/s_hi in shared.
+__device__ void cta_enumerate(const DevSet& D, int pid, const mk_problem& p, const i128* s_lo,
+                              const i128* s_hi, unsigned long long* s_best, int* s_skip,
+                              DevStats* st) {
+  const int nv = p.nvars;
+  if (threadIdx.x == 0) {
+    *s_best = ~0ull;
+    i128 c[MK_MAXV];
+    mk_corner(s_lo, s_hi, nv, p.maxmask, c);
+    *s_skip = inc_dominates(D, pid, p, c) ? 1 : 0;
+  }
+  __syncthreads();
+  const unsigned long long vol = (unsigned long long)mk_volume(s_lo, s_hi, nv);
+  if (*s_skip) {
+    if (threadIdx.x == 0) {
+      atomicAdd(&st->covered, (double)vol);
+      atomicAdd(&st->leaves, 1ull);
+    }
+    __syncthreads();
+    return;
+  }
+  const MkProb P = view(D, pid);
+  MkCv R[MK_MAXR];
+  i128 x[MK_MAXV];
+  int64_t cnt = 0;
+  unsigned long long evaluated = 0;
+  bool ovf = false;
+  for (unsigned long long idx = threadIdx.x; idx < vol; idx += blockDim.x) {
+    if (idx > *((volatile unsigned long long*)s_best)) break;
+    mk_decode(s_lo, s_hi, nv, p.maxmask, idx, x);
+    ++evaluated;
+    if (mk_eval_point(P, x, R, &ovf, &cnt)) {
+      atomicMin(s_best, idx);
+      break;
+    }
+  }
+  if (ovf) atomicExch(&D.inc[pid].err, 1);
+  atomicAdd(&st->points, evaluated);
+  atomicAdd(&st->insns_leaf, (unsigned long long)cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd(&st->leaves, 1ull);
+    atomicAdd(&st->covered, (double)vol);
+    if (*s_best != ~0ull) {
+      mk_decode(s_lo, s_hi, nv, p.maxmask, *s_best, x);
+      inc_offer(D, pid, p, x);
+    }
+  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(128) k_bb(DevSet D, const void* chunk, int n, int K,
@@ -161,70 +341,21 @@ __global__ void __launch_bounds__(128) k_bb(DevSet D, const void* chunk, int n, 
   const int pid = in->prob;
   const mk_problem p = D.probs[pid];
   const int nv = p.nvars;
-  const MkProb P = view(D, pid);
-  i128 lo[MK_MAXV], hi[MK_MAXV], c[MK_MAXV];
-  const mk_i128* blo = box_lo(const_cast<Box*>(in));
-  for (int v = 0; v < nv; ++v) {
-    lo[v] = mk_ld(blo[v]);
-    hi[v] = mk_ld(blo[D.stride + v]);
-  }
-  atomicAdd(&st->boxes, 1ull);
-  mk_corner(lo, hi, nv, p.maxmask, c);
-  if (inc_dominates(D, pid, p, c)) {
-    atomicAdd(&st->covered, mk_volume_f(lo, hi, nv));
-    return;
-  }
-  double vol0 = mk_volume_f(lo, hi, nv);
-  if (!mk_contract(P, lo, hi, 4)) {
-    atomicAdd(&st->covered, vol0);
-    return;
-  }
-  MkIv R[MK_MAXR];
-  int64_t cnt = 0;
-  MkBoxVerdict v = mk_eval_box(P, lo, hi, R, &cnt);
-  atomicAdd(&st->insns_bb, (unsigned long long)cnt);
-  if (v.any_false) {
-    atomicAdd(&st->covered, vol0);
-    return;
-  }
-  if (v.all_true) {
-    mk_corner(lo, hi, nv, p.maxmask, c);
-    inc_offer(D, pid, p, c);
-    atomicAdd(&st->covered, vol0);
-    return;
-  }
-  long long vol = mk_volume(lo, hi, nv);
-  if (vol <= leaf_volume) {
-    Box* out = box_at(leaf_out, D.box_bytes, i);
-    out->prob = pid;
-    mk_i128* olo = box_lo(out);
-    for (int k = 0; k < nv; ++k) {
-      olo[k] = mk_st(lo[k]);
-      olo[D.stride + k] = mk_st(hi[k]);
-    }
+  i128 lo[MK_MAXV], hi[MK_MAXV];
+  load_box(in, nv, D.stride, lo, hi);
+  Act a = process_box(D, pid, p, lo, hi, K, leaf_volume, st);
+  if (a.kind == ACT_LEAF) {
+    write_box(box_at(leaf_out, D.box_bytes, i), pid, lo, hi, nv, D.stride, -1, 0, 0);
     leaf_flag[i] = 1;
-    return;
-  }
-  int sv = mk_pick_split(lo, hi, nv, v.und_mask, *((volatile int*)&D.inc[pid].has) != 0);
-  if (sv < 0) {  // every symbol of an undecided atom is fixed: saturated arithmetic
-    atomicExch(&D.inc[pid].err, 1);
-    return;
-  }
-  i128 size = hi[sv] - lo[sv] + 1;
-  int m = size < (i128)K ? (int)size : K;
-  bool mx = (p.maxmask >> sv) & 1;
-  for (int t = 0; t < m; ++t) {
-    i128 plo, phi;
-    mk_piece(lo[sv], hi[sv], m, t, mx, &plo, &phi);
-    size_t slot = (size_t)i * K + (K - 1 - t);  // best piece in the highest slot
-    Box* out = box_at(child_out, D.box_bytes, slot);
-    out->prob = pid;
-    mk_i128* olo = box_lo(out);
-    for (int k = 0; k < nv; ++k) {
-      olo[k] = mk_st(k == sv ? plo : lo[k]);
-      olo[D.stride + k] = mk_st(k == sv ? phi : hi[k]);
+  } else if (a.kind == ACT_SPLIT) {
+    bool mx = (p.maxmask >> a.sv) & 1;
+    for (int t = 0; t < a.m; ++t) {
+      i128 plo, phi;
+      mk_piece(lo[a.sv], hi[a.sv], a.m, t, mx, &plo, &phi);
+      size_t slot = (size_t)i * K + (K - 1 - t);  // best piece in the highest slot
+      write_box(box_at(child_out, D.box_bytes, slot), pid, lo, hi, nv, D.stride, a.sv, plo, phi);
+      child_flag[slot] = 1;
     }
-    child_flag[slot] = 1;
   }
 }
 
@@ -242,51 +373,158 @@ __global__ void __launch_bounds__(256) k_leaf(DevSet D, const void* leaves, int 
     s_lo[v] = mk_ld(blo[v]);
     s_hi[v] = mk_ld(blo[D.stride + v]);
   }
-  if (threadIdx.x == 0) {
-    s_best = ~0ull;
-    s_skip = 0;
-  }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    i128 c[MK_MAXV];
-    mk_corner(s_lo, s_hi, nv, p.maxmask, c);
-    if (inc_dominates(D, pid, p, c)) s_skip = 1;
-  }
-  __syncthreads();
-  const unsigned long long vol = (unsigned long long)mk_volume(s_lo, s_hi, nv);
-  if (s_skip) {
-    if (threadIdx.x == 0) {
-      atomicAdd(&st->covered, (double)vol);
-      atomicAdd(&st->leaves, 1ull);
+  cta_enumerate(D, pid, p, s_lo, s_hi, &s_best, &s_skip, st);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_stamp(unsigned long long* out) { *out = globaltimer_ns(); }
+
+// Persistent search: each CTA takes tasks (pre-split boxes, best first) and
+// runs a 128-wide best-first DFS from its own HBM stack: pop the top n boxes,
+// one per thread, process, block-scan the children counts, write children in
+// lexicographic order (best on top), enumerate leaves CTA-wide; repeat until
+// the stack is empty.  Incumbents are shared across CTAs through the seqlock.
+#define SEARCH_THREADS 128
+// control block: [0] task counter, [1] idle CTAs, [2] dumped boxes,
+//                [4..5] start stamp (u64)
+__global__ void __launch_bounds__(SEARCH_THREADS) k_search(
+    DevSet D, const void* tasks, int ntasks, int* ctl, void* stacks, long long cap,
+    void* leafbuf, int K, long long leaf_volume, unsigned long long budget_ns,
+    unsigned long long slice_ns, void* dump, long long dump_cap, int* pending, DevStats* st) {
+  typedef cub::BlockScan<int, SEARCH_THREADS> Scan;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int s_task, s_abort, s_dump;
+  __shared__ long long s_top, s_dump_off;
+  __shared__ int s_nleaf;
+  __shared__ i128 s_lo[MK_MAXV], s_hi[MK_MAXV];
+  __shared__ unsigned long long s_best;
+  __shared__ int s_skip;
+  const unsigned long long t_start = *reinterpret_cast<const unsigned long long*>(ctl + 4);
+  const unsigned long long deadline_ns = t_start + budget_ns;
+  const int grid = gridDim.x;
+  char* my_stack = static_cast<char*>(stacks) + (size_t)blockIdx.x * (size_t)cap * D.box_bytes;
+  char* my_leaves = static_cast<char*>(leafbuf) + (size_t)blockIdx.x * SEARCH_THREADS * D.box_bytes;
+  const int t = threadIdx.x;
+  const size_t words = D.box_bytes / sizeof(int4);
+  for (;;) {
+    if (t == 0) s_task = atomicAdd(ctl, 1);
+    __syncthreads();
+    const int task = s_task;
+    if (task >= ntasks) {
+      if (t == 0) atomicAdd(ctl + 1, 1);  // idle from now on
+      return;
     }
-    return;
-  }
-  const MkProb P = view(D, pid);
-  MkCv R[MK_MAXR];
-  i128 x[MK_MAXV];
-  int64_t cnt = 0;
-  unsigned long long evaluated = 0;
-  bool ovf = false;
-  for (unsigned long long idx = threadIdx.x; idx < vol; idx += blockDim.x) {
-    if (idx > *((volatile unsigned long long*)&s_best)) break;
-    mk_decode(s_lo, s_hi, nv, p.maxmask, idx, x);
-    ++evaluated;
-    if (mk_eval_point(P, x, R, &ovf, &cnt)) {
-      atomicMin(&s_best, idx);
-      break;
+    // tasks are taken best-first: the top of the task stack
+    const Box* tb = box_at(const_cast<void*>(tasks), D.box_bytes, (size_t)(ntasks - 1 - task));
+    const int pid = tb->prob;
+    const mk_problem p = D.probs[pid];
+    const int nv = p.nvars;
+    {
+      const int4* src = reinterpret_cast<const int4*>(tb);
+      int4* dst = reinterpret_cast<int4*>(my_stack);
+      for (size_t w = t; w < words; w += SEARCH_THREADS) dst[w] = src[w];
     }
-  }
-  if (ovf) atomicExch(&D.inc[pid].err, 1);
-  atomicAdd(&st->points, evaluated);
-  atomicAdd(&st->insns_leaf, (unsigned long long)cnt);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicAdd(&st->leaves, 1ull);
-    atomicAdd(&st->covered, (double)vol);
-    if (s_best != ~0ull) {
-      mk_decode(s_lo, s_hi, nv, p.maxmask, s_best, x);
-      inc_offer(D, pid, p, x);
+    if (t == 0) {
+      s_top = 1;
+      s_abort = globaltimer_ns() > deadline_ns ? 1 : 0;
+      s_dump = 0;
     }
+    __syncthreads();
+    if (s_abort) {
+      if (t == 0) pending[pid] = 1;
+      __syncthreads();
+      continue;
+    }
+    while (s_top > 0) {
+      long long top = s_top;
+      long long room = cap - top;
+      long long n = top < SEARCH_THREADS ? top : SEARCH_THREADS;
+      long long fit = room / (K - 1);
+      if (fit < n) n = fit;
+      if (n < 1) {  // stack full: give up on this task honestly
+        if (t == 0) atomicExch(&D.inc[pid].err, 1);
+        break;
+      }
+      const long long base = top - n;
+      i128 lo[MK_MAXV], hi[MK_MAXV];
+      Act a;
+      a.kind = ACT_DONE;
+      a.m = 0;
+      a.sv = -1;
+      if (t < n) {
+        load_box(box_at(my_stack, D.box_bytes, (size_t)(base + t)), nv, D.stride, lo, hi);
+        a = process_box(D, pid, p, lo, hi, K, leaf_volume, st);
+      }
+      int nch = a.kind == ACT_SPLIT ? a.m : 0;
+      int isleaf = a.kind == ACT_LEAF ? 1 : 0;
+      int coff, ctot, loff, ltot;
+      Scan(scan_tmp).ExclusiveSum(nch, coff, ctot);
+      __syncthreads();
+      Scan(scan_tmp).ExclusiveSum(isleaf, loff, ltot);
+      __syncthreads();  // every popped box has been read: its slot may be reused
+      if (nch) {
+        bool mx = (p.maxmask >> a.sv) & 1;
+        for (int j = 0; j < a.m; ++j) {
+          i128 plo, phi;
+          mk_piece(lo[a.sv], hi[a.sv], a.m, a.m - 1 - j, mx, &plo, &phi);  // worst first
+          write_box(box_at(my_stack, D.box_bytes, (size_t)(base + coff + j)), pid, lo, hi, nv,
+                    D.stride, a.sv, plo, phi);
+        }
+      }
+      if (isleaf) write_box(box_at(my_leaves, D.box_bytes, loff), pid, lo, hi, nv, D.stride, -1, 0, 0);
+      if (t == 0) {
+        s_top = base + ctot;
+        s_nleaf = ltot;
+        unsigned long long now = globaltimer_ns();
+        if (now > deadline_ns) s_abort = 1;
+        // hand the remaining subtrees back when a quarter of the grid idles
+        int idle = *((volatile int*)(ctl + 1));
+        if (s_top > 0 && idle * 4 >= grid && now > t_start + slice_ns) s_dump = 1;
+      }
+      __syncthreads();
+      for (int l = 0; l < s_nleaf; ++l) {
+        const Box* lb = box_at(my_leaves, D.box_bytes, l);
+        for (int v = t; v < nv; v += SEARCH_THREADS) {
+          s_lo[v] = mk_ld(box_lo(const_cast<Box*>(lb))[v]);
+          s_hi[v] = mk_ld(box_lo(const_cast<Box*>(lb))[D.stride + v]);
+        }
+        __syncthreads();
+        cta_enumerate(D, pid, p, s_lo, s_hi, &s_best, &s_skip, st);
+      }
+      if (s_abort) {
+        if (t == 0 && s_top > 0) pending[pid] = 1;
+        break;
+      }
+      if (s_dump) {
+        if (t == 0) {
+          long long off = atomicAdd(reinterpret_cast<unsigned long long*>(ctl + 2),
+                                    (unsigned long long)s_top);
+          s_dump_off = off;
+          if (off + s_top > dump_cap) {
+            atomicExch(&D.inc[pid].err, 1);
+            s_dump_off = -1;
+          }
+        }
+        __syncthreads();
+        if (s_dump_off >= 0) {
+          const int4* src = reinterpret_cast<const int4*>(my_stack);
+          int4* dst = reinterpret_cast<int4*>(static_cast<char*>(dump) +
+                                              (size_t)s_dump_off * D.box_bytes);
+          size_t total = (size_t)s_top * words;
+          for (size_t w = t; w < total; w += SEARCH_THREADS) dst[w] = src[w];
+        }
+        __syncthreads();
+        break;
+      }
+    }
+    __syncthreads();
+    if (s_dump) return;  // this launch ends; the host redistributes the dump
   }
 }
 
@@ -315,6 +553,7 @@ __global__ void k_scatter(const char* src, const int* flag, const int* pos, long
 
 struct mk_ctx {
   int device = 0;
+  int search_ctas = 148;
   std::string err;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -370,6 +609,13 @@ extern "C" int mk_ctx_create(int device, mk_ctx** out) {
   }
   for (int i = 0; i < 4; ++i) cudaEventCreate(&ctx->ev[i]);
   cudaMallocHost(&ctx->h_pinned, 4096);
+  {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, SEARCH_THREADS, 0);
+    if (per_sm < 1) per_sm = 1;
+    ctx->search_ctas = sms * per_sm;
+  }
   *out = ctx;
   return MK_OK;
 }
@@ -495,7 +741,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   int* d_pend = reinterpret_cast<int*>(base + o_pend);
 
   // ---- work buffers: stack, child/leaf staging, flags, cub scratch
-  size_t cap_boxes = ((size_t)4 << 30) / box_bytes;  // 4 GiB of box stack in HBM
+  size_t cap_boxes = ((size_t)3 << 30) / box_bytes;  // 3 GiB of box stack in HBM
   if (cap_boxes < (size_t)nprob + (size_t)chunk * K) cap_boxes = (size_t)nprob + (size_t)chunk * K;
   size_t cub_bytes = 0;
   {
@@ -519,6 +765,18 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   size_t w_lpos = wplace(sizeof(int) * (size_t)chunk);
   size_t w_leaves = wplace(box_bytes * (size_t)chunk);
   size_t w_cub = wplace(cub_bytes + 256);
+  // persistent search: per-CTA stacks and leaf lists
+  const int grid_max = ctx->search_ctas;
+  long long cta_cap = (long long)(((size_t)6 << 30) / ((size_t)grid_max * box_bytes));
+  if (cta_cap > 65536) cta_cap = 65536;
+  if (cta_cap < 4 * SEARCH_THREADS) cta_cap = 4 * SEARCH_THREADS;
+  size_t w_cstack = wplace(box_bytes * (size_t)cta_cap * grid_max);
+  size_t w_cleaf = wplace(box_bytes * (size_t)SEARCH_THREADS * grid_max);
+  size_t w_tctr = wplace(sizeof(int) * 8);
+  // redistribution buffer: the dump of one launch is the task list of the
+  // next; it alternates with the pre-split stack (both cap_boxes)
+  size_t w_dump = wplace(box_bytes * cap_boxes);
+  const long long dump_cap = (long long)cap_boxes;
   rc = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, w);
   if (rc) return rc;
   char* wb = static_cast<char*>(ctx->d_work);
@@ -531,6 +789,12 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   int* lpos = reinterpret_cast<int*>(wb + w_lpos);
   char* leaves = wb + w_leaves;
   void* cub_tmp = wb + w_cub;
+  void* cta_stacks = wb + w_cstack;
+  void* cta_leaves = wb + w_cleaf;
+  int* ctl = reinterpret_cast<int*>(wb + w_tctr);
+  void* cta_dump = wb + w_dump;
+  // pre-split until every CTA of the persistent search has a task
+  const long long presplit_target = lim && lim->chunk < 0 ? 0 : (long long)grid_max;
 
   k_roots<<<(nprob + 127) / 128, 128, 0, s>>>(D, nprob, stack);
   CK(cudaGetLastError());
@@ -545,6 +809,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
       budget_hit = true;
       break;
     }
+    if (top >= presplit_target) break;  // hand over to the persistent search
     long long room = (long long)cap_boxes - top;
     long long n = top < chunk ? top : chunk;
     // popping n boxes frees n slots and their children need up to n*K:
@@ -608,6 +873,49 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
       }
     }
   }
+  double search_ms = 0.0;
+  int launches = 0;
+  void* tasks_buf = stack;
+  void* dump_buf = cta_dump;
+  while (!budget_hit && top > 0) {
+    double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    double left = max_seconds - el;
+    if (left <= 0) {
+      budget_hit = true;
+      break;
+    }
+    // the wall budget is checked on the device against %globaltimer, stamped
+    // stream-ordered just before the launch
+    CK(cudaMemsetAsync(ctl, 0, sizeof(int) * 8, s));
+    k_stamp<<<1, 1, 0, s>>>(reinterpret_cast<unsigned long long*>(ctl + 4));
+    // always the full persistent grid: CTAs without a task idle at once,
+    // which is what triggers redistribution of a lone deep subtree
+    int grid = grid_max;
+    CK(cudaEventRecord(ctx->ev[0], s));
+    k_search<<<grid, SEARCH_THREADS, 0, s>>>(
+        D, tasks_buf, (int)top, ctl, cta_stacks, cta_cap, cta_leaves, K, leaf_volume,
+        (unsigned long long)(left * 1e9), (unsigned long long)200000, dump_buf, dump_cap,
+        d_pend, d_st);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev[1], s));
+    long long dumped = 0;
+    CK(cudaMemcpyAsync(&dumped, ctl + 2, sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    CK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    search_ms += ms;
+    ++launches;
+    top = dumped;
+    void* tmp = tasks_buf;
+    tasks_buf = dump_buf;
+    dump_buf = tmp;
+  }
+  if (budget_hit && top > 0 && tasks_buf != stack) {
+    k_mark_pending<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, tasks_buf, top, d_pend);
+    CK(cudaGetLastError());
+    top = 0;
+  }
   if (budget_hit && top > 0) {
     k_mark_pending<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, stack, top, d_pend);
     CK(cudaGetLastError());
@@ -626,14 +934,14 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
     if (inc[i].err || pend[i]) status[i] = MK_UNKNOWN;
     else status[i] = inc[i].has ? MK_SAT : MK_UNSAT;
   }
-  local_stats.rounds = rounds;
+  local_stats.rounds = rounds + launches;
   local_stats.boxes = (int64_t)dst.boxes;
   local_stats.leaves = (int64_t)dst.leaves;
   local_stats.points = (int64_t)dst.points;
   local_stats.covered = dst.covered;
   local_stats.insns_bb = (int64_t)dst.insns_bb;
   local_stats.insns_leaf = (int64_t)dst.insns_leaf;
-  local_stats.bb_ms = bb_ms;
+  local_stats.bb_ms = bb_ms + search_ms;
   local_stats.leaf_ms = leaf_ms;
   local_stats.seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
