@@ -752,7 +752,8 @@ class _Presolve:
             if lf is None or len(lf[0]) != 1:
                 continue
             (k, c1), = lf[0].items()
-            if isinstance(k, str) or k[0] != "b" or k[1] != "emod" or abs(c1) != 1:
+            if isinstance(k, str) or k[0] != "b" or k[1] != "emod" or abs(c1) != 1 \
+                    or k[3][0] != "c":
                 continue
             m = k[3][1]
             r = -lf[1] * c1

@@ -90,7 +90,7 @@ _LIBS = {}
 
 
 def load_library(path: Optional[str] = None) -> ctypes.CDLL:
-    path = os.path.abspath(path or os.environ.get("MK_B200_LIB") or DEFAULT_LIB)
+    path = os.path.abspath(path or DEFAULT_LIB)
     lib = _LIBS.get(path)
     if lib is not None:
         return lib

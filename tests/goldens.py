@@ -9,7 +9,10 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def workloads():
-    return sorted(f[:-5] for f in os.listdir(GOLDEN) if f.endswith(".json"))
+    """Golden workloads recorded from the reference front end (kernel.mk +
+    ctx.json under workloads/); random_small.json has its own format."""
+    return sorted(f[:-5] for f in os.listdir(GOLDEN)
+                  if f.endswith(".json") and not f.startswith("random"))
 
 
 def load(name):

@@ -1,0 +1,45 @@
+"""End-to-end drop-in parity: the reference's own analyze() with its checking
+stage swapped for GpuDetectors must produce the reference's findings array
+bit for bit (engine/report.py:41-51, :109-140)."""
+import os
+
+import pytest
+
+from goldens import load, workloads
+from refpath import ROOT, add_reference, analyze_workload
+
+HAVE_REF = add_reference()
+EMU = os.path.join(ROOT, "tests", "emu", "libmk_emu.so")
+
+
+def _run(name, checker):
+    from paper_2603_24595_b200.detectors import install, uninstall
+
+    prev = install(checker=checker)
+    try:
+        return analyze_workload(name)
+    finally:
+        uninstall(prev)
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference front end not available")
+@pytest.mark.parametrize("name", ["racy", "rms_norm", "fused_add_rms_norm"])
+def test_dropin_emulated(name):
+    from paper_2603_24595_b200.engine import SiteChecker
+
+    chk = SiteChecker(lib_path=EMU)
+    doc = _run(name, chk)
+    assert doc["findings"] == load(name)["findings"]
+    assert doc["coverage"] == "complete"
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not HAVE_REF, reason="reference front end not available")
+@pytest.mark.parametrize("name", workloads())
+def test_dropin_gpu(name):
+    from paper_2603_24595_b200.engine import SiteChecker
+
+    chk = SiteChecker(device=0)
+    doc = _run(name, chk)
+    assert doc["findings"] == load(name)["findings"]
+    assert doc["coverage"] == "complete"
