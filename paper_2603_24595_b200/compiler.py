@@ -40,7 +40,7 @@ from dataclasses import dataclass, field
 from fractions import Fraction
 from typing import Callable, Dict, List, Optional, Sequence, Set, Tuple
 
-from . import ir
+from . import ir, refmirror
 from .ir import Node
 from .order import optimization_order
 
@@ -1321,16 +1321,15 @@ def compile_query(assertions: Sequence[Node],
     free_default: Dict[str, int] = {}
     seen_syms: Set[str] = set()
 
+    entailed = refmirror.entailed_bounds(simplified)
     for comp in _components(simplified):
         csyms: Dict[str, str] = {}
         for a in comp:
             ir.symbols_of(a, csyms)
         seen_syms |= set(csyms)
-        reason = None
-        for a in comp:
-            reason = _component_unsupported(a)
-            if reason:
-                break
+        # the reference gives up on the whole component when its division
+        # rewrite or path expansion raises (solver/builtin.py:805-811)
+        reason = refmirror.component_giveup(comp, entailed)
         if reason:
             groups.append(Group("unknown", reason, True))
             continue
