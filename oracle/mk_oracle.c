@@ -13,7 +13,9 @@
  *   eval_node        sym/expr.py:332-383  evaluate(..., "mathematical")
  *                    sym/expr.py:273-319  _trunc_div/_trunc_mod/_euclid_mod/
  *                                         _shift_amount/_apply_binop
- *   is_model         solver/query.py:45-62 validate_model
+ *   is_model         solver/query.py:45-62 validate_model, plus the top-level
+ *                    "symbolic divisor != 0" side constraints of
+ *                    solver/linear.py:184-259 (rewrite_divs)
  *   mko_lexmin       engine/report.py:147-203 canonicalize_witness + the
  *                    solver/interface.py:112-187 bisection, whose exact
  *                    result is the lexicographic optimum in
@@ -250,10 +252,29 @@ static int eval_node(const Node* n, const i128* x, i128* out) {
   return E_WIDE;
 }
 
+/* Symbolic divisors anywhere in the query: the reference's division rewrite
+ * (solver/linear.py:184-259) states "divisor >= 1 or divisor <= -1" as a
+ * top-level side constraint, so a point with any zero symbolic divisor is
+ * never a model, even when short-circuit evaluation would skip it. */
+static Node* g_divs[4096];
+static int g_ndivs;
+static void collect_divisors(Node* n) {
+  if (n->kind == N_BIN && (n->op == B_DIV || n->op == B_MOD || n->op == B_EMOD) &&
+      n->args[1]->kind != N_CONST && g_ndivs < 4096)
+    g_divs[g_ndivs++] = n->args[1];
+  for (int i = 0; i < n->nargs; ++i) collect_divisors(n->args[i]);
+}
+
 /* validate_model (solver/query.py:45-62): symbols inside their widths (the
  * enumeration box is clipped to them by the caller), every assertion truthy,
  * any EvalError -> not a model. */
 static int is_model(Node** as, int na, const i128* x, int* wide) {
+  for (int i = 0; i < g_ndivs; ++i) {
+    i128 v;
+    int e = eval_node(g_divs[i], x, &v);
+    if (e == E_WIDE) { *wide = 1; return 0; }
+    if (e == E_RAISE || v == 0) return 0;
+  }
   for (int i = 0; i < na; ++i) {
     i128 v;
     int e = eval_node(as[i], x, &v);
@@ -298,6 +319,8 @@ int mko_lexmin(const char* text, int n, const char* const* names, const int* max
     as[na++] = parse(&P);
     if (P.err) return -1;
   }
+  g_ndivs = 0;
+  for (int i = 0; i < na; ++i) collect_divisors(as[i]);
   i128 lo[256], hi[256], x[256];
   unsigned __int128 vol = 1;
   for (int i = 0; i < n; ++i) {

@@ -425,6 +425,20 @@ def _nnf(e: Node, neg: bool, flags: Dict[str, bool]) -> Node:
     raise CompileError(f"cannot assert a {t} node")
 
 
+def _symbolic_divisors(nodes) -> List[Node]:
+    out: List[Node] = []
+    seen: Set[Node] = set()
+    stack = list(nodes)
+    while stack:
+        e = stack.pop()
+        if e[0] == "b" and e[1] in ("div", "mod", "emod") and e[3][0] != "c":
+            if e[3] not in seen:
+                seen.add(e[3])
+                out.append(e[3])
+        stack.extend(ir.children(e))
+    return out
+
+
 def _may_err(e: Node) -> bool:
     """True when evaluating ``e`` can raise (symbolic or zero divisor)."""
     if e[0] == "b" and e[1] in ("div", "mod", "emod"):
@@ -1336,6 +1350,12 @@ def compile_query(assertions: Sequence[Node],
         flags = {"unsupported": False}
         try:
             atoms = [ir.simplify(_nnf(a, False, flags)) for a in comp]
+            # the reference's division rewrite adds its case split for a
+            # symbolic divisor as a top-level side constraint, so no model of
+            # the component has a zero divisor anywhere, even inside an
+            # operand a short-circuit would skip (solver/linear.py:5-10,
+            # :184-259)
+            atoms.extend(("p", "ne", d, ("c", 0, ir.width_of(d))) for d in _symbolic_divisors(comp))
         except CompileError as exc:
             groups.append(Group("unknown", str(exc), True))
             continue
