@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Checking-stage benchmark (one JSON line on rank 0).
+
+A *step* decides every checker site query of one kernel x model
+configuration (the queries the reference front end emits for it, recorded in
+tests/golden/<workload>.json by oracle/gen_golden.py): verdict plus canonical
+witness per site, i.e. the reference's Solver.check + canonicalize_witness
+(engine/detectors.py, engine/report.py:147-203) for all sites at once.
+
+metric  checked (thread, input) instances per second: the instances of all
+        sites' compiled domains (thread identities x loop indices x havoc
+        loads x user-controlled launch assignments, the boxes the engine
+        certifies point by point or by interval proof) divided by the
+        time-to-verdict of the step.  The same instance count is used by
+        the reference arm, so the driver's ratio is the time-to-verdict
+        ratio.
+value   device-resident problem set (mk_set_eval), CUDA-event time on the
+        engine stream; L2 flushed between steps.
+e2e     the public API a user calls (SiteChecker.check_queries): compile,
+        pack, H2D copy, search, D2H copy, witness assembly, every step.
+
+--impl reference runs the reference's own checker (baseline/_ref, the
+unmodified MiniKernel: Solver.check + canonicalize_witness) on the same
+queries on the host cores; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_WORKLOAD = "rotary_embedding"   # BASELINE.json configs[1] (Llama-3-8B rotary)
+CONFIG_NAMES = {
+    "rms_norm": "vLLM rms_norm, Llama-2-7B (hidden 4096), num_tokens 1..2^20",
+    "rotary_embedding": "vLLM rotary_embedding (NeoX), Llama-3-8B (32/8 heads, head 128), "
+                        "symbolic positions and num_tokens 1..2^20",
+    "moe_align": "fused-MoE moe_align_block_size port (Fig. 7), symbolic num_tokens x top_k",
+    "fused_add_rms_norm": "vLLM fused_add_rms_norm (Fig. 2), hidden 7168, inferred context",
+    "racy": "race probe (shared + global stores)",
+}
+
+
+def _load_workload(name):
+    from paper_2603_24595_b200 import ir
+    from paper_2603_24595_b200.order import origin_lookup
+
+    with open(os.path.join(ROOT, "tests", "golden", f"{name}.json")) as fh:
+        doc = json.load(fh)
+    queries = [([ir.from_json(a) for a in s["query"]], origin_lookup(s["origins"]))
+               for s in doc["sites"]]
+    return doc, queries
+
+
+def _instances(compiled):
+    """Instances certified per site: the volume of every compiled problem's
+    root box (free symbols after exact presolve)."""
+    per_site = []
+    for cq, _ in compiled:
+        v = 0
+        if cq is not None:
+            for p in cq.problems:
+                v += p.volume()
+        per_site.append(v)
+    return per_site
+
+
+class Clocks:
+    """nvidia-smi samples during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int) -> None:
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                         "--format=csv,noheader,nounits"],
+                        capture_output=True, text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def _ncu_traffic(workload):
+    """dram bytes per launch of the search kernel from a committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{workload}_summary.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get("k_search_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def _reference_checker_sample(queries, per_site, budget_s):
+    """Reference's own checking stage (Solver.check + canonicalize_witness)
+    on the site queries in order until ``budget_s`` of CPU time is spent."""
+    from refbridge import reference_check_queries  # noqa: WPS433 (bench-local helper)
+
+    t0 = time.perf_counter()
+    done, inst = reference_check_queries(queries, budget_s=budget_s)
+    dt = time.perf_counter() - t0
+    return done, sum(per_site[:done]), dt
+
+
+def run_reference(args):
+    """--impl reference: the unmodified reference checker on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from refbridge import have_reference, reference_check_queries
+
+    if not have_reference():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "reference MiniKernel not installed under baseline/_ref"}))
+        return
+    from paper_2603_24595_b200.engine import compile_all
+
+    doc, queries = _load_workload(args.workload)
+    per_site = _instances(compile_all(queries))
+    total = sum(per_site)
+    times = []
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        done, _ = reference_check_queries(queries)
+        dt = time.perf_counter() - t0
+        assert done == len(queries)
+        if step >= args.warmup:
+            times.append(dt)
+    avg = sum(times) / len(times)
+    value = total / avg
+    out = {
+        "impl": "reference",
+        "metric": "checked (thread, input) access instances/sec; time-to-verdict per kernel x model",
+        "value": value, "unit": "instances/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": avg * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int128 (mathematical integers)",
+        "data": "recorded reference site queries", "time_to_verdict_ms": avg * 1e3,
+        "config": {"workload": args.workload, "description": CONFIG_NAMES.get(args.workload),
+                   "sites": len(queries)},
+        "cpu_baseline": {"value": value, "unit": "instances/s", "cores": 1, "kind": "reference",
+                         "sample": f"all {len(queries)} {args.workload} site queries per step, "
+                                   "reference Solver.check + canonicalize_witness, 1 thread"},
+        "e2e": {"value": value, "unit": "instances/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2603_24595_b200.engine import SiteChecker, compile_all
+    from paper_2603_24595_b200.native import PackedSet
+
+    doc, queries = _load_workload(args.workload)
+    compiled = compile_all(queries)
+    per_site = _instances(compiled)
+    instances = sum(per_site)
+    chk = SiteChecker(device=local)
+    packed, offsets = chk.pack([c for c, _ in compiled])
+    resident = chk.engine.upload(packed)
+    limits = dict(chk.limits)
+    limits["max_seconds"] = min(chk.limits["max_seconds"] * len(queries), 3600.0)
+
+    # parity gate: the benchmarked result must be the reference's
+    results = chk.decide(compiled, packed, offsets)
+    bad = [i for i, (s, r) in enumerate(zip(doc["sites"], results))
+           if r.status != s["verdict"] or (r.status == "sat" and r.witness != s.get("witness"))]
+    if bad:
+        raise SystemExit(f"parity failure on sites {bad[:10]}")
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    for _ in range(args.warmup):
+        resident.run(limits)
+    clocks = Clocks(local).start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev_ms, wall, launches = [], [], 0
+    stats_acc = {}
+    for _ in range(args.steps):
+        flush.random_(0, 255)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st = resident.run(limits)
+        wall.append(time.perf_counter() - t0)
+        dev_ms.append(st["device_ms"])
+        launches += int(st["launches"])
+        for k, v in st.items():
+            stats_acc[k] = stats_acc.get(k, 0) + v
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_step = sum(dev_ms) / len(dev_ms)
+    if world > 1:
+        t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = world * instances / (ms_step / 1e3)
+
+    # e2e through the public API with host buffers (compile + H2D + search + D2H)
+    e2e_t = []
+    for step in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        res = chk.check_queries(queries)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_t) / len(e2e_t)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    # roofline of the dominant kernel (the persistent search): integer issue
+    n = args.steps
+    search_ms = stats_acc["bb_ms"] / n
+    insns = (stats_acc["insns_bb"] + stats_acc["insns_leaf"]) / n
+    peaks, src = _peaks()
+    sm_mhz = clk["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    int_peak = sms * 128 * sm_mhz * 1e6           # INT32 lanes x clock (B200: 148 SMs)
+    achieved = insns / (search_ms / 1e3) if search_ms > 0 else 0.0
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        try:
+            from refbridge import have_reference, reference_check_queries
+            if have_reference():
+                t0 = time.perf_counter()
+                done, _ = reference_check_queries(queries, budget_s=args.cpu_budget)
+                dt = time.perf_counter() - t0
+                cpu = {"value": sum(per_site[:done]) / dt, "unit": "instances/s", "cores": 1,
+                       "kind": "reference",
+                       "sample": f"first {done} of {len(queries)} {args.workload} site queries "
+                                 "through the reference's Solver.check + canonicalize_witness "
+                                 f"(baseline/_ref), {dt:.1f}s, 1 thread"}
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "instances/s", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        out = {
+            "metric": "checked (thread, input) access instances/sec; time-to-verdict per kernel x model",
+            "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int128 (mathematical integers)",
+            "data": "site queries recorded from the reference front end on the workload port",
+            "config": {"workload": args.workload, "description": CONFIG_NAMES.get(args.workload),
+                       "sites": len(queries), "instances_per_step": instances,
+                       "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": f"{world} independent replicas of the kernel x model check"},
+            "time_to_verdict_ms": ms_step,
+            "wall_ms_per_step": 1e3 * sum(wall) / len(wall),
+            "evaluated_per_step": {"boxes": stats_acc["boxes"] / n, "points": stats_acc["points"] / n},
+            "e2e": {"value": world * instances / e2e_s, "unit": "instances/s",
+                    "h2d_bytes_per_step": packed.host_bytes(),
+                    "d2h_bytes_per_step": resident.d2h_bytes(), "ms_per_step": e2e_s * 1e3},
+            "roofline": {"bound": "int32-issue", "achieved": achieved / 1e9,
+                         "peak": int_peak / 1e9, "unit": "Gop/s",
+                         "frac": achieved / int_peak if int_peak else None,
+                         "traffic": _ncu_traffic(args.workload),
+                         "kernel": "k_search (+k_bb pre-split)",
+                         "ops": "bytecode instructions executed (interval + concrete)",
+                         "peak_source": f"{sms} SMs x 128 INT32 lanes x {sm_mhz:.0f} MHz "
+                                        f"(clock sampled; peaks file: {src})"},
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(out))
+    resident.free()
+    chk.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -144,6 +144,8 @@ typedef struct mk_stats {
   double leaf_ms;       /* device time of the leaf kernels (CUDA events) */
   int64_t insns_bb;     /* bytecode instructions executed by the prune kernel */
   int64_t insns_leaf;   /* bytecode instructions executed by the leaf kernel */
+  double device_ms;     /* CUDA-event time of the whole call on the engine stream */
+  int64_t launches;     /* kernels launched by the call */
 } mk_stats;
 
 typedef struct mk_ctx mk_ctx;
@@ -160,6 +162,14 @@ const char* mk_last_error(const mk_ctx* ctx);
  * the device happen inside the call. */
 int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_limits* lim,
                  int32_t* status, mk_i128* point, mk_stats* stats);
+
+/* Device-resident problem sets: upload once, decide many times (the data
+ * stays in HBM; only verdicts and points come back). */
+typedef struct mk_dset mk_dset;
+int mk_set_upload(mk_ctx* ctx, const mk_problem_set* set, mk_dset** out);
+int mk_set_eval(mk_ctx* ctx, mk_dset* set, const mk_limits* lim, int32_t* status,
+                mk_i128* point, mk_stats* stats);
+int mk_set_free(mk_ctx* ctx, mk_dset* set);
 
 #ifdef __cplusplus
 }

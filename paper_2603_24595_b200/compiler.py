@@ -537,6 +537,7 @@ class _Presolve:
         self.fm_rounds = 0
         self.fbbt_passes = 0
         self.agg_done: Set[Tuple] = set()
+        self._canon_memo: Dict[Tuple, Node] = {}
         self.cuts: Set[Node] = set()
 
     # symbols of an IR node (memo-free; atoms are small)
@@ -545,7 +546,16 @@ class _Presolve:
         return set(ir.symbols_of(e))
 
     def _canon_cmp(self, lin: _Lin, op: str, l: Node, r: Node) -> Node:
-        """Normalise ``l op r`` to ``L op' 0`` with op' in le/eq/ne."""
+        """Normalise ``l op r`` to ``L op' 0`` with op' in le/eq/ne (pure in
+        its arguments, so memoised across presolve passes)."""
+        key = (op, l, r)
+        got = self._canon_memo.get(key)
+        if got is None:
+            got = self._canon_cmp_raw(lin, op, l, r)
+            self._canon_memo[key] = got
+        return got
+
+    def _canon_cmp_raw(self, lin: _Lin, op: str, l: Node, r: Node) -> Node:
         lf = _lin_add(lin.lin(l), lin.lin(r), -1)
         terms, c = lf
         if op in ("gt", "ge"):

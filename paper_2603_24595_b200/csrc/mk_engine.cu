@@ -551,15 +551,22 @@ __global__ void k_scatter(const char* src, const int* flag, const int* pos, long
 
 }  // namespace
 
+struct mk_dset {
+  void* d = nullptr;
+  size_t cap = 0;
+  int nprob = 0, S = 1, nvar_total = 0;
+  size_t o_probs, o_insn, o_const, o_ar, o_am, o_rows, o_terms, o_vlo, o_vhi, o_best, o_inc,
+      o_pend, o_stats, o_counts;
+};
+
 struct mk_ctx {
   int device = 0;
   int search_ctas = 148;
   std::string err;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   // growable device buffers
-  void* d_set = nullptr;
-  size_t d_set_bytes = 0;
+  mk_dset scratch;
   void* d_work = nullptr;
   size_t d_work_bytes = 0;
   void* h_pinned = nullptr;
@@ -607,7 +614,7 @@ extern "C" int mk_ctx_create(int device, mk_ctx** out) {
     delete ctx;
     return MK_ECUDA;
   }
-  for (int i = 0; i < 4; ++i) cudaEventCreate(&ctx->ev[i]);
+  for (int i = 0; i < 6; ++i) cudaEventCreate(&ctx->ev[i]);
   cudaMallocHost(&ctx->h_pinned, 4096);
   {
     int sms = 0, per_sm = 0;
@@ -623,11 +630,11 @@ extern "C" int mk_ctx_create(int device, mk_ctx** out) {
 extern "C" int mk_ctx_destroy(mk_ctx* ctx) {
   if (!ctx) return MK_OK;
   cudaSetDevice(ctx->device);
-  if (ctx->d_set) cudaFree(ctx->d_set);
   if (ctx->d_work) cudaFree(ctx->d_work);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 6; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+  if (ctx->scratch.d) cudaFree(ctx->scratch.d);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return MK_OK;
@@ -653,18 +660,9 @@ static int ensure(mk_ctx* ctx, void** buf, size_t* cap, size_t need) {
   return MK_OK;
 }
 
-extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_limits* lim,
-                            int32_t* status, mk_i128* point, mk_stats* stats) {
-  if (!ctx || !set || !status || !point) return fail(ctx, MK_EINVAL, "null argument");
-  auto t0 = std::chrono::steady_clock::now();
-  CK(cudaSetDevice(ctx->device));
-  mk_stats local_stats;
-  std::memset(&local_stats, 0, sizeof(local_stats));
+
+static int upload_set(mk_ctx* ctx, const mk_problem_set* set, mk_dset* ds) {
   const int nprob = set->nprob;
-  if (nprob <= 0) {
-    if (stats) *stats = local_stats;
-    return MK_OK;
-  }
   int S = 1;
   for (int i = 0; i < nprob; ++i) {
     const mk_problem& p = set->probs[i];
@@ -672,73 +670,87 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
       return fail(ctx, MK_EINVAL, "problem exceeds MK_MAXV symbols or MK_MAXR registers");
     if (p.nvars > S) S = p.nvars;
   }
-  int64_t max_rounds = lim && lim->max_rounds > 0 ? lim->max_rounds : 200000;
-  int64_t max_boxes = lim && lim->max_boxes > 0 ? lim->max_boxes : (int64_t)4e9;
-  double max_seconds = lim && lim->max_seconds > 0 ? lim->max_seconds : 30.0;
-  int K = lim && lim->split_k > 1 ? lim->split_k : 16;
-  int chunk = lim && lim->chunk > 0 ? lim->chunk : 65536;
-  long long leaf_volume = lim && lim->leaf_volume > 0 ? lim->leaf_volume : 4096;
-
-  // ---- upload the problem set (one contiguous device block)
-  const size_t box_bytes = sizeof(Box) + 2 * sizeof(mk_i128) * (size_t)S;
   size_t off = 0;
   auto place = [&](size_t bytes) {
     size_t o = off;
     off = align_up(off + bytes, 256);
     return o;
   };
-  size_t o_probs = place(sizeof(mk_problem) * nprob);
-  size_t o_insn = place(sizeof(mk_insn) * (size_t)set->ninsn_total + 16);
-  size_t o_const = place(sizeof(mk_i128) * (size_t)set->nconst_total + 16);
-  size_t o_ar = place(sizeof(int32_t) * (size_t)set->natom_total + 16);
-  size_t o_am = place(sizeof(uint64_t) * (size_t)set->natom_total + 16);
-  size_t o_rows = place(sizeof(mk_row) * (size_t)set->nrow_total + 16);
-  size_t o_terms = place(sizeof(mk_row_term) * (size_t)set->nterm_total + 16);
-  size_t o_vlo = place(sizeof(mk_i128) * (size_t)set->nvar_total + 16);
-  size_t o_vhi = place(sizeof(mk_i128) * (size_t)set->nvar_total + 16);
-  size_t o_best = place(sizeof(mk_i128) * (size_t)set->nvar_total + 16);
-  size_t o_inc = place(sizeof(Incumbent) * nprob);
-  size_t o_pend = place(sizeof(int) * nprob);
-  size_t o_stats = place(sizeof(DevStats));
-  size_t o_counts = place(sizeof(int) * 4);
-  size_t set_bytes = off;
-  int rc = ensure(ctx, &ctx->d_set, &ctx->d_set_bytes, set_bytes);
+  ds->o_probs = place(sizeof(mk_problem) * (nprob + 1));
+  ds->o_insn = place(sizeof(mk_insn) * (size_t)set->ninsn_total + 16);
+  ds->o_const = place(sizeof(mk_i128) * (size_t)set->nconst_total + 16);
+  ds->o_ar = place(sizeof(int32_t) * (size_t)set->natom_total + 16);
+  ds->o_am = place(sizeof(uint64_t) * (size_t)set->natom_total + 16);
+  ds->o_rows = place(sizeof(mk_row) * (size_t)set->nrow_total + 16);
+  ds->o_terms = place(sizeof(mk_row_term) * (size_t)set->nterm_total + 16);
+  ds->o_vlo = place(sizeof(mk_i128) * (size_t)set->nvar_total + 16);
+  ds->o_vhi = place(sizeof(mk_i128) * (size_t)set->nvar_total + 16);
+  ds->o_best = place(sizeof(mk_i128) * (size_t)set->nvar_total + 16);
+  ds->o_inc = place(sizeof(Incumbent) * (nprob + 1));
+  ds->o_pend = place(sizeof(int) * (nprob + 1));
+  ds->o_stats = place(sizeof(DevStats));
+  ds->o_counts = place(sizeof(int) * 4);
+  int rc = ensure(ctx, &ds->d, &ds->cap, off);
   if (rc) return rc;
-  char* base = static_cast<char*>(ctx->d_set);
+  ds->nprob = nprob;
+  ds->S = S;
+  ds->nvar_total = set->nvar_total;
+  char* base = static_cast<char*>(ds->d);
   cudaStream_t s = ctx->stream;
   auto h2d = [&](size_t o, const void* src, size_t bytes) -> cudaError_t {
     if (!bytes || !src) return cudaSuccess;
     return cudaMemcpyAsync(base + o, src, bytes, cudaMemcpyHostToDevice, s);
   };
-  CK(h2d(o_probs, set->probs, sizeof(mk_problem) * nprob));
-  CK(h2d(o_insn, set->insns, sizeof(mk_insn) * (size_t)set->ninsn_total));
-  CK(h2d(o_const, set->consts, sizeof(mk_i128) * (size_t)set->nconst_total));
-  CK(h2d(o_ar, set->atom_regs, sizeof(int32_t) * (size_t)set->natom_total));
-  CK(h2d(o_am, set->atom_masks, sizeof(uint64_t) * (size_t)set->natom_total));
-  CK(h2d(o_rows, set->rows, sizeof(mk_row) * (size_t)set->nrow_total));
-  CK(h2d(o_terms, set->row_terms, sizeof(mk_row_term) * (size_t)set->nterm_total));
-  CK(h2d(o_vlo, set->var_lo, sizeof(mk_i128) * (size_t)set->nvar_total));
-  CK(h2d(o_vhi, set->var_hi, sizeof(mk_i128) * (size_t)set->nvar_total));
-  CK(cudaMemsetAsync(base + o_pend, 0, sizeof(int) * nprob, s));
-  CK(cudaMemsetAsync(base + o_stats, 0, sizeof(DevStats), s));
+  CK(h2d(ds->o_probs, set->probs, sizeof(mk_problem) * nprob));
+  CK(h2d(ds->o_insn, set->insns, sizeof(mk_insn) * (size_t)set->ninsn_total));
+  CK(h2d(ds->o_const, set->consts, sizeof(mk_i128) * (size_t)set->nconst_total));
+  CK(h2d(ds->o_ar, set->atom_regs, sizeof(int32_t) * (size_t)set->natom_total));
+  CK(h2d(ds->o_am, set->atom_masks, sizeof(uint64_t) * (size_t)set->natom_total));
+  CK(h2d(ds->o_rows, set->rows, sizeof(mk_row) * (size_t)set->nrow_total));
+  CK(h2d(ds->o_terms, set->row_terms, sizeof(mk_row_term) * (size_t)set->nterm_total));
+  CK(h2d(ds->o_vlo, set->var_lo, sizeof(mk_i128) * (size_t)set->nvar_total));
+  CK(h2d(ds->o_vhi, set->var_hi, sizeof(mk_i128) * (size_t)set->nvar_total));
+  return MK_OK;
+}
+
+static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* status,
+                   mk_i128* point, mk_stats* stats, std::chrono::steady_clock::time_point t0) {
+  mk_stats local_stats;
+  std::memset(&local_stats, 0, sizeof(local_stats));
+  const int nprob = ds->nprob;
+  const int S = ds->S;
+  int64_t max_rounds = lim && lim->max_rounds > 0 ? lim->max_rounds : 200000;
+  int64_t max_boxes = lim && lim->max_boxes > 0 ? lim->max_boxes : (int64_t)4e9;
+  double max_seconds = lim && lim->max_seconds > 0 ? lim->max_seconds : 30.0;
+  int K = lim && lim->split_k > 1 ? lim->split_k : 16;
+  int chunk = lim && lim->chunk > 0 ? lim->chunk : 65536;
+  long long leaf_volume = lim && lim->leaf_volume > 0 ? lim->leaf_volume : 4096;
+  const size_t box_bytes = sizeof(Box) + 2 * sizeof(mk_i128) * (size_t)S;
+  char* base = static_cast<char*>(ds->d);
+  cudaStream_t s = ctx->stream;
+  int64_t launches = 0;
+  CK(cudaEventRecord(ctx->ev[4], s));
+  CK(cudaMemsetAsync(base + ds->o_pend, 0, sizeof(int) * nprob, s));
+  CK(cudaMemsetAsync(base + ds->o_stats, 0, sizeof(DevStats), s));
 
   DevSet D;
-  D.probs = reinterpret_cast<const mk_problem*>(base + o_probs);
-  D.insns = reinterpret_cast<const mk_insn*>(base + o_insn);
-  D.consts = reinterpret_cast<const mk_i128*>(base + o_const);
-  D.atom_regs = reinterpret_cast<const int32_t*>(base + o_ar);
-  D.atom_masks = reinterpret_cast<const uint64_t*>(base + o_am);
-  D.rows = reinterpret_cast<const mk_row*>(base + o_rows);
-  D.terms = reinterpret_cast<const mk_row_term*>(base + o_terms);
-  D.var_lo = reinterpret_cast<const mk_i128*>(base + o_vlo);
-  D.var_hi = reinterpret_cast<const mk_i128*>(base + o_vhi);
-  D.inc = reinterpret_cast<Incumbent*>(base + o_inc);
-  D.best = reinterpret_cast<mk_i128*>(base + o_best);
+  D.probs = reinterpret_cast<const mk_problem*>(base + ds->o_probs);
+  D.insns = reinterpret_cast<const mk_insn*>(base + ds->o_insn);
+  D.consts = reinterpret_cast<const mk_i128*>(base + ds->o_const);
+  D.atom_regs = reinterpret_cast<const int32_t*>(base + ds->o_ar);
+  D.atom_masks = reinterpret_cast<const uint64_t*>(base + ds->o_am);
+  D.rows = reinterpret_cast<const mk_row*>(base + ds->o_rows);
+  D.terms = reinterpret_cast<const mk_row_term*>(base + ds->o_terms);
+  D.var_lo = reinterpret_cast<const mk_i128*>(base + ds->o_vlo);
+  D.var_hi = reinterpret_cast<const mk_i128*>(base + ds->o_vhi);
+  D.inc = reinterpret_cast<Incumbent*>(base + ds->o_inc);
+  D.best = reinterpret_cast<mk_i128*>(base + ds->o_best);
   D.stride = S;
   D.box_bytes = box_bytes;
-  DevStats* d_st = reinterpret_cast<DevStats*>(base + o_stats);
-  int* d_counts = reinterpret_cast<int*>(base + o_counts);
-  int* d_pend = reinterpret_cast<int*>(base + o_pend);
+  DevStats* d_st = reinterpret_cast<DevStats*>(base + ds->o_stats);
+  int* d_counts = reinterpret_cast<int*>(base + ds->o_counts);
+  int* d_pend = reinterpret_cast<int*>(base + ds->o_pend);
+  int rc = MK_OK;
 
   // ---- work buffers: stack, child/leaf staging, flags, cub scratch
   size_t cap_boxes = ((size_t)3 << 30) / box_bytes;  // 3 GiB of box stack in HBM
@@ -797,6 +809,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   const long long presplit_target = lim && lim->chunk < 0 ? 0 : (long long)grid_max;
 
   k_roots<<<(nprob + 127) / 128, 128, 0, s>>>(D, nprob, stack);
+    ++launches;
   CK(cudaGetLastError());
   long long top = nprob;
   int64_t rounds = 0;
@@ -827,6 +840,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
     int threads = 128;
     k_bb<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(
         D, chunk_ptr, (int)n, K, leaf_volume, child, cflag, leafst, lflag, d_st);
+    ++launches;
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[1], s));
     top = basei;
@@ -835,15 +849,19 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
     {
       size_t tb = cub_bytes;
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, cflag, cpos, (int)(n * K), s));
+      ++launches;
       long long nc = n * K;
       k_scatter<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
           child, cflag, cpos, nc, static_cast<char*>(stack) + (size_t)top * box_bytes, box_bytes,
           d_counts);
+    ++launches;
       CK(cudaGetLastError());
       tb = cub_bytes;
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, lflag, lpos, (int)n, s));
+      ++launches;
       k_scatter<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(leafst, lflag, lpos, n, leaves,
                                                              box_bytes, d_counts + 1);
+    ++launches;
       CK(cudaGetLastError());
     }
     CK(cudaMemcpyAsync(h_counts, d_counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -856,6 +874,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
     if (nleaf > 0) {
       CK(cudaEventRecord(ctx->ev[2], s));
       k_leaf<<<(unsigned)nleaf, 256, 0, s>>>(D, leaves, (int)nleaf, d_st);
+    ++launches;
       CK(cudaGetLastError());
       CK(cudaEventRecord(ctx->ev[3], s));
       CK(cudaEventSynchronize(ctx->ev[3]));
@@ -874,7 +893,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
     }
   }
   double search_ms = 0.0;
-  int launches = 0;
+  int search_launches = 0;
   void* tasks_buf = stack;
   void* dump_buf = cta_dump;
   while (!budget_hit && top > 0) {
@@ -888,6 +907,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
     // stream-ordered just before the launch
     CK(cudaMemsetAsync(ctl, 0, sizeof(int) * 8, s));
     k_stamp<<<1, 1, 0, s>>>(reinterpret_cast<unsigned long long*>(ctl + 4));
+    ++launches;
     // always the full persistent grid: CTAs without a task idle at once,
     // which is what triggers redistribution of a lone deep subtree
     int grid = grid_max;
@@ -896,6 +916,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
         D, tasks_buf, (int)top, ctl, cta_stacks, cta_cap, cta_leaves, K, leaf_volume,
         (unsigned long long)(left * 1e9), (unsigned long long)200000, dump_buf, dump_cap,
         d_pend, d_st);
+    ++launches;
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[1], s));
     long long dumped = 0;
@@ -905,7 +926,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
     search_ms += ms;
-    ++launches;
+    ++search_launches;
     top = dumped;
     void* tmp = tasks_buf;
     tasks_buf = dump_buf;
@@ -913,11 +934,13 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   }
   if (budget_hit && top > 0 && tasks_buf != stack) {
     k_mark_pending<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, tasks_buf, top, d_pend);
+    ++launches;
     CK(cudaGetLastError());
     top = 0;
   }
   if (budget_hit && top > 0) {
     k_mark_pending<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, stack, top, d_pend);
+    ++launches;
     CK(cudaGetLastError());
   }
   // ---- results
@@ -926,15 +949,16 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   DevStats dst;
   CK(cudaMemcpyAsync(inc.data(), D.inc, sizeof(Incumbent) * nprob, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(pend.data(), d_pend, sizeof(int) * nprob, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(point, D.best, sizeof(mk_i128) * (size_t)set->nvar_total,
+  CK(cudaMemcpyAsync(point, D.best, sizeof(mk_i128) * (size_t)ds->nvar_total,
                      cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(ctx->ev[5], s));
   CK(cudaMemcpyAsync(&dst, d_st, sizeof(DevStats), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   for (int i = 0; i < nprob; ++i) {
     if (inc[i].err || pend[i]) status[i] = MK_UNKNOWN;
     else status[i] = inc[i].has ? MK_SAT : MK_UNSAT;
   }
-  local_stats.rounds = rounds + launches;
+  local_stats.rounds = rounds + search_launches;
   local_stats.boxes = (int64_t)dst.boxes;
   local_stats.leaves = (int64_t)dst.leaves;
   local_stats.points = (int64_t)dst.points;
@@ -945,6 +969,62 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   local_stats.leaf_ms = leaf_ms;
   local_stats.seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  {
+    float dms = 0.f;
+    cudaEventElapsedTime(&dms, ctx->ev[4], ctx->ev[5]);
+    local_stats.device_ms = dms;
+  }
+  local_stats.launches = launches;
   if (stats) *stats = local_stats;
   return MK_OK;
+}
+
+extern "C" int mk_set_upload(mk_ctx* ctx, const mk_problem_set* set, mk_dset** out) {
+  if (!ctx || !set || !out) return fail(ctx, MK_EINVAL, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  mk_dset* ds = new mk_dset();
+  int rc = upload_set(ctx, set, ds);
+  if (rc) {
+    if (ds->d) cudaFree(ds->d);
+    delete ds;
+    return rc;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  *out = ds;
+  return MK_OK;
+}
+
+extern "C" int mk_set_free(mk_ctx* ctx, mk_dset* ds) {
+  if (!ds) return MK_OK;
+  if (ctx) cudaSetDevice(ctx->device);
+  if (ds->d) cudaFree(ds->d);
+  delete ds;
+  return MK_OK;
+}
+
+extern "C" int mk_set_eval(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* status,
+                           mk_i128* point, mk_stats* stats) {
+  if (!ctx || !ds || !status || !point) return fail(ctx, MK_EINVAL, "null argument");
+  auto t0 = std::chrono::steady_clock::now();
+  CK(cudaSetDevice(ctx->device));
+  if (ds->nprob <= 0) {
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    return MK_OK;
+  }
+  return run_set(ctx, ds, lim, status, point, stats, t0);
+}
+
+extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_limits* lim,
+                            int32_t* status, mk_i128* point, mk_stats* stats) {
+  if (!ctx || !set || !status || !point) return fail(ctx, MK_EINVAL, "null argument");
+  auto t0 = std::chrono::steady_clock::now();
+  CK(cudaSetDevice(ctx->device));
+  if (set->nprob <= 0) {
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    return MK_OK;
+  }
+  // one-shot: the context's scratch set is reused across calls
+  int rc = upload_set(ctx, set, &ctx->scratch);
+  if (rc) return rc;
+  return run_set(ctx, &ctx->scratch, lim, status, point, stats, t0);
 }

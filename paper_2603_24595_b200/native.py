@@ -21,7 +21,7 @@ MK_UNSAT, MK_SAT, MK_UNKNOWN = 0, 1, 2
 STATUS_NAME = {MK_UNSAT: "unsat", MK_SAT: "sat", MK_UNKNOWN: "unknown"}
 
 EXPORTS = ("mk_abi_version", "mk_device_count", "mk_ctx_create", "mk_ctx_destroy",
-           "mk_last_error", "mk_site_eval")
+           "mk_last_error", "mk_site_eval", "mk_set_upload", "mk_set_eval", "mk_set_free")
 
 
 class NativeUnavailable(RuntimeError):
@@ -67,7 +67,8 @@ class Stats(ctypes.Structure):
                 ("leaves", ctypes.c_int64), ("points", ctypes.c_int64),
                 ("covered", ctypes.c_double), ("seconds", ctypes.c_double),
                 ("bb_ms", ctypes.c_double), ("leaf_ms", ctypes.c_double),
-                ("insns_bb", ctypes.c_int64), ("insns_leaf", ctypes.c_int64)]
+                ("insns_bb", ctypes.c_int64), ("insns_leaf", ctypes.c_int64),
+                ("device_ms", ctypes.c_double), ("launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -83,6 +84,11 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
     lib.mk_site_eval.argtypes = [ctypes.c_void_p, ctypes.POINTER(ProblemSet),
                                  ctypes.POINTER(Limits), ctypes.c_void_p, ctypes.c_void_p,
                                  ctypes.POINTER(Stats)]
+    lib.mk_set_upload.argtypes = [ctypes.c_void_p, ctypes.POINTER(ProblemSet),
+                                  ctypes.POINTER(ctypes.c_void_p)]
+    lib.mk_set_eval.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Limits),
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
+    lib.mk_set_free.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     return lib
 
 
@@ -248,3 +254,47 @@ class Engine:
 
     def solve(self, problems, limits: Optional[dict] = None):
         return self.solve_packed(PackedSet(problems), limits)
+
+    # -- device-resident sets ------------------------------------------------------
+
+    def upload(self, packed: PackedSet) -> "ResidentSet":
+        h = ctypes.c_void_p()
+        rc = self.lib.mk_set_upload(self.ctx, ctypes.byref(packed.struct), ctypes.byref(h))
+        if rc != 0:
+            msg = self.lib.mk_last_error(self.ctx)
+            raise RuntimeError(f"mk_set_upload failed ({rc}): {msg.decode() if msg else ''}")
+        return ResidentSet(self, packed, h)
+
+
+class ResidentSet:
+    """A problem set kept in HBM; ``run`` decides it again without any
+    host-to-device copy (only verdicts and points come back)."""
+
+    def __init__(self, engine: Engine, packed: PackedSet, handle) -> None:
+        self.engine = engine
+        self.packed = packed
+        self.handle = handle
+        P = len(packed.problems)
+        self.status = np.zeros(max(P, 1), dtype=np.int32)
+        self.point = np.zeros(max(packed.nvar_total, 1), dtype=I128)
+
+    def run(self, limits: Optional[dict] = None) -> dict:
+        lim = Limits(0, 0, 0.0, 0, 0, 0)
+        for k, v in (limits or {}).items():
+            setattr(lim, k, v)
+        st = Stats()
+        e = self.engine
+        rc = e.lib.mk_set_eval(e.ctx, self.handle, ctypes.byref(lim), self.status.ctypes.data,
+                               self.point.ctypes.data, ctypes.byref(st))
+        if rc != 0:
+            msg = e.lib.mk_last_error(e.ctx)
+            raise RuntimeError(f"mk_set_eval failed ({rc}): {msg.decode() if msg else ''}")
+        return st.as_dict()
+
+    def d2h_bytes(self) -> int:
+        return self.status.nbytes + self.point.nbytes
+
+    def free(self) -> None:
+        if self.handle:
+            self.engine.lib.mk_set_free(self.engine.ctx, self.handle)
+            self.handle = None

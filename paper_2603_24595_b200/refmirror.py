@@ -362,6 +362,12 @@ def _find_int_ite(e: Node) -> Optional[Node]:
     return None
 
 
+def _find_any_ite(e: Node) -> bool:
+    if e[0] == "i":
+        return True
+    return any(_find_any_ite(c) for c in ir.children(e))
+
+
 def _replace_all(e: Node, old: Node, new: Node) -> Node:
     if e == old:
         return new
@@ -378,6 +384,8 @@ def count_paths(assertions: Sequence[Node], cap: int) -> int:
     done = 0
     work: List[List[Node]] = [list(assertions)]
     simp: Dict[Node, Node] = {}
+    # integer if-then-else never appears unless the input has one
+    has_ite = any(_find_any_ite(a) for a in assertions)
     while work:
         if len(work) + done > cap:
             raise GiveUp(f"more than {cap} case splits")
@@ -418,7 +426,7 @@ def count_paths(assertions: Sequence[Node], cap: int) -> int:
                     raise GiveUp("unsupported: non-boolean assertion")
                 continue
             if t == "p":
-                ite = _find_int_ite(e)
+                ite = _find_int_ite(e) if has_ite else None
                 if ite is not None:
                     then_atom = _replace_all(e, ite, ite[2])
                     else_atom = _replace_all(e, ite, ite[3])
@@ -438,13 +446,45 @@ def count_paths(assertions: Sequence[Node], cap: int) -> int:
     return done
 
 
+def _path_bound(e: Node, neg: bool, cap: int) -> int:
+    """Upper bound on the paths boolean_paths expands ``e`` (or its negation)
+    into; every pending work item stands for at least one of them, so
+    ``len(work) + done`` never exceeds this bound.  Saturates at cap + 1."""
+    t = e[0]
+    if t == "o":
+        if e[1] == "not":
+            return _path_bound(e[2][0], not neg, cap)
+        conj = (e[1] == "and") != neg
+        acc = 1 if conj else 0
+        for a in e[2]:
+            b = _path_bound(a, neg, cap)
+            acc = acc * b if conj else acc + b
+            if acc > cap:
+                return cap + 1
+        return max(acc, 1)
+    if t == "p":
+        if _find_int_ite(e) is not None:
+            return cap + 1
+        op = _NEGC[e[1]] if neg else e[1]
+        return 2 if op == "ne" else 1
+    if t == "i":
+        return cap + 1
+    return 1
+
+
 def component_giveup(component: Sequence[Node], bounds: Dict[str, Interval],
                      max_paths: int = 512) -> Optional[str]:
     """The reason the reference gives up on this (simplified) component in
     solver/builtin.py:805-811, or None when it proceeds to linearisation."""
     try:
         rewritten = rewrite_divs(component, bounds)
-        count_paths(rewritten, max_paths)
+        total = 1
+        for a in rewritten:
+            total *= _path_bound(a, False, max_paths)
+            if total > max_paths:
+                break
+        if total > max_paths:
+            count_paths(rewritten, max_paths)   # exact traversal only when needed
     except GiveUp as g:
         return str(g)
     return None

@@ -160,3 +160,21 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   if (stats) *stats = st;
   return MK_OK;
 }
+
+struct mk_dset {
+  const mk_problem_set* set;
+};
+extern "C" int mk_set_upload(mk_ctx* ctx, const mk_problem_set* set, mk_dset** out) {
+  (void)ctx;
+  *out = new mk_dset{set};
+  return MK_OK;
+}
+extern "C" int mk_set_eval(mk_ctx* ctx, mk_dset* d, const mk_limits* lim, int32_t* status,
+                           mk_i128* point, mk_stats* stats) {
+  return mk_site_eval(ctx, d->set, lim, status, point, stats);
+}
+extern "C" int mk_set_free(mk_ctx* ctx, mk_dset* d) {
+  (void)ctx;
+  delete d;
+  return MK_OK;
+}
