@@ -92,9 +92,15 @@ typedef struct mk_problem {
   int32_t const_off; /* into consts */
   int32_t atom_off;  /* into atom_regs / atom_masks */
   int32_t row_off;   /* into rows */
-  int32_t pad;
+  int32_t flags;     /* MK_PF_* */
   uint64_t maxmask;  /* bit i: symbol i is maximised */
 } mk_problem;
+
+/* mk_problem.flags: the site compiler proved that every register interval
+ * over the root box, every corner product and every contraction-row sum lies
+ * in (-2^61, 2^61): the engine evaluates the problem in exact 64-bit
+ * arithmetic instead of saturating 128-bit arithmetic. */
+#define MK_PF_NARROW 1
 
 /* Linear rows used for bound contraction inside a box:
  *   sum_k coef_k * x_var_k + c0  (rel 0: <= 0, rel 1: == 0) */
@@ -131,6 +137,8 @@ typedef struct mk_limits {
   int32_t split_k;      /* children per split (0 = default 16) */
   int32_t chunk;        /* boxes per round (0 = default) */
   int64_t leaf_volume;  /* boxes at most this large are enumerated exhaustively */
+  int64_t unit_stack;   /* boxes per search-unit stack (0 = sized from HBM); a
+                           full stack spills to the next launch's task list */
 } mk_limits;
 
 typedef struct mk_stats {

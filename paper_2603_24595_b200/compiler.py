@@ -84,6 +84,7 @@ class Problem:
     atom_masks: List[int] = field(default_factory=list)
     rows: List[Tuple[int, int, List[Tuple[int, int]]]] = field(default_factory=list)
     ops_per_point: int = 0         # instructions evaluated per instance
+    narrow: bool = False           # exact in 64-bit arithmetic (narrow_proof)
 
     @property
     def nvars(self) -> int:
@@ -1269,6 +1270,11 @@ def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
         raise CompileError(f"{len(var_names)} free symbols in one component (> {MAX_VARS})")
     index = {n: i for i, n in enumerate(var_names)}
     em = _Emitter(index)
+    # an atom that holds without error at every point of the root box (sound
+    # interval proof, no possible EvalError) leaves the model set unchanged:
+    # drop it (typically the far side of an overflow pin, x <= 2^63 - 1)
+    ivl = _Ivl({n: (a, b) for n, a, b in zip(var_names, lo, hi)})
+    atoms = [a for a in atoms if _may_err(a) or _truth(a, ivl) != "T"]
     # cheap linear rows first: a definitely-false atom ends evaluation early
     atoms = sorted(atoms, key=lambda a: (0 if a[0] == "p" and a[1] in ("le", "eq") else 1))
     for i, a in enumerate(atoms):
@@ -1290,10 +1296,92 @@ def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
             if terms and all(isinstance(k, str) for k in terms):
                 rows.append((0 if a[1] == "le" else 1, c0,
                              [(index[k], v) for k, v in sorted(terms.items())]))
-    return Problem(var_names=var_names, lo=lo, hi=hi, maximize=maximize,
+    prob = Problem(var_names=var_names, lo=lo, hi=hi, maximize=maximize,
                    insns=code, consts=list(em.consts), nregs=nregs,
                    atom_regs=atom_regs, atom_masks=masks, rows=rows,
                    ops_per_point=len(code))
+    prob.narrow = narrow_proof(prob)
+    return prob
+
+
+NARROW_LIMIT = 1 << 61
+_I64_MIN, _I64_MAX = -(1 << 63), (1 << 63) - 1
+_ARITH_CODES = frozenset({OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_MOD, OP_EMOD, OP_SHL, OP_SHR})
+
+
+def narrow_proof(p: Problem) -> bool:
+    """True when exact 64-bit evaluation of ``p`` cannot overflow on the
+    device (mk_core.cuh, MK_PF_NARROW).
+
+    Runs the program once over the root box with interval bounds that
+    contain the device's interval semantics (csrc/mk_core.cuh mk_iv_binop):
+    every corner product of a multiplication is a product of in-range
+    values, quotients are bounded by the dividend, remainders by the
+    divisor.  Interval arithmetic is inclusion-isotonic, so the values the
+    device computes on any sub-box or point lie inside these root ranges.
+    Symbol bounds, arithmetic operands and results must stay inside
+    (-2^61, 2^61); registers that are only compared (e.g. the i64 bounds of
+    an overflow pin) need only fit in int64.  The contraction rows are
+    bounded by the sum of |coef| * max|x| + |c0|."""
+    nv = p.nvars
+    R: Dict[int, Tuple[int, int]] = {}
+
+    def small(r: Tuple[int, int]) -> bool:
+        return -NARROW_LIMIT < r[0] and r[1] < NARROW_LIMIT
+
+    for i in range(nv):
+        R[i] = (p.lo[i], p.hi[i])
+        if not small(R[i]):
+            return False
+    for j, c in enumerate(p.consts):
+        if not _I64_MIN <= c <= _I64_MAX:
+            return False
+        R[nv + j] = (c, c)
+    for op, d, a, b, c in p.insns:
+        if op == OP_ATOM:
+            continue
+        A = R.get(a, (0, 0))
+        B = R.get(b, (0, 0))
+        if op in _ARITH_CODES and not (small(A) and small(B)):
+            return False
+        if op == OP_ADD:
+            r = (A[0] + B[0], A[1] + B[1])
+        elif op == OP_SUB:
+            r = (A[0] - B[1], A[1] - B[0])
+        elif op == OP_MUL:
+            cs = (A[0] * B[0], A[0] * B[1], A[1] * B[0], A[1] * B[1])
+            r = (min(cs), max(cs))
+        elif op == OP_SHL:
+            if B[0] != B[1] or B[0] < 0:
+                return False
+            r = (A[0] << B[0], A[1] << B[0])
+        elif op == OP_SHR:
+            if B[0] != B[1] or B[0] < 0:
+                return False
+            r = (A[0] >> B[0], A[1] >> B[0])
+        elif op == OP_DIV:
+            m = max(abs(A[0]), abs(A[1]))
+            r = (-m, m)
+        elif op == OP_MOD:
+            m = max(abs(B[0]), abs(B[1]))
+            r = (-m, m)
+        elif op == OP_EMOD:
+            r = (0, max(abs(B[0]), abs(B[1])))
+        elif op == OP_ITE:
+            C = R.get(c, (0, 0))
+            r = (min(B[0], C[0]), max(B[1], C[1]))
+        else:   # comparisons and booleans
+            r = (0, 1)
+        if op in _ARITH_CODES and not small(r):
+            return False
+        if not (_I64_MIN <= r[0] and r[1] <= _I64_MAX):
+            return False
+        R[d] = r
+    for _rel, c0, terms in p.rows:
+        s = abs(c0) + sum(abs(cf) * max(abs(p.lo[v]), abs(p.hi[v])) for v, cf in terms)
+        if s >= NARROW_LIMIT:
+            return False
+    return True
 
 
 # -- driver ------------------------------------------------------------------------------

@@ -8,17 +8,30 @@
 //   shift (:315-318); casts are the identity (:356-364); Cmp -> 0/1; and/or
 //   short-circuit (:367-378); division/remainder by zero raises EvalError and the
 //   point is not a model (solver/query.py:59-62).
-// Values are 128-bit two's complement.  |v| >= MK_INF means "beyond the exact
-// range": interval endpoints saturate outward (sound), a concrete value that
-// saturates marks the problem inexact (reported unknown, never guessed).
+//
+// Every routine is a template over the value type V:
+//   V = i128 ("wide"): 128-bit two's complement.  |v| >= MK_INF means "beyond
+//     the exact range": interval endpoints saturate outward (sound), a concrete
+//     value that saturates marks the problem inexact (reported unknown, never
+//     guessed).
+//   V = int64_t ("narrow"): used only for problems the site compiler proved
+//     narrow (mk_problem.flags & MK_PF_NARROW): every symbol bound, every
+//     arithmetic operand and result interval over the root box and every
+//     contraction-row sum lies in (-2^61, 2^61), and every register (e.g. a
+//     constant that is only compared) fits in int64.  Interval arithmetic is
+//     inclusion-isotonic, so every value computed on any sub-box or point
+//     stays in those ranges: plain 64-bit arithmetic is exact and no
+//     saturation logic is needed.
 #pragma once
 #include <stdint.h>
 #include "mk_b200.h"
 
 #if defined(__CUDACC__)
 #define MK_HD __host__ __device__ __forceinline__
+#define MK_HDM __host__ __device__ __forceinline__ static
 #else
 #define MK_HD static inline
+#define MK_HDM static inline
 #endif
 
 typedef __int128 i128;
@@ -42,12 +55,6 @@ MK_HD mk_i128 mk_st(i128 x) {
   r.hi = (int64_t)(uint64_t)((u128)x >> 64);
   return r;
 }
-MK_HD i128 mk_clamp(i128 x) {
-  if (x >= MK_INF) return MK_INF;
-  if (x <= -MK_INF) return -MK_INF;
-  return x;
-}
-MK_HD bool mk_isinf(i128 x) { return x >= MK_INF || x <= -MK_INF; }
 
 MK_HD int mk_clz64(uint64_t x) {
 #if defined(__CUDA_ARCH__)
@@ -62,42 +69,99 @@ MK_HD int mk_bitlen(u128 x) {
   uint64_t l = (uint64_t)x;
   return l ? 64 - mk_clz64(l) : 0;
 }
+MK_HD int mk_bitlen(uint64_t x) { return x ? 64 - mk_clz64(x) : 0; }
 MK_HD u128 mk_abs(i128 x) { return x < 0 ? (u128)(-x) : (u128)x; }
 
-// saturating arithmetic on clamped operands (|a|,|b| <= MK_INF)
-MK_HD i128 mk_add(i128 a, i128 b) { return mk_clamp(a + b); }
-MK_HD i128 mk_sub(i128 a, i128 b) { return mk_clamp(a - b); }
-MK_HD i128 mk_mul(i128 a, i128 b) {
-  if (a == 0 || b == 0) return 0;
-  bool neg = (a < 0) != (b < 0);
-  if (mk_bitlen(mk_abs(a)) + mk_bitlen(mk_abs(b)) > 125) return neg ? -MK_INF : MK_INF;
-  return mk_clamp(a * b);
-}
+// ---------------------------------------------------------------------------
+// number traits
+
+template <typename V>
+struct MkNum;
+
+template <>
+struct MkNum<i128> {
+  typedef u128 U;
+  static constexpr bool kWide = true;
+  MK_HDM i128 inf() { return MK_INF; }
+  MK_HDM i128 clamp(i128 x) {
+    if (x >= MK_INF) return MK_INF;
+    if (x <= -MK_INF) return -MK_INF;
+    return x;
+  }
+  MK_HDM bool isinf(i128 x) { return x >= MK_INF || x <= -MK_INF; }
+  // saturating arithmetic on clamped operands (|a|,|b| <= MK_INF)
+  MK_HDM i128 add(i128 a, i128 b) { return clamp(a + b); }
+  MK_HDM i128 sub(i128 a, i128 b) { return clamp(a - b); }
+  MK_HDM i128 mul(i128 a, i128 b) {
+    if (a == 0 || b == 0) return 0;
+    bool neg = (a < 0) != (b < 0);
+    if (mk_bitlen(mk_abs(a)) + mk_bitlen(mk_abs(b)) > 125) return neg ? -MK_INF : MK_INF;
+    return clamp(a * b);
+  }
+  // a * 2^k, k >= 0
+  MK_HDM i128 shl(i128 a, int k) {
+    if (k >= 125) return a == 0 ? 0 : (a < 0 ? -MK_INF : MK_INF);
+    return mul(a, (i128)1 << k);
+  }
+  MK_HDM i128 shr(i128 a, int k) {
+    if (k > 126) k = 126;
+    return isinf(a) ? a : (a >> k);
+  }
+  MK_HDM i128 ld(const mk_i128& v) { return mk_ld(v); }
+};
+
+template <>
+struct MkNum<int64_t> {
+  typedef uint64_t U;
+  static constexpr bool kWide = false;
+  // never reached: narrow problems stay inside (-2^61, 2^61)
+  MK_HDM int64_t inf() { return INT64_MAX; }
+  MK_HDM int64_t clamp(int64_t x) { return x; }
+  MK_HDM bool isinf(int64_t) { return false; }
+  MK_HDM int64_t add(int64_t a, int64_t b) { return a + b; }
+  MK_HDM int64_t sub(int64_t a, int64_t b) { return a - b; }
+  MK_HDM int64_t mul(int64_t a, int64_t b) { return a * b; }
+  MK_HDM int64_t shl(int64_t a, int k) {
+    // the narrow proof bounds |a * 2^k| < 2^61, so k < 61 unless a == 0
+    return k >= 62 ? 0 : (int64_t)((uint64_t)a << k);
+  }
+  MK_HDM int64_t shr(int64_t a, int k) { return a >> (k > 63 ? 63 : k); }
+  MK_HDM int64_t ld(const mk_i128& v) { return (int64_t)v.lo; }
+};
+
+template <typename V>
+MK_HD V mk_min(V a, V b) { return a < b ? a : b; }
+template <typename V>
+MK_HD V mk_max(V a, V b) { return a > b ? a : b; }
+
 // truncating division; b != 0.  infinite numerator stays infinite, an infinite
 // divisor drives a finite numerator to 0 (the limit; sound at interval corners)
-MK_HD i128 mk_tdiv(i128 a, i128 b) {
-  if (mk_isinf(a)) return ((a < 0) != (b < 0)) ? -MK_INF : MK_INF;
-  if (mk_isinf(b)) return 0;
+template <typename V>
+MK_HD V mk_tdiv(V a, V b) {
+  typedef MkNum<V> N;
+  if (N::isinf(a)) return ((a < 0) != (b < 0)) ? -N::inf() : N::inf();
+  if (N::isinf(b)) return 0;
   return a / b;
 }
-MK_HD i128 mk_floordiv(i128 a, i128 b) {
-  i128 q = a / b;
+template <typename V>
+MK_HD V mk_floordiv(V a, V b) {
+  V q = a / b;
   if ((a % b != 0) && ((a < 0) != (b < 0))) q -= 1;
   return q;
 }
-MK_HD i128 mk_ceildiv(i128 a, i128 b) {
-  i128 q = a / b;
+template <typename V>
+MK_HD V mk_ceildiv(V a, V b) {
+  V q = a / b;
   if ((a % b != 0) && ((a < 0) == (b < 0))) q += 1;
   return q;
 }
-MK_HD i128 mk_emod_c(i128 a, i128 b) {  // exact, b != 0, finite
-  i128 m = b < 0 ? -b : b;
-  i128 r = a % m;
+template <typename V>
+MK_HD V mk_emod_c(V a, V b) {  // exact, b != 0, finite
+  V m = b < 0 ? -b : b;
+  V r = a % m;
   if (r < 0) r += m;
   return r;
 }
-MK_HD i128 mk_min(i128 a, i128 b) { return a < b ? a : b; }
-MK_HD i128 mk_max(i128 a, i128 b) { return a > b ? a : b; }
 
 struct MkProb {
   const mk_problem* p;
@@ -131,30 +195,44 @@ MK_HD MkProb mk_prob_view(const mk_problem* probs, int pid, const mk_insn* insns
 // evaluates without error, plus flags: OK = some point evaluates, ERR = some
 // point raises.  Booleans use [0,1].
 
-struct MkIv {
-  i128 lo, hi;
+template <typename V>
+struct MkIvT {
+  V lo, hi;
   uint8_t fl;
 };
+typedef MkIvT<i128> MkIv;
 
-MK_HD bool mk_sure_lt(const MkIv& a, const MkIv& b) {
-  return a.hi != MK_INF && b.lo != -MK_INF && a.hi < b.lo;
+template <typename V>
+MK_HD bool mk_sure_lt(const MkIvT<V>& a, const MkIvT<V>& b) {
+  typedef MkNum<V> N;
+  if (!N::kWide) return a.hi < b.lo;  // narrow: every endpoint is exact
+  return a.hi != N::inf() && b.lo != -N::inf() && a.hi < b.lo;
 }
-MK_HD bool mk_sure_le(const MkIv& a, const MkIv& b) {
-  return a.hi != MK_INF && b.lo != -MK_INF && a.hi <= b.lo;
+template <typename V>
+MK_HD bool mk_sure_le(const MkIvT<V>& a, const MkIvT<V>& b) {
+  typedef MkNum<V> N;
+  if (!N::kWide) return a.hi <= b.lo;
+  return a.hi != N::inf() && b.lo != -N::inf() && a.hi <= b.lo;
 }
-MK_HD bool mk_exact1(const MkIv& a) { return a.lo == a.hi && !mk_isinf(a.lo); }
+template <typename V>
+MK_HD bool mk_exact1(const MkIvT<V>& a) { return a.lo == a.hi && !MkNum<V>::isinf(a.lo); }
 
-MK_HD void mk_corners(i128 c0, i128 c1, i128 c2, i128 c3, i128* lo, i128* hi) {
+template <typename V>
+MK_HD void mk_corners(V c0, V c1, V c2, V c3, V* lo, V* hi) {
   *lo = mk_min(mk_min(c0, c1), mk_min(c2, c3));
   *hi = mk_max(mk_max(c0, c1), mk_max(c2, c3));
 }
 
-MK_HD void mk_iv_div_part(i128 xlo, i128 xhi, i128 d1, i128 d2, i128* lo, i128* hi) {
+template <typename V>
+MK_HD void mk_iv_div_part(V xlo, V xhi, V d1, V d2, V* lo, V* hi) {
   mk_corners(mk_tdiv(xlo, d1), mk_tdiv(xlo, d2), mk_tdiv(xhi, d1), mk_tdiv(xhi, d2), lo, hi);
 }
 
-MK_HD MkIv mk_iv_binop(int op, const MkIv& a, const MkIv& b) {
-  MkIv r;
+template <typename V>
+MK_HD MkIvT<V> mk_iv_binop(int op, const MkIvT<V>& a, const MkIvT<V>& b) {
+  typedef MkNum<V> N;
+  const V INF = N::inf();
+  MkIvT<V> r;
   r.fl = 0;
   bool ok = (a.fl & MK_FL_OK) && (b.fl & MK_FL_OK);
   bool err = (a.fl & MK_FL_ERR) || (b.fl & MK_FL_ERR);
@@ -166,32 +244,36 @@ MK_HD MkIv mk_iv_binop(int op, const MkIv& a, const MkIv& b) {
   }
   switch (op) {
     case MK_OP_ADD:
-      r.lo = mk_add(a.lo, b.lo);
-      r.hi = mk_add(a.hi, b.hi);
-      if (a.lo == -MK_INF || b.lo == -MK_INF) r.lo = -MK_INF;
-      if (a.hi == MK_INF || b.hi == MK_INF) r.hi = MK_INF;
+      r.lo = N::add(a.lo, b.lo);
+      r.hi = N::add(a.hi, b.hi);
+      if (N::kWide) {
+        if (a.lo == -INF || b.lo == -INF) r.lo = -INF;
+        if (a.hi == INF || b.hi == INF) r.hi = INF;
+      }
       break;
     case MK_OP_SUB:
-      r.lo = mk_sub(a.lo, b.hi);
-      r.hi = mk_sub(a.hi, b.lo);
-      if (a.lo == -MK_INF || b.hi == MK_INF) r.lo = -MK_INF;
-      if (a.hi == MK_INF || b.lo == -MK_INF) r.hi = MK_INF;
+      r.lo = N::sub(a.lo, b.hi);
+      r.hi = N::sub(a.hi, b.lo);
+      if (N::kWide) {
+        if (a.lo == -INF || b.hi == INF) r.lo = -INF;
+        if (a.hi == INF || b.lo == -INF) r.hi = INF;
+      }
       break;
     case MK_OP_MUL:
-      mk_corners(mk_mul(a.lo, b.lo), mk_mul(a.lo, b.hi), mk_mul(a.hi, b.lo), mk_mul(a.hi, b.hi),
+      mk_corners(N::mul(a.lo, b.lo), N::mul(a.lo, b.hi), N::mul(a.hi, b.lo), N::mul(a.hi, b.hi),
                  &r.lo, &r.hi);
       break;
     case MK_OP_SHL: {
       int k = (int)b.lo;  // compiler guarantees a constant in [0,256]
-      i128 f = k >= 125 ? MK_INF : ((i128)1 << k);
-      mk_corners(mk_mul(a.lo, f), mk_mul(a.hi, f), mk_mul(a.lo, f), mk_mul(a.hi, f), &r.lo, &r.hi);
+      V x = N::shl(a.lo, k), y = N::shl(a.hi, k);
+      r.lo = mk_min(x, y);
+      r.hi = mk_max(x, y);
       break;
     }
     case MK_OP_SHR: {
       int k = (int)b.lo;
-      if (k > 126) k = 126;
-      r.lo = mk_isinf(a.lo) ? a.lo : (a.lo >> k);
-      r.hi = mk_isinf(a.hi) ? a.hi : (a.hi >> k);
+      r.lo = N::shr(a.lo, k);
+      r.hi = N::shr(a.hi, k);
       break;
     }
     case MK_OP_DIV:
@@ -206,26 +288,26 @@ MK_HD MkIv mk_iv_binop(int op, const MkIv& a, const MkIv& b) {
       if (op == MK_OP_DIV) {
         bool first = true;
         if (b.hi >= 1) {  // positive divisor part
-          i128 l, h;
-          mk_iv_div_part(a.lo, a.hi, mk_max(b.lo, 1), b.hi, &l, &h);
+          V l, h;
+          mk_iv_div_part<V>(a.lo, a.hi, mk_max<V>(b.lo, 1), b.hi, &l, &h);
           r.lo = l; r.hi = h; first = false;
         }
         if (b.lo <= -1) {
-          i128 l, h;
-          mk_iv_div_part(a.lo, a.hi, b.lo, mk_min(b.hi, -1), &l, &h);
+          V l, h;
+          mk_iv_div_part<V>(a.lo, a.hi, b.lo, mk_min<V>(b.hi, -1), &l, &h);
           if (first) { r.lo = l; r.hi = h; }
           else { r.lo = mk_min(r.lo, l); r.hi = mk_max(r.hi, h); }
         }
-        if (a.lo == -MK_INF || a.hi == MK_INF) {
+        if (N::kWide && (a.lo == -INF || a.hi == INF)) {
           // unbounded numerator: be explicit about the sign reach
-          if (a.lo == -MK_INF) { if (b.hi >= 1) r.lo = -MK_INF; if (b.lo <= -1) r.hi = MK_INF; }
-          if (a.hi == MK_INF) { if (b.hi >= 1) r.hi = MK_INF; if (b.lo <= -1) r.lo = -MK_INF; }
+          if (a.lo == -INF) { if (b.hi >= 1) r.lo = -INF; if (b.lo <= -1) r.hi = INF; }
+          if (a.hi == INF) { if (b.hi >= 1) r.hi = INF; if (b.lo <= -1) r.lo = -INF; }
         }
       } else {
-        i128 m;  // max |divisor| - 1
-        if (mk_isinf(b.lo) || mk_isinf(b.hi)) m = MK_INF;
-        else m = mk_max(b.lo < 0 ? -b.lo : b.lo, b.hi < 0 ? -b.hi : b.hi) - 1;
-        bool xfin = !mk_isinf(a.lo) && !mk_isinf(a.hi);
+        V m;  // max |divisor| - 1
+        if (N::isinf(b.lo) || N::isinf(b.hi)) m = INF;
+        else m = mk_max<V>(b.lo < 0 ? -b.lo : b.lo, b.hi < 0 ? -b.hi : b.hi) - 1;
+        bool xfin = !N::isinf(a.lo) && !N::isinf(a.hi);
         bool dsing = mk_exact1(b);
         if (op == MK_OP_MOD) {
           if (xfin && dsing && a.lo == a.hi) {
@@ -234,14 +316,14 @@ MK_HD MkIv mk_iv_binop(int op, const MkIv& a, const MkIv& b) {
                                        (a.hi <= 0 && a.lo / b.lo == a.hi / b.lo))) {
             r.lo = a.lo % b.lo;
             r.hi = a.hi % b.lo;
-            if (r.lo > r.hi) { i128 t = r.lo; r.lo = r.hi; r.hi = t; }
+            if (r.lo > r.hi) { V t = r.lo; r.lo = r.hi; r.hi = t; }
           } else {
-            r.lo = (a.lo >= 0) ? 0 : ((a.lo == -MK_INF) ? -m : mk_max(a.lo, -m));
-            r.hi = (a.hi <= 0) ? 0 : ((a.hi == MK_INF) ? m : mk_min(a.hi, m));
+            r.lo = (a.lo >= 0) ? 0 : ((a.lo == -INF) ? -m : mk_max<V>(a.lo, -m));
+            r.hi = (a.hi <= 0) ? 0 : ((a.hi == INF) ? m : mk_min<V>(a.hi, m));
           }
         } else {
           if (xfin && dsing) {
-            i128 M = b.lo < 0 ? -b.lo : b.lo;
+            V M = b.lo < 0 ? -b.lo : b.lo;
             if (mk_floordiv(a.lo, M) == mk_floordiv(a.hi, M)) {
               r.lo = mk_emod_c(a.lo, M);
               r.hi = mk_emod_c(a.hi, M);
@@ -290,36 +372,39 @@ MK_HD MkIv mk_iv_binop(int op, const MkIv& a, const MkIv& b) {
 }
 
 // short-circuit booleans: a is evaluated first
-MK_HD MkIv mk_iv_and(const MkIv& a, const MkIv& b) {
+template <typename V>
+MK_HD MkIvT<V> mk_iv_and(const MkIvT<V>& a, const MkIvT<V>& b) {
   bool aok = a.fl & MK_FL_OK, bok = b.fl & MK_FL_OK;
   bool a_t = aok && a.hi == 1, a_f = aok && a.lo == 0;
   bool b_t = bok && b.hi == 1, b_f = bok && b.lo == 0;
   bool t = a_t && b_t;
   bool f = a_f || (a_t && b_f);
   bool e = (a.fl & MK_FL_ERR) || (a_t && (b.fl & MK_FL_ERR));
-  MkIv r;
+  MkIvT<V> r;
   r.lo = f ? 0 : 1;
   r.hi = t ? 1 : 0;
   r.fl = ((t || f) ? MK_FL_OK : 0) | (e ? MK_FL_ERR : 0);
   return r;
 }
-MK_HD MkIv mk_iv_or(const MkIv& a, const MkIv& b) {
+template <typename V>
+MK_HD MkIvT<V> mk_iv_or(const MkIvT<V>& a, const MkIvT<V>& b) {
   bool aok = a.fl & MK_FL_OK, bok = b.fl & MK_FL_OK;
   bool a_t = aok && a.hi == 1, a_f = aok && a.lo == 0;
   bool b_t = bok && b.hi == 1, b_f = bok && b.lo == 0;
   bool t = a_t || (a_f && b_t);
   bool f = a_f && b_f;
   bool e = (a.fl & MK_FL_ERR) || (a_f && (b.fl & MK_FL_ERR));
-  MkIv r;
+  MkIvT<V> r;
   r.lo = f ? 0 : 1;
   r.hi = t ? 1 : 0;
   r.fl = ((t || f) ? MK_FL_OK : 0) | (e ? MK_FL_ERR : 0);
   return r;
 }
-MK_HD MkIv mk_iv_ite(const MkIv& c, const MkIv& x, const MkIv& y) {
+template <typename V>
+MK_HD MkIvT<V> mk_iv_ite(const MkIvT<V>& c, const MkIvT<V>& x, const MkIvT<V>& y) {
   bool cok = c.fl & MK_FL_OK;
   bool c_t = cok && c.hi == 1, c_f = cok && c.lo == 0;
-  MkIv r;
+  MkIvT<V> r;
   bool any = false;
   r.lo = 0; r.hi = 0;
   uint8_t e = (c.fl & MK_FL_ERR) ? MK_FL_ERR : 0;
@@ -347,8 +432,10 @@ struct MkBoxVerdict {
   uint64_t und_mask;  // symbols of undecided atoms
 };
 
-MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const i128* vlo, const i128* vhi, MkIv* R,
+template <typename V>
+MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const V* vlo, const V* vhi, MkIvT<V>* R,
                                int64_t* insn_count) {
+  typedef MkNum<V> N;
   const int nv = P.p->nvars;
   const int nc = P.p->nconst;
   for (int i = 0; i < nv; ++i) {
@@ -357,7 +444,7 @@ MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const i128* vlo, const i128* vhi
     R[i].fl = MK_FL_OK;
   }
   for (int i = 0; i < nc; ++i) {
-    i128 c = mk_ld(P.consts[i]);
+    V c = N::ld(P.consts[i]);
     R[nv + i].lo = c;
     R[nv + i].hi = c;
     R[nv + i].fl = MK_FL_OK;
@@ -372,7 +459,7 @@ MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const i128* vlo, const i128* vhi
     const mk_insn in = P.insns[k];
     switch (in.op) {
       case MK_OP_ATOM: {
-        const MkIv r = R[in.a];
+        const MkIvT<V> r = R[in.a];
         bool ok = r.fl & MK_FL_OK;
         bool may_true = ok && r.hi == 1;
         bool sure_true = ok && r.lo == 1 && !(r.fl & MK_FL_ERR);
@@ -391,7 +478,7 @@ MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const i128* vlo, const i128* vhi
       case MK_OP_AND: R[in.dst] = mk_iv_and(R[in.a], R[in.b]); break;
       case MK_OP_OR: R[in.dst] = mk_iv_or(R[in.a], R[in.b]); break;
       case MK_OP_NOT: {
-        MkIv a = R[in.a], r;
+        MkIvT<V> a = R[in.a], r;
         r.lo = 1 - a.hi;
         r.hi = 1 - a.lo;
         r.fl = a.fl;
@@ -399,7 +486,7 @@ MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const i128* vlo, const i128* vhi
         break;
       }
       case MK_OP_ITE: R[in.dst] = mk_iv_ite(R[in.a], R[in.b], R[in.c]); break;
-      default: R[in.dst] = mk_iv_binop(in.op, R[in.a], R[in.b]); break;
+      default: R[in.dst] = mk_iv_binop<V>(in.op, R[in.a], R[in.b]); break;
     }
   }
   *insn_count += n;
@@ -410,58 +497,61 @@ MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const i128* vlo, const i128* vhi
 // bound contraction over the linear rows (one FBBT sweep per call);
 // returns false when the box is empty.
 
-MK_HD bool mk_contract(const MkProb& P, i128* lo, i128* hi, int sweeps) {
+template <typename V>
+MK_HD bool mk_contract(const MkProb& P, V* lo, V* hi, int sweeps) {
+  typedef MkNum<V> N;
+  const V INF = N::inf();
   const int nr = P.p->nrows;
   for (int s = 0; s < sweeps; ++s) {
     bool changed = false;
     for (int r = 0; r < nr; ++r) {
       const mk_row row = P.rows[r];
       const mk_row_term* T = P.terms + row.term_off;
-      i128 fmin = mk_ld(row.c0), fmax = fmin;
+      V fmin = N::ld(row.c0), fmax = fmin;
       int nmin_inf = 0, nmax_inf = 0;
       for (int k = 0; k < row.nterms; ++k) {
-        i128 c = mk_ld(T[k].coef);
+        V c = N::ld(T[k].coef);
         int v = T[k].var;
-        i128 a = mk_mul(c, lo[v]), b = mk_mul(c, hi[v]);
-        i128 mn = mk_min(a, b), mx = mk_max(a, b);
-        if (mn == -MK_INF) nmin_inf++; else fmin = mk_add(fmin, mn);
-        if (mx == MK_INF) nmax_inf++; else fmax = mk_add(fmax, mx);
+        V a = N::mul(c, lo[v]), b = N::mul(c, hi[v]);
+        V mn = mk_min(a, b), mx = mk_max(a, b);
+        if (N::kWide && mn == -INF) nmin_inf++; else fmin = N::add(fmin, mn);
+        if (N::kWide && mx == INF) nmax_inf++; else fmax = N::add(fmax, mx);
       }
-      if (nmin_inf == 0 && fmin > 0 && fmin != MK_INF) return false;  // sum >= fmin > 0
-      if (nmin_inf == 0 && fmin == MK_INF) return false;
-      if (row.rel == 1 && nmax_inf == 0 && fmax < 0 && fmax != -MK_INF) return false;
-      if (row.rel == 1 && nmax_inf == 0 && fmax == -MK_INF) return false;
+      if (nmin_inf == 0 && fmin > 0 && fmin != INF) return false;  // sum >= fmin > 0
+      if (N::kWide && nmin_inf == 0 && fmin == INF) return false;
+      if (row.rel == 1 && nmax_inf == 0 && fmax < 0 && fmax != -INF) return false;
+      if (N::kWide && row.rel == 1 && nmax_inf == 0 && fmax == -INF) return false;
       for (int k = 0; k < row.nterms; ++k) {
-        i128 c = mk_ld(T[k].coef);
+        V c = N::ld(T[k].coef);
         int v = T[k].var;
-        i128 a = mk_mul(c, lo[v]), b = mk_mul(c, hi[v]);
-        i128 mn = mk_min(a, b), mx = mk_max(a, b);
+        V a = N::mul(c, lo[v]), b = N::mul(c, hi[v]);
+        V mn = mk_min(a, b), mx = mk_max(a, b);
         // others_min = fmin - mn (when finite)
-        int oinf = nmin_inf - (mn == -MK_INF ? 1 : 0);
+        int oinf = nmin_inf - ((N::kWide && mn == -INF) ? 1 : 0);
         if (oinf == 0) {
-          i128 omin = (mn == -MK_INF) ? fmin : mk_sub(fmin, mn);
-          if (!mk_isinf(omin)) {
+          V omin = (N::kWide && mn == -INF) ? fmin : N::sub(fmin, mn);
+          if (!N::isinf(omin)) {
             // c*x <= -omin
             if (c > 0) {
-              i128 nb = mk_floordiv(-omin, c);
+              V nb = mk_floordiv<V>(-omin, c);
               if (nb < hi[v]) { hi[v] = nb; changed = true; }
             } else {
-              i128 nb = mk_ceildiv(-omin, c);
+              V nb = mk_ceildiv<V>(-omin, c);
               if (nb > lo[v]) { lo[v] = nb; changed = true; }
             }
           }
         }
         if (row.rel == 1) {
-          int oinf2 = nmax_inf - (mx == MK_INF ? 1 : 0);
+          int oinf2 = nmax_inf - ((N::kWide && mx == INF) ? 1 : 0);
           if (oinf2 == 0) {
-            i128 omax = (mx == MK_INF) ? fmax : mk_sub(fmax, mx);
-            if (!mk_isinf(omax)) {
+            V omax = (N::kWide && mx == INF) ? fmax : N::sub(fmax, mx);
+            if (!N::isinf(omax)) {
               // c*x >= -omax
               if (c > 0) {
-                i128 nb = mk_ceildiv(-omax, c);
+                V nb = mk_ceildiv<V>(-omax, c);
                 if (nb > lo[v]) { lo[v] = nb; changed = true; }
               } else {
-                i128 nb = mk_floordiv(-omax, c);
+                V nb = mk_floordiv<V>(-omax, c);
                 if (nb < hi[v]) { hi[v] = nb; changed = true; }
               }
             }
@@ -479,22 +569,26 @@ MK_HD bool mk_contract(const MkProb& P, i128* lo, i128* hi, int sweeps) {
 // concrete (point) evaluation.  Registers hold exact values; an error bit per
 // register tracks EvalError with the reference's short-circuit rules.
 
-struct MkCv {
-  i128 v;
+template <typename V>
+struct MkCvT {
+  V v;
   uint8_t err;
 };
+typedef MkCvT<i128> MkCv;
 
-MK_HD bool mk_eval_point(const MkProb& P, const i128* x, MkCv* R, bool* overflow,
+template <typename V>
+MK_HD bool mk_eval_point(const MkProb& P, const V* x, MkCvT<V>* R, bool* overflow,
                          int64_t* insn_count) {
+  typedef MkNum<V> N;
   const int nv = P.p->nvars;
   const int nc = P.p->nconst;
   for (int i = 0; i < nv; ++i) { R[i].v = x[i]; R[i].err = 0; }
-  for (int i = 0; i < nc; ++i) { R[nv + i].v = mk_ld(P.consts[i]); R[nv + i].err = 0; }
+  for (int i = 0; i < nc; ++i) { R[nv + i].v = N::ld(P.consts[i]); R[nv + i].err = 0; }
   const int n = P.p->ninsn;
   bool ovf = false;
   for (int k = 0; k < n; ++k) {
     const mk_insn in = P.insns[k];
-    const MkCv a = R[in.a], b = R[in.b];
+    const MkCvT<V> a = R[in.a], b = R[in.b];
     if (in.op == MK_OP_ATOM) {
       if (a.err || !a.v) {
         *insn_count += k + 1;
@@ -503,7 +597,7 @@ MK_HD bool mk_eval_point(const MkProb& P, const i128* x, MkCv* R, bool* overflow
       }
       continue;
     }
-    MkCv r;
+    MkCvT<V> r;
     r.err = 0;
     r.v = 0;
     switch (in.op) {
@@ -517,7 +611,7 @@ MK_HD bool mk_eval_point(const MkProb& P, const i128* x, MkCv* R, bool* overflow
         r.err = a.err; r.v = a.v ? 0 : 1;
         break;
       case MK_OP_ITE: {
-        const MkCv c = R[in.c];
+        const MkCvT<V> c = R[in.c];
         if (a.err) r.err = 1; else r = a.v ? b : c;
         break;
       }
@@ -525,21 +619,11 @@ MK_HD bool mk_eval_point(const MkProb& P, const i128* x, MkCv* R, bool* overflow
         r.err = a.err | b.err;
         if (!r.err) {
           switch (in.op) {
-            case MK_OP_ADD: r.v = mk_add(a.v, b.v); break;
-            case MK_OP_SUB: r.v = mk_sub(a.v, b.v); break;
-            case MK_OP_MUL: r.v = mk_mul(a.v, b.v); break;
-            case MK_OP_SHL: {
-              int k2 = (int)b.v;
-              r.v = (k2 >= 125) ? (a.v == 0 ? 0 : (a.v < 0 ? -MK_INF : MK_INF))
-                                : mk_mul(a.v, (i128)1 << k2);
-              break;
-            }
-            case MK_OP_SHR: {
-              int k2 = (int)b.v;
-              if (k2 > 126) k2 = 126;
-              r.v = a.v >> k2;
-              break;
-            }
+            case MK_OP_ADD: r.v = N::add(a.v, b.v); break;
+            case MK_OP_SUB: r.v = N::sub(a.v, b.v); break;
+            case MK_OP_MUL: r.v = N::mul(a.v, b.v); break;
+            case MK_OP_SHL: r.v = N::shl(a.v, (int)b.v); break;
+            case MK_OP_SHR: r.v = N::shr(a.v, (int)b.v); break;
             case MK_OP_DIV:
               if (b.v == 0) r.err = 1; else r.v = a.v / b.v;
               break;
@@ -557,7 +641,7 @@ MK_HD bool mk_eval_point(const MkProb& P, const i128* x, MkCv* R, bool* overflow
             case MK_OP_GE: r.v = a.v >= b.v; break;
             default: break;
           }
-          if (mk_isinf(r.v)) ovf = true;
+          if (N::isinf(r.v)) ovf = true;
         }
       }
     }
@@ -569,7 +653,8 @@ MK_HD bool mk_eval_point(const MkProb& P, const i128* x, MkCv* R, bool* overflow
 }
 
 // lexicographic comparison in witness order: true when x is strictly better
-MK_HD bool mk_lex_better(const i128* x, const i128* y, int nv, uint64_t maxmask) {
+template <typename V>
+MK_HD bool mk_lex_better(const V* x, const V* y, int nv, uint64_t maxmask) {
   for (int i = 0; i < nv; ++i) {
     if (x[i] == y[i]) continue;
     bool mx = (maxmask >> i) & 1;
@@ -579,36 +664,39 @@ MK_HD bool mk_lex_better(const i128* x, const i128* y, int nv, uint64_t maxmask)
 }
 
 // the best corner of a box (its lexicographic lower bound)
-MK_HD void mk_corner(const i128* lo, const i128* hi, int nv, uint64_t maxmask, i128* out) {
+template <typename V>
+MK_HD void mk_corner(const V* lo, const V* hi, int nv, uint64_t maxmask, V* out) {
   for (int i = 0; i < nv; ++i) out[i] = ((maxmask >> i) & 1) ? hi[i] : lo[i];
 }
 
 // box volume, saturating at 2^62
-MK_HD int64_t mk_volume(const i128* lo, const i128* hi, int nv) {
-  const i128 cap = ((i128)1) << 62;
-  i128 v = 1;
+template <typename V>
+MK_HD int64_t mk_volume(const V* lo, const V* hi, int nv) {
+  const u128 cap = ((u128)1) << 62;
+  u128 v = 1;
   for (int i = 0; i < nv; ++i) {
-    i128 s = hi[i] - lo[i] + 1;
+    u128 s = (u128)(hi[i] - lo[i]) + 1;
     if (s >= cap) return (int64_t)cap;
     v = v * s;
     if (v >= cap) return (int64_t)cap;
   }
   return (int64_t)v;
 }
-MK_HD double mk_volume_f(const i128* lo, const i128* hi, int nv) {
+template <typename V>
+MK_HD double mk_volume_f(const V* lo, const V* hi, int nv) {
   double v = 1.0;
   for (int i = 0; i < nv; ++i) v *= (double)(hi[i] - lo[i] + 1);
   return v;
 }
 
 // decode point #idx of a box in lexicographic order (index order == witness order)
-MK_HD void mk_decode(const i128* lo, const i128* hi, int nv, uint64_t maxmask, uint64_t idx,
-                     i128* x) {
+template <typename V>
+MK_HD void mk_decode(const V* lo, const V* hi, int nv, uint64_t maxmask, uint64_t idx, V* x) {
   for (int i = nv - 1; i >= 0; --i) {
     uint64_t s = (uint64_t)(hi[i] - lo[i] + 1);
     uint64_t d = idx % s;
     idx /= s;
-    x[i] = ((maxmask >> i) & 1) ? hi[i] - (i128)d : lo[i] + (i128)d;
+    x[i] = ((maxmask >> i) & 1) ? hi[i] - (V)d : lo[i] + (V)d;
   }
 }
 
@@ -618,14 +706,15 @@ MK_HD void mk_decode(const i128* lo, const i128* hi, int nv, uint64_t maxmask, u
 // an incumbent exists, the first symbol in witness order (children are then
 // lexicographically ordered and the incumbent prunes whole subtrees).
 // Returns -1 when every such symbol is fixed.
-MK_HD int mk_pick_split(const i128* lo, const i128* hi, int nv, uint64_t und_mask,
+template <typename V>
+MK_HD int mk_pick_split(const V* lo, const V* hi, int nv, uint64_t und_mask,
                         bool have_incumbent) {
   int best = -1;
-  i128 bw = 0;
+  V bw = 0;
   for (int i = 0; i < nv; ++i) {
     if (!((und_mask >> i) & 1) || lo[i] >= hi[i]) continue;
     if (have_incumbent) return i;
-    i128 w = hi[i] - lo[i];
+    V w = hi[i] - lo[i];
     if (best < 0 || w < bw) {
       best = i;
       bw = w;
@@ -635,13 +724,15 @@ MK_HD int mk_pick_split(const i128* lo, const i128* hi, int nv, uint64_t und_mas
 }
 
 // piece t (0 = best in the symbol's direction) of m near-equal pieces of [lo,hi]
-MK_HD void mk_piece(i128 lo, i128 hi, int m, int t, bool maximize, i128* plo, i128* phi) {
-  u128 size = (u128)(hi - lo) + 1;
-  u128 q = size / (u128)m, rem = size % (u128)m;
+template <typename V>
+MK_HD void mk_piece(V lo, V hi, int m, int t, bool maximize, V* plo, V* phi) {
+  typedef typename MkNum<V>::U U;
+  U size = (U)(hi - lo) + 1;
+  U q = size / (U)m, rem = size % (U)m;
   // ascending piece j covers [lo + j*q + min(j,rem), ...]
   int j = maximize ? (m - 1 - t) : t;
-  u128 start = (u128)j * q + (u128)((u128)j < rem ? (u128)j : rem);
-  u128 len = q + ((u128)j < rem ? 1 : 0);
-  *plo = lo + (i128)start;
-  *phi = *plo + (i128)len - 1;
+  U start = (U)j * q + ((U)j < rem ? (U)j : rem);
+  U len = q + ((U)j < rem ? 1 : 0);
+  *plo = lo + (V)start;
+  *phi = *plo + (V)len - 1;
 }

@@ -6,21 +6,27 @@
 // data-parallel lexicographic branch-and-prune over the problem's box of free
 // symbols:
 //
-//   k_bb    one thread per box: incumbent test on the box's best corner, linear
-//           bound contraction, interval evaluation of the bytecode, then
-//           prune / accept the corner / hand to leaf enumeration / split the
-//           first undecided symbol (witness order) into K children written in
-//           lexicographic order;
-//   k_leaf  one CTA per small box: exhaustive concrete evaluation of every
-//           instance in lexicographic order, first model per thread, CTA min
-//           reduction of the instance index (index order == witness order),
-//           incumbent update under a per-problem seqlock;
-//   stack   LIFO of boxes in HBM; children are compacted with
-//           cub::DeviceSelect::Flagged (order preserving) so the best child
-//           of the best box is always on top (depth-first in witness order,
-//           which finds the incumbent early and prunes the rest).
+//   k_bb      pre-split rounds, one thread per box: incumbent test on the
+//             box's best corner, linear bound contraction, interval
+//             evaluation of the bytecode, then prune / accept the corner /
+//             hand to leaf enumeration / split into K children written in
+//             lexicographic order; the host compacts the children
+//             (order-preserving scan) until every search unit has a task;
+//   k_search  persistent best-first search, one independent unit per WARP:
+//             pop the best 32 boxes of the warp's HBM stack (one per lane),
+//             process, warp-scan the child counts, write children worst
+//             first (best on top), enumerate small boxes warp-wide in
+//             lexicographic index order; incumbents are shared through a
+//             64-bit atomicMin key plus a per-problem seqlock.  When a
+//             quarter of the units idles, busy units dump their stacks and
+//             the host relaunches on the dumped boxes (bulk-synchronous
+//             redistribution).
 //
-// The host loop (mk_site_eval) runs rounds until the stack is empty.
+// Every per-box / per-point routine is instantiated for two value types
+// (mk_core.cuh): exact int64 for problems the compiler proved narrow, and
+// saturating int128 otherwise; narrow and wide problems run as two
+// concurrent persistent grids on two streams.  Small problems (<= 8 free
+// symbols, <= 64 registers) use compile-time-sized per-lane arrays.
 
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
@@ -36,11 +42,15 @@
 
 namespace {
 
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int SMALL_V = 8;    // free symbols of a "small" problem
+constexpr int SMALL_R = 64;   // registers of a "small" problem
+
 struct Box {
   int32_t prob;
   int32_t pad0;
   int64_t pad1;
-  // followed by i128 lo[S], hi[S]
+  // followed by mk_i128 lo[S], hi[S]
 };
 
 struct Incumbent {
@@ -75,21 +85,92 @@ struct DevStats {
   double covered;
 };
 
+// per-lane counters, flushed to DevStats once per unit
+struct LaneStats {
+  unsigned long long boxes, leaves, points, insns_bb, insns_leaf;
+  double covered;
+  __device__ void zero() {
+    boxes = leaves = points = insns_bb = insns_leaf = 0;
+    covered = 0.0;
+  }
+  __device__ void flush(DevStats* st) {
+    if (boxes) atomicAdd(&st->boxes, boxes);
+    if (leaves) atomicAdd(&st->leaves, leaves);
+    if (points) atomicAdd(&st->points, points);
+    if (insns_bb) atomicAdd(&st->insns_bb, insns_bb);
+    if (insns_leaf) atomicAdd(&st->insns_leaf, insns_leaf);
+    if (covered != 0.0) atomicAdd(&st->covered, covered);
+  }
+  __device__ void flush_warp(DevStats* st) {
+    for (int o = 16; o > 0; o >>= 1) {
+      boxes += __shfl_down_sync(FULL, boxes, o);
+      leaves += __shfl_down_sync(FULL, leaves, o);
+      points += __shfl_down_sync(FULL, points, o);
+      insns_bb += __shfl_down_sync(FULL, insns_bb, o);
+      insns_leaf += __shfl_down_sync(FULL, insns_leaf, o);
+      covered += __shfl_down_sync(FULL, covered, o);
+    }
+    if ((threadIdx.x & 31) == 0) flush(st);
+  }
+};
+
+__device__ __forceinline__ bool is_narrow(const mk_problem& p) {
+  return (p.flags & MK_PF_NARROW) != 0;
+}
+__device__ __forceinline__ bool is_small(const mk_problem& p) {
+  return p.nvars <= SMALL_V && p.nregs <= SMALL_R;
+}
+
 __device__ __forceinline__ Box* box_at(void* base, size_t box_bytes, size_t i) {
   return reinterpret_cast<Box*>(reinterpret_cast<char*>(base) + i * box_bytes);
 }
 __device__ __forceinline__ mk_i128* box_lo(Box* b) { return reinterpret_cast<mk_i128*>(b + 1); }
 
+// box storage: the pre-split stack keeps int128 bounds (mk_i128); the narrow
+// search class keeps int64 bounds (half the HBM per box)
+template <typename T>
+struct Store;
+template <>
+struct Store<i128> {
+  typedef mk_i128 E;
+  __device__ static i128 get(const E& e) { return mk_ld(e); }
+  __device__ static E put(i128 x) { return mk_st(x); }
+};
+template <>
+struct Store<int64_t> {
+  typedef int64_t E;
+  __device__ static int64_t get(const E& e) { return e; }
+  __device__ static E put(i128 x) { return (int64_t)x; }
+};
+template <typename T>
+__host__ __device__ constexpr size_t box_bytes_of(int S) {
+  return sizeof(Box) + 2 * sizeof(typename Store<T>::E) * (size_t)S;
+}
+
+template <typename V>
+__device__ __forceinline__ V ldv(const mk_i128& v) {
+  return MkNum<V>::ld(v);
+}
+template <typename V>
+__device__ __forceinline__ V ldv_volatile(const volatile mk_i128* p) {
+  mk_i128 t;
+  t.lo = p->lo;
+  t.hi = p->hi;
+  return MkNum<V>::ld(t);
+}
+
 // 64-bit lexicographic key of a point (see Incumbent::key)
-__device__ unsigned long long lex_key(const DevSet& D, const mk_problem& p, const i128* x) {
+template <typename V>
+__device__ unsigned long long lex_key(const DevSet& D, const mk_problem& p, const V* x) {
+  typedef typename MkNum<V>::U U;
   unsigned long long key = 0;
   int left = 64;
   for (int i = 0; i < p.nvars && left > 0; ++i) {
-    i128 rlo = mk_ld(D.var_lo[p.var_off + i]), rhi = mk_ld(D.var_hi[p.var_off + i]);
-    u128 span = (u128)(rhi - rlo);
+    V rlo = ldv<V>(D.var_lo[p.var_off + i]), rhi = ldv<V>(D.var_hi[p.var_off + i]);
+    U span = (U)(rhi - rlo);
     int bits = mk_bitlen(span);
     if (bits == 0) continue;
-    u128 d = ((p.maxmask >> i) & 1) ? (u128)(rhi - x[i]) : (u128)(x[i] - rlo);
+    U d = ((p.maxmask >> i) & 1) ? (U)(rhi - x[i]) : (U)(x[i] - rlo);
     if (bits <= left) {
       key = (bits == 64 ? 0ull : (key << bits)) | (unsigned long long)d;
       left -= bits;
@@ -104,14 +185,14 @@ __device__ unsigned long long lex_key(const DevSet& D, const mk_problem& p, cons
 
 // incumbent test: true when the box cannot hold anything better than the
 // current incumbent (its best corner is not strictly better)
-__device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, const i128* corner) {
+template <typename V>
+__device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, const V* corner) {
   Incumbent* I = D.inc + pid;
   {
     unsigned long long kmin = *((volatile unsigned long long*)&I->key);
-    if (kmin != ~0ull) {
-      unsigned long long k = lex_key(D, p, corner);
-      if (k > kmin) return true;   // a strictly better model was offered
-    }
+    if (kmin == ~0ull) return false;  // nothing offered yet
+    unsigned long long k = lex_key<V>(D, p, corner);
+    if (k > kmin) return true;        // a strictly better model was offered
   }
   unsigned v1 = *((volatile unsigned*)&I->version);
   if (v1 & 1u) return false;
@@ -121,10 +202,7 @@ __device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, con
   const volatile mk_i128* B = D.best + p.var_off;
   bool dominated = true;
   for (int i = 0; i < p.nvars; ++i) {
-    mk_i128 t;
-    t.lo = B[i].lo;
-    t.hi = B[i].hi;
-    i128 b = mk_ld(t);
+    V b = ldv_volatile<V>(B + i);
     if (corner[i] == b) continue;
     bool mx = (p.maxmask >> i) & 1;
     dominated = !(mx ? corner[i] > b : corner[i] < b);
@@ -136,16 +214,17 @@ __device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, con
   return dominated;
 }
 
-__device__ void inc_offer(const DevSet& D, int pid, const mk_problem& p, const i128* x) {
+template <typename V>
+__device__ void inc_offer(const DevSet& D, int pid, const mk_problem& p, const V* x) {
   Incumbent* I = D.inc + pid;
   // lock-free filter: a candidate whose key prefix is worse than the best
   // offered key loses without touching the lock
   {
-    unsigned long long k = lex_key(D, p, x);
+    unsigned long long k = lex_key<V>(D, p, x);
     unsigned long long old = atomicMin(&I->key, k);
     if (k > old) return;
   }
-  if (inc_dominates(D, pid, p, x)) return;
+  if (inc_dominates<V>(D, pid, p, x)) return;
   unsigned ns = 32;
   while (atomicCAS(&I->lock, 0, 1) != 0) {
     __nanosleep(ns);
@@ -153,15 +232,20 @@ __device__ void inc_offer(const DevSet& D, int pid, const mk_problem& p, const i
   }
   __threadfence();
   bool better = true;
-  if (I->has) {
-    i128 cur[MK_MAXV];
-    for (int i = 0; i < p.nvars; ++i) cur[i] = mk_ld(D.best[p.var_off + i]);
-    better = mk_lex_better(x, cur, p.nvars, p.maxmask);
+  if (I->has) {  // strictly better in witness order (equal points are not)
+    better = false;
+    for (int i = 0; i < p.nvars; ++i) {
+      V b = ldv<V>(D.best[p.var_off + i]);
+      if (x[i] == b) continue;
+      bool mx = (p.maxmask >> i) & 1;
+      better = mx ? x[i] > b : x[i] < b;
+      break;
+    }
   }
   if (better) {
     atomicAdd(&I->version, 1u);
     __threadfence();
-    for (int i = 0; i < p.nvars; ++i) D.best[p.var_off + i] = mk_st(x[i]);
+    for (int i = 0; i < p.nvars; ++i) D.best[p.var_off + i] = mk_st((i128)x[i]);
     I->has = 1;
     __threadfence();
     atomicAdd(&I->version, 1u);
@@ -195,8 +279,7 @@ __global__ void k_roots(DevSet D, int nprob, void* stack) {
 }
 
 // ---------------------------------------------------------------------------
-// per-box step shared by the round kernel (k_bb) and the persistent search
-// kernel (k_search)
+// per-box step
 
 enum { ACT_DONE = 0, ACT_LEAF = 1, ACT_SPLIT = 2 };
 
@@ -208,38 +291,39 @@ struct Act {
 
 // lo/hi: the box (contracted in place).  Prunes, accepts the best corner of an
 // all-true box, hands small boxes to enumeration, or chooses a split.
-__device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, i128* lo, i128* hi,
-                           int K, long long leaf_volume, DevStats* st) {
+template <typename V, int CAPV, int CAPR>
+__device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo, V* hi, int K,
+                           long long leaf_volume, LaneStats& st) {
   const int nv = p.nvars;
   const MkProb P = view(D, pid);
   Act a;
   a.kind = ACT_DONE;
   a.sv = -1;
   a.m = 0;
-  i128 c[MK_MAXV];
-  atomicAdd(&st->boxes, 1ull);
+  V c[CAPV];
+  st.boxes++;
   mk_corner(lo, hi, nv, p.maxmask, c);
-  double vol0 = mk_volume_f(lo, hi, nv);
-  if (inc_dominates(D, pid, p, c)) {
-    atomicAdd(&st->covered, vol0);
+  const double vol0 = mk_volume_f(lo, hi, nv);
+  if (inc_dominates<V>(D, pid, p, c)) {
+    st.covered += vol0;
     return a;
   }
   if (!mk_contract(P, lo, hi, 4)) {
-    atomicAdd(&st->covered, vol0);
+    st.covered += vol0;
     return a;
   }
-  MkIv R[MK_MAXR];
+  MkIvT<V> R[CAPR];
   int64_t cnt = 0;
   MkBoxVerdict v = mk_eval_box(P, lo, hi, R, &cnt);
-  atomicAdd(&st->insns_bb, (unsigned long long)cnt);
+  st.insns_bb += (unsigned long long)cnt;
   if (v.any_false) {
-    atomicAdd(&st->covered, vol0);
+    st.covered += vol0;
     return a;
   }
   if (v.all_true) {
     mk_corner(lo, hi, nv, p.maxmask, c);
-    inc_offer(D, pid, p, c);
-    atomicAdd(&st->covered, vol0);
+    inc_offer<V>(D, pid, p, c);
+    st.covered += vol0;
     return a;
   }
   if (mk_volume(lo, hi, nv) <= leaf_volume) {
@@ -251,130 +335,166 @@ __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, i128* 
     atomicExch(&D.inc[pid].err, 1);
     return a;
   }
-  i128 size = hi[sv] - lo[sv] + 1;
+  typedef typename MkNum<V>::U U;
+  U size = (U)(hi[sv] - lo[sv]) + 1;
   a.kind = ACT_SPLIT;
   a.sv = sv;
-  a.m = size < (i128)K ? (int)size : K;
+  a.m = size < (U)K ? (int)size : K;
   return a;
 }
 
-__device__ __forceinline__ void write_box(Box* out, int pid, const i128* lo, const i128* hi,
-                                          int nv, int stride, int sv, i128 plo, i128 phi) {
+template <typename T, typename V>
+__device__ __forceinline__ void write_box(Box* out, int pid, const V* lo, const V* hi, int nv,
+                                          int stride, int sv, V plo, V phi) {
+  typedef Store<T> St;
   out->prob = pid;
-  mk_i128* olo = box_lo(out);
+  typename St::E* olo = reinterpret_cast<typename St::E*>(out + 1);
   for (int k = 0; k < nv; ++k) {
-    olo[k] = mk_st(k == sv ? plo : lo[k]);
-    olo[stride + k] = mk_st(k == sv ? phi : hi[k]);
+    olo[k] = St::put((i128)(k == sv ? plo : lo[k]));
+    olo[stride + k] = St::put((i128)(k == sv ? phi : hi[k]));
   }
 }
 
-__device__ __forceinline__ void load_box(const Box* in, int nv, int stride, i128* lo, i128* hi) {
-  const mk_i128* blo = box_lo(const_cast<Box*>(in));
+template <typename T, typename V>
+__device__ __forceinline__ void load_box(const Box* in, int nv, int stride, V* lo, V* hi) {
+  typedef Store<T> St;
+  const typename St::E* blo = reinterpret_cast<const typename St::E*>(in + 1);
   for (int v = 0; v < nv; ++v) {
-    lo[v] = mk_ld(blo[v]);
-    hi[v] = mk_ld(blo[stride + v]);
+    lo[v] = (V)St::get(blo[v]);
+    hi[v] = (V)St::get(blo[stride + v]);
   }
 }
 
-// Exhaustive enumeration of one small box by the whole CTA: every instance in
-// lexicographic index order (== witness order), each thread stops at its
-// first model, CTA min of the index, incumbent update.  s_lo/s_hi in shared.
-__device__ void cta_enumerate(const DevSet& D, int pid, const mk_problem& p, const i128* s_lo,
-                              const i128* s_hi, unsigned long long* s_best, int* s_skip,
-                              DevStats* st) {
-  const int nv = p.nvars;
-  if (threadIdx.x == 0) {
-    *s_best = ~0ull;
-    i128 c[MK_MAXV];
-    mk_corner(s_lo, s_hi, nv, p.maxmask, c);
-    *s_skip = inc_dominates(D, pid, p, c) ? 1 : 0;
-  }
-  __syncthreads();
-  const unsigned long long vol = (unsigned long long)mk_volume(s_lo, s_hi, nv);
-  if (*s_skip) {
-    if (threadIdx.x == 0) {
-      atomicAdd(&st->covered, (double)vol);
-      atomicAdd(&st->leaves, 1ull);
-    }
-    __syncthreads();
-    return;
-  }
-  const MkProb P = view(D, pid);
-  MkCv R[MK_MAXR];
-  i128 x[MK_MAXV];
-  int64_t cnt = 0;
-  unsigned long long evaluated = 0;
-  bool ovf = false;
-  for (unsigned long long idx = threadIdx.x; idx < vol; idx += blockDim.x) {
-    if (idx > *((volatile unsigned long long*)s_best)) break;
-    mk_decode(s_lo, s_hi, nv, p.maxmask, idx, x);
-    ++evaluated;
-    if (mk_eval_point(P, x, R, &ovf, &cnt)) {
-      atomicMin(s_best, idx);
-      break;
-    }
-  }
-  if (ovf) atomicExch(&D.inc[pid].err, 1);
-  atomicAdd(&st->points, evaluated);
-  atomicAdd(&st->insns_leaf, (unsigned long long)cnt);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicAdd(&st->leaves, 1ull);
-    atomicAdd(&st->covered, (double)vol);
-    if (*s_best != ~0ull) {
-      mk_decode(s_lo, s_hi, nv, p.maxmask, *s_best, x);
-      inc_offer(D, pid, p, x);
-    }
-  }
-  __syncthreads();
-}
+// ---------------------------------------------------------------------------
+// pre-split round kernel: one thread per box
 
-__global__ void __launch_bounds__(128) k_bb(DevSet D, const void* chunk, int n, int K,
-                                            long long leaf_volume, void* child_out,
-                                            int* child_flag, void* leaf_out, int* leaf_flag,
-                                            DevStats* st) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  for (int j = 0; j < K; ++j) child_flag[(size_t)i * K + j] = 0;
-  leaf_flag[i] = 0;
-  const Box* in = box_at(const_cast<void*>(chunk), D.box_bytes, i);
-  const int pid = in->prob;
-  const mk_problem p = D.probs[pid];
+template <typename V, int CAPV, int CAPR>
+__device__ void bb_one(const DevSet& D, const Box* in, int pid, const mk_problem& p, int i, int K,
+                       long long leaf_volume, void* child_out, int* child_flag, void* leaf_out,
+                       int* leaf_flag, LaneStats& st) {
   const int nv = p.nvars;
-  i128 lo[MK_MAXV], hi[MK_MAXV];
-  load_box(in, nv, D.stride, lo, hi);
-  Act a = process_box(D, pid, p, lo, hi, K, leaf_volume, st);
+  V lo[CAPV], hi[CAPV];
+  load_box<i128, V>(in, nv, D.stride, lo, hi);
+  Act a = process_box<V, CAPV, CAPR>(D, pid, p, lo, hi, K, leaf_volume, st);
   if (a.kind == ACT_LEAF) {
-    write_box(box_at(leaf_out, D.box_bytes, i), pid, lo, hi, nv, D.stride, -1, 0, 0);
+    write_box<i128, V>(box_at(leaf_out, D.box_bytes, i), pid, lo, hi, nv, D.stride, -1, 0, 0);
     leaf_flag[i] = 1;
   } else if (a.kind == ACT_SPLIT) {
     bool mx = (p.maxmask >> a.sv) & 1;
     for (int t = 0; t < a.m; ++t) {
-      i128 plo, phi;
+      V plo, phi;
       mk_piece(lo[a.sv], hi[a.sv], a.m, t, mx, &plo, &phi);
       size_t slot = (size_t)i * K + (K - 1 - t);  // best piece in the highest slot
-      write_box(box_at(child_out, D.box_bytes, slot), pid, lo, hi, nv, D.stride, a.sv, plo, phi);
+      write_box<i128, V>(box_at(child_out, D.box_bytes, slot), pid, lo, hi, nv, D.stride, a.sv,
+                         plo, phi);
       child_flag[slot] = 1;
     }
   }
 }
 
-__global__ void __launch_bounds__(256) k_leaf(DevSet D, const void* leaves, int nleaf,
-                                              DevStats* st) {
-  const Box* in = box_at(const_cast<void*>(leaves), D.box_bytes, blockIdx.x);
+__global__ void __launch_bounds__(128) k_bb(DevSet D, const void* chunk, int n, int K,
+                                            long long leaf_volume, void* child_out,
+                                            int* child_flag, void* leaf_out, int* leaf_flag,
+                                            DevStats* dst) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  LaneStats st;
+  st.zero();
+  if (i < n) {
+    for (int j = 0; j < K; ++j) child_flag[(size_t)i * K + j] = 0;
+    leaf_flag[i] = 0;
+    const Box* in = box_at(const_cast<void*>(chunk), D.box_bytes, i);
+    const int pid = in->prob;
+    const mk_problem p = D.probs[pid];
+    if (is_narrow(p)) {
+      if (is_small(p))
+        bb_one<int64_t, SMALL_V, SMALL_R>(D, in, pid, p, i, K, leaf_volume, child_out, child_flag,
+                                          leaf_out, leaf_flag, st);
+      else
+        bb_one<int64_t, MK_MAXV, MK_MAXR>(D, in, pid, p, i, K, leaf_volume, child_out, child_flag,
+                                          leaf_out, leaf_flag, st);
+    } else {
+      bb_one<i128, MK_MAXV, MK_MAXR>(D, in, pid, p, i, K, leaf_volume, child_out, child_flag,
+                                     leaf_out, leaf_flag, st);
+    }
+  }
+  st.flush_warp(dst);
+}
+
+// ---------------------------------------------------------------------------
+// warp-wide exhaustive enumeration of one small box: lane l evaluates index
+// 32*r + l of round r (index order == witness order); the first round with a
+// model gives the lexicographic optimum of the box (lowest such lane).
+
+template <typename T, typename V, int CAPV, int CAPR>
+__device__ void warp_enumerate(const DevSet& D, int pid, const mk_problem& p, const Box* box,
+                               LaneStats& st) {
+  const int lane = threadIdx.x & 31;
+  const int nv = p.nvars;
+  V lo[CAPV], hi[CAPV], x[CAPV];
+  load_box<T, V>(box, nv, D.stride, lo, hi);
+  int skip = 0;
+  if (lane == 0) {
+    mk_corner(lo, hi, nv, p.maxmask, x);
+    skip = inc_dominates<V>(D, pid, p, x) ? 1 : 0;
+  }
+  skip = __shfl_sync(FULL, skip, 0);
+  const unsigned long long vol = (unsigned long long)mk_volume(lo, hi, nv);
+  if (lane == 0) {
+    st.leaves++;
+    st.covered += (double)vol;
+  }
+  if (skip) return;
+  const MkProb P = view(D, pid);
+  MkCvT<V> R[CAPR];
+  int64_t cnt = 0;
+  bool ovf = false;
+  unsigned long long found = ~0ull;
+  for (unsigned long long base = 0; base < vol; base += 32) {
+    const unsigned long long idx = base + lane;
+    bool model = false;
+    if (idx < vol) {
+      mk_decode(lo, hi, nv, p.maxmask, idx, x);
+      st.points++;
+      model = mk_eval_point(P, x, R, &ovf, &cnt);
+    }
+    unsigned m = __ballot_sync(FULL, model);
+    if (m) {
+      found = base + (unsigned long long)(__ffs(m) - 1);
+      break;
+    }
+  }
+  st.insns_leaf += (unsigned long long)cnt;
+  if (__any_sync(FULL, ovf) && lane == 0) atomicExch(&D.inc[pid].err, 1);
+  if (lane == 0 && found != ~0ull) {
+    mk_decode(lo, hi, nv, p.maxmask, found, x);
+    inc_offer<V>(D, pid, p, x);
+  }
+}
+
+template <typename V, int CAPV, int CAPR>
+__device__ void leaf_block(const DevSet& D, const Box* in, LaneStats& st) {
   const int pid = in->prob;
   const mk_problem p = D.probs[pid];
-  const int nv = p.nvars;
-  __shared__ i128 s_lo[MK_MAXV], s_hi[MK_MAXV];
-  __shared__ unsigned long long s_best;
-  __shared__ int s_skip;
-  const mk_i128* blo = box_lo(const_cast<Box*>(in));
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-    s_lo[v] = mk_ld(blo[v]);
-    s_hi[v] = mk_ld(blo[D.stride + v]);
+  warp_enumerate<i128, V, CAPV, CAPR>(D, pid, p, in, st);
+}
+
+// pre-split leaves: one warp per leaf box
+__global__ void __launch_bounds__(128) k_leaf(DevSet D, const void* leaves, int nleaf,
+                                              DevStats* dst) {
+  const int w = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  LaneStats st;
+  st.zero();
+  if (w < nleaf) {
+    const Box* in = box_at(const_cast<void*>(leaves), D.box_bytes, w);
+    const mk_problem p = D.probs[in->prob];
+    if (is_narrow(p)) {
+      if (is_small(p)) leaf_block<int64_t, SMALL_V, SMALL_R>(D, in, st);
+      else leaf_block<int64_t, MK_MAXV, MK_MAXR>(D, in, st);
+    } else {
+      leaf_block<i128, MK_MAXV, MK_MAXR>(D, in, st);
+    }
   }
-  __syncthreads();
-  cta_enumerate(D, pid, p, s_lo, s_hi, &s_best, &s_skip, st);
+  st.flush_warp(dst);
 }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -385,155 +505,216 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 
 __global__ void k_stamp(unsigned long long* out) { *out = globaltimer_ns(); }
 
-// Persistent search: each CTA takes tasks (pre-split boxes, best first) and
-// runs a 128-wide best-first DFS from its own HBM stack: pop the top n boxes,
-// one per thread, process, block-scan the children counts, write children in
-// lexicographic order (best on top), enumerate leaves CTA-wide; repeat until
-// the stack is empty.  Incumbents are shared across CTAs through the seqlock.
+// ---------------------------------------------------------------------------
+// persistent warp-granular search
+
 #define SEARCH_THREADS 128
-// control block: [0] task counter, [1] idle CTAs, [2] dumped boxes,
-//                [4..5] start stamp (u64)
-__global__ void __launch_bounds__(SEARCH_THREADS) k_search(
-    DevSet D, const void* tasks, int ntasks, int* ctl, void* stacks, long long cap,
-    void* leafbuf, int K, long long leaf_volume, unsigned long long budget_ns,
-    unsigned long long slice_ns, void* dump, long long dump_cap, int* pending, DevStats* st) {
-  typedef cub::BlockScan<int, SEARCH_THREADS> Scan;
-  __shared__ typename Scan::TempStorage scan_tmp;
-  __shared__ int s_task, s_abort, s_dump;
-  __shared__ long long s_top, s_dump_off;
-  __shared__ int s_nleaf;
-  __shared__ i128 s_lo[MK_MAXV], s_hi[MK_MAXV];
-  __shared__ unsigned long long s_best;
-  __shared__ int s_skip;
-  const unsigned long long t_start = *reinterpret_cast<const unsigned long long*>(ctl + 4);
-  const unsigned long long deadline_ns = t_start + budget_ns;
-  const int grid = gridDim.x;
-  char* my_stack = static_cast<char*>(stacks) + (size_t)blockIdx.x * (size_t)cap * D.box_bytes;
-  char* my_leaves = static_cast<char*>(leafbuf) + (size_t)blockIdx.x * SEARCH_THREADS * D.box_bytes;
-  const int t = threadIdx.x;
-  const size_t words = D.box_bytes / sizeof(int4);
-  for (;;) {
-    if (t == 0) s_task = atomicAdd(ctl, 1);
-    __syncthreads();
-    const int task = s_task;
-    if (task >= ntasks) {
-      if (t == 0) atomicAdd(ctl + 1, 1);  // idle from now on
-      return;
+#define WARPS_PER_CTA (SEARCH_THREADS / 32)
+
+struct SearchArgs {
+  const void* tasks;
+  int ntasks;
+  int* ctl;  // [0] task counter, [1] idle units, [2..3] dumped boxes (u64), [4..5] start stamp
+  void* stacks;
+  long long cap;  // boxes per unit stack
+  void* leafbuf;  // 32 boxes per unit
+  int K;
+  long long leaf_volume;
+  unsigned long long budget_ns, slice_ns;
+  void* dump;
+  long long dump_cap;
+  int* pending;
+  DevStats* st;
+  int units;
+  size_t box_bytes;  // class storage (Store<V>)
+};
+
+// TASK_DUMPED: redistribution (every task has been handed out), the unit
+// ends this launch
+enum { TASK_DONE = 0, TASK_ABORT = 1, TASK_DUMPED = 2 };
+
+// copy the unit's stack [0, top) to the global dump buffer; returns false
+// (and reserves nothing) when the dump buffer cannot take it
+__device__ bool dump_stack(const SearchArgs& A, const DevSet& D, char* stack, long long top) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long off = ~0ull;
+  if (lane == 0) {
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(A.ctl + 2);
+    unsigned long long cur = *((volatile unsigned long long*)ctr);
+    for (;;) {
+      if (cur + (unsigned long long)top > (unsigned long long)A.dump_cap) break;
+      unsigned long long prev = atomicCAS(ctr, cur, cur + (unsigned long long)top);
+      if (prev == cur) {
+        off = cur;
+        break;
+      }
+      cur = prev;
     }
-    // tasks are taken best-first: the top of the task stack
-    const Box* tb = box_at(const_cast<void*>(tasks), D.box_bytes, (size_t)(ntasks - 1 - task));
-    const int pid = tb->prob;
-    const mk_problem p = D.probs[pid];
-    const int nv = p.nvars;
-    {
-      const int4* src = reinterpret_cast<const int4*>(tb);
-      int4* dst = reinterpret_cast<int4*>(my_stack);
-      for (size_t w = t; w < words; w += SEARCH_THREADS) dst[w] = src[w];
-    }
-    if (t == 0) {
-      s_top = 1;
-      s_abort = globaltimer_ns() > deadline_ns ? 1 : 0;
-      s_dump = 0;
-    }
-    __syncthreads();
-    if (s_abort) {
-      if (t == 0) pending[pid] = 1;
-      __syncthreads();
+  }
+  off = __shfl_sync(FULL, off, 0);
+  if (off == ~0ull) return false;
+  const size_t words = A.box_bytes / sizeof(int4);
+  const int4* src = reinterpret_cast<const int4*>(stack);
+  int4* dst = reinterpret_cast<int4*>(static_cast<char*>(A.dump) + (size_t)off * A.box_bytes);
+  const size_t total = (size_t)top * words;
+  for (size_t w = lane; w < total; w += 32) dst[w] = src[w];
+  return true;
+}
+
+template <typename V, int CAPV, int CAPR>
+__device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const mk_problem& p,
+                           char* stack, char* leaves, unsigned long long t_start,
+                           LaneStats& st) {
+  const int lane = threadIdx.x & 31;
+  const int nv = p.nvars;
+  const int K = A.K;
+  const unsigned long long deadline_ns = t_start + A.budget_ns;
+  long long top = 1;
+  while (top > 0) {
+    long long room = A.cap - top;
+    long long n = top < 32 ? top : 32;
+    long long fit = room / (K - 1);
+    if (fit < n) n = fit;
+    if (n < 1) {
+      // stack full: the bottom (worst) half goes to the next launch's task
+      // list, the unit keeps searching its best half
+      const long long spill = top - top / 2;
+      if (!dump_stack(A, D, stack, spill)) {
+        if (lane == 0) atomicExch(&D.inc[pid].err, 1);
+        return TASK_DONE;
+      }
+      const size_t words = A.box_bytes / sizeof(int4);
+      const int4* src = reinterpret_cast<const int4*>(stack + (size_t)spill * A.box_bytes);
+      int4* dst = reinterpret_cast<int4*>(stack);
+      const size_t total = (size_t)(top - spill) * words;  // <= spill * words: no overlap
+      for (size_t w = lane; w < total; w += 32) dst[w] = src[w];
+      __syncwarp();
+      top -= spill;
       continue;
     }
-    while (s_top > 0) {
-      long long top = s_top;
-      long long room = cap - top;
-      long long n = top < SEARCH_THREADS ? top : SEARCH_THREADS;
-      long long fit = room / (K - 1);
-      if (fit < n) n = fit;
-      if (n < 1) {  // stack full: give up on this task honestly
-        if (t == 0) atomicExch(&D.inc[pid].err, 1);
-        break;
-      }
-      const long long base = top - n;
-      i128 lo[MK_MAXV], hi[MK_MAXV];
-      Act a;
-      a.kind = ACT_DONE;
-      a.m = 0;
-      a.sv = -1;
-      if (t < n) {
-        load_box(box_at(my_stack, D.box_bytes, (size_t)(base + t)), nv, D.stride, lo, hi);
-        a = process_box(D, pid, p, lo, hi, K, leaf_volume, st);
-      }
-      int nch = a.kind == ACT_SPLIT ? a.m : 0;
-      int isleaf = a.kind == ACT_LEAF ? 1 : 0;
-      int coff, ctot, loff, ltot;
-      Scan(scan_tmp).ExclusiveSum(nch, coff, ctot);
-      __syncthreads();
-      Scan(scan_tmp).ExclusiveSum(isleaf, loff, ltot);
-      __syncthreads();  // every popped box has been read: its slot may be reused
-      if (nch) {
-        bool mx = (p.maxmask >> a.sv) & 1;
-        for (int j = 0; j < a.m; ++j) {
-          i128 plo, phi;
-          mk_piece(lo[a.sv], hi[a.sv], a.m, a.m - 1 - j, mx, &plo, &phi);  // worst first
-          write_box(box_at(my_stack, D.box_bytes, (size_t)(base + coff + j)), pid, lo, hi, nv,
-                    D.stride, a.sv, plo, phi);
-        }
-      }
-      if (isleaf) write_box(box_at(my_leaves, D.box_bytes, loff), pid, lo, hi, nv, D.stride, -1, 0, 0);
-      if (t == 0) {
-        s_top = base + ctot;
-        s_nleaf = ltot;
-        unsigned long long now = globaltimer_ns();
-        if (now > deadline_ns) s_abort = 1;
-        // hand the remaining subtrees back when a quarter of the grid idles
-        int idle = *((volatile int*)(ctl + 1));
-        if (s_top > 0 && idle * 4 >= grid && now > t_start + slice_ns) s_dump = 1;
-      }
-      __syncthreads();
-      for (int l = 0; l < s_nleaf; ++l) {
-        const Box* lb = box_at(my_leaves, D.box_bytes, l);
-        for (int v = t; v < nv; v += SEARCH_THREADS) {
-          s_lo[v] = mk_ld(box_lo(const_cast<Box*>(lb))[v]);
-          s_hi[v] = mk_ld(box_lo(const_cast<Box*>(lb))[D.stride + v]);
-        }
-        __syncthreads();
-        cta_enumerate(D, pid, p, s_lo, s_hi, &s_best, &s_skip, st);
-      }
-      if (s_abort) {
-        if (t == 0 && s_top > 0) pending[pid] = 1;
-        break;
-      }
-      if (s_dump) {
-        if (t == 0) {
-          long long off = atomicAdd(reinterpret_cast<unsigned long long*>(ctl + 2),
-                                    (unsigned long long)s_top);
-          s_dump_off = off;
-          if (off + s_top > dump_cap) {
-            atomicExch(&D.inc[pid].err, 1);
-            s_dump_off = -1;
-          }
-        }
-        __syncthreads();
-        if (s_dump_off >= 0) {
-          const int4* src = reinterpret_cast<const int4*>(my_stack);
-          int4* dst = reinterpret_cast<int4*>(static_cast<char*>(dump) +
-                                              (size_t)s_dump_off * D.box_bytes);
-          size_t total = (size_t)s_top * words;
-          for (size_t w = t; w < total; w += SEARCH_THREADS) dst[w] = src[w];
-        }
-        __syncthreads();
-        break;
+    const long long base = top - n;
+    V lo[CAPV], hi[CAPV];
+    Act a;
+    a.kind = ACT_DONE;
+    a.m = 0;
+    a.sv = -1;
+    if (lane < n) {
+      load_box<V, V>(box_at(stack, A.box_bytes, (size_t)(base + lane)), nv, D.stride, lo, hi);
+      a = process_box<V, CAPV, CAPR>(D, pid, p, lo, hi, K, A.leaf_volume, st);
+    }
+    const int nch = a.kind == ACT_SPLIT ? a.m : 0;
+    int incl = nch;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int ctot = __shfl_sync(FULL, incl, 31);
+    const int coff = incl - nch;
+    const unsigned leafmask = __ballot_sync(FULL, a.kind == ACT_LEAF);
+    __syncwarp();  // every popped box has been read: its slot may be reused
+    if (nch) {
+      bool mx = (p.maxmask >> a.sv) & 1;
+      for (int j = 0; j < a.m; ++j) {
+        V plo, phi;
+        mk_piece(lo[a.sv], hi[a.sv], a.m, a.m - 1 - j, mx, &plo, &phi);  // worst first
+        write_box<V, V>(box_at(stack, A.box_bytes, (size_t)(base + coff + j)), pid, lo, hi, nv,
+                        D.stride, a.sv, plo, phi);
       }
     }
-    __syncthreads();
-    if (s_dump) return;  // this launch ends; the host redistributes the dump
+    if (a.kind == ACT_LEAF) {
+      const int loff = __popc(leafmask & ((1u << lane) - 1u));
+      write_box<V, V>(box_at(leaves, A.box_bytes, loff), pid, lo, hi, nv, D.stride, -1, 0, 0);
+    }
+    __syncwarp();
+    top = base + ctot;
+    const int nleaf = __popc(leafmask);
+    for (int l = 0; l < nleaf; ++l)
+      warp_enumerate<V, V, CAPV, CAPR>(D, pid, p, box_at(leaves, A.box_bytes, l), st);
+    int ctlw = 0;
+    if (lane == 0) {
+      unsigned long long now = globaltimer_ns();
+      if (now > deadline_ns) ctlw = 1;
+      // hand the remaining subtrees back when a quarter of the units idles
+      int idle = *((volatile int*)(A.ctl + 1));
+      if (!ctlw && top > 0 && idle * 4 >= A.units && now > t_start + A.slice_ns) ctlw = 2;
+    }
+    ctlw = __shfl_sync(FULL, ctlw, 0);
+    if (ctlw == 1) return top > 0 ? TASK_ABORT : TASK_DONE;
+    // a redistribution dump that does not fit simply keeps searching
+    if (ctlw == 2 && dump_stack(A, D, stack, top)) return TASK_DUMPED;
   }
+  return TASK_DONE;
+}
+
+// resident CTAs per SM the register allocation is bounded for (occupancy
+// vs. spills; measured)
+#ifndef MK_MINB_NARROW
+#define MK_MINB_NARROW 4
+#endif
+#ifndef MK_MINB_WIDE
+#define MK_MINB_WIDE 2
+#endif
+template <typename V>
+struct MinBlocks {
+  static constexpr int value = MkNum<V>::kWide ? MK_MINB_WIDE : MK_MINB_NARROW;
+};
+
+template <typename V>
+__global__ void __launch_bounds__(SEARCH_THREADS, MinBlocks<V>::value)
+    k_search(DevSet D, SearchArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int unit = blockIdx.x * WARPS_PER_CTA + threadIdx.x / 32;
+  const unsigned long long t_start = *reinterpret_cast<const unsigned long long*>(A.ctl + 4);
+  char* stack = static_cast<char*>(A.stacks) + (size_t)unit * (size_t)A.cap * A.box_bytes;
+  char* leaves = static_cast<char*>(A.leafbuf) + (size_t)unit * 32 * A.box_bytes;
+  const size_t words = A.box_bytes / sizeof(int4);
+  LaneStats st;
+  st.zero();
+  for (;;) {
+    int task = 0;
+    if (lane == 0) task = atomicAdd(A.ctl, 1);
+    task = __shfl_sync(FULL, task, 0);
+    if (task >= A.ntasks) {
+      if (lane == 0) atomicAdd(A.ctl + 1, 1);  // idle from now on
+      break;
+    }
+    // tasks are taken best-first: the top of the task stack
+    const Box* tb = box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - 1 - task));
+    {
+      const int4* src = reinterpret_cast<const int4*>(tb);
+      int4* dst = reinterpret_cast<int4*>(stack);
+      for (size_t w = lane; w < words; w += 32) dst[w] = src[w];
+    }
+    __syncwarp();
+    const int pid = tb->prob;
+    const mk_problem p = D.probs[pid];
+    if (globaltimer_ns() > t_start + A.budget_ns) {
+      if (lane == 0) A.pending[pid] = 1;
+      continue;
+    }
+    int r;
+    if (is_small(p)) r = search_task<V, SMALL_V, SMALL_R>(A, D, pid, p, stack, leaves, t_start, st);
+    else r = search_task<V, MK_MAXV, MK_MAXR>(A, D, pid, p, stack, leaves, t_start, st);
+    if (r == TASK_ABORT && lane == 0) A.pending[pid] = 1;
+    if (r == TASK_DUMPED) break;  // this launch ends for the unit; the host redistributes
+  }
+  st.flush_warp(A.st);
 }
 
 // problems that still own boxes when the budget runs out are undecided
-__global__ void k_mark_pending(DevSet D, const void* stack, long long top, int* pending) {
+__global__ void k_mark_pending(const void* stack, size_t box_bytes, long long top, int* pending) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= top) return;
-  const Box* b = box_at(const_cast<void*>(stack), D.box_bytes, (size_t)i);
+  const Box* b = box_at(const_cast<void*>(stack), box_bytes, (size_t)i);
   pending[b->prob] = 1;
+}
+
+// flag[i] = box i belongs to a problem of class `narrow` (1) / wide (0)
+__global__ void k_class_flags(DevSet D, const void* boxes, long long n, int narrow, int* flag) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Box* b = box_at(const_cast<void*>(boxes), D.box_bytes, (size_t)i);
+  flag[i] = (((D.probs[b->prob].flags & MK_PF_NARROW) != 0) == (narrow != 0)) ? 1 : 0;
 }
 
 // move flagged fixed-size box records to their scanned positions; the last
@@ -549,6 +730,24 @@ __global__ void k_scatter(const char* src, const int* flag, const int* pos, long
   for (size_t w = 0; w < box_bytes / sizeof(int4); ++w) d[w] = s[w];
 }
 
+// partition: box i of the int128 pre-split stack goes, converted to the
+// class storage T, to slot pos[i] when flagged; the last thread publishes
+// the selected count
+template <typename T>
+__global__ void k_to_class(DevSet D, const char* src, const int* flag, const int* pos,
+                           long long n, char* dst, int* count) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i == n - 1) *count = pos[i] + flag[i];
+  if (!flag[i]) return;
+  const Box* in = reinterpret_cast<const Box*>(src + (size_t)i * D.box_bytes);
+  Box* out = reinterpret_cast<Box*>(dst + (size_t)pos[i] * box_bytes_of<T>(D.stride));
+  const int nv = D.probs[in->prob].nvars;
+  T lo[MK_MAXV], hi[MK_MAXV];
+  load_box<i128, T>(in, nv, D.stride, lo, hi);
+  write_box<T, T>(out, in->prob, lo, hi, nv, D.stride, -1, 0, 0);
+}
+
 }  // namespace
 
 struct mk_dset {
@@ -561,10 +760,13 @@ struct mk_dset {
 
 struct mk_ctx {
   int device = 0;
-  int search_ctas = 148;
+  int sms = 148;
+  int units[2] = {592, 592};  // search units (warps) of the wide [0] / narrow [1] grid
+  int ctas[2] = {148, 148};
   std::string err;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t ev[8] = {};
   // growable device buffers
   mk_dset scratch;
   void* d_work = nullptr;
@@ -608,20 +810,28 @@ extern "C" int mk_ctx_create(int device, mk_ctx** out) {
     delete ctx;
     return MK_ECUDA;
   }
-  // the evaluators keep their register files in local memory
+  // the wide evaluators keep their register files in local memory
   cudaDeviceSetLimit(cudaLimitStackSize, 32 * 1024);
   if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
     return MK_ECUDA;
   }
-  for (int i = 0; i < 6; ++i) cudaEventCreate(&ctx->ev[i]);
+  for (int c = 0; c < 2; ++c) cudaStreamCreateWithFlags(&ctx->side[c], cudaStreamNonBlocking);
+  for (int i = 0; i < 8; ++i) cudaEventCreate(&ctx->ev[i]);
   cudaMallocHost(&ctx->h_pinned, 4096);
   {
-    int sms = 0, per_sm = 0;
+    int sms = 0, per_wide = 0, per_narrow = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, SEARCH_THREADS, 0);
-    if (per_sm < 1) per_sm = 1;
-    ctx->search_ctas = sms * per_sm;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_wide, k_search<i128>, SEARCH_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_narrow, k_search<int64_t>, SEARCH_THREADS,
+                                                  0);
+    if (per_wide < 1) per_wide = 1;
+    if (per_narrow < 1) per_narrow = 1;
+    ctx->sms = sms;
+    ctx->ctas[0] = sms * per_wide;
+    ctx->ctas[1] = sms * per_narrow;
+    ctx->units[0] = ctx->ctas[0] * WARPS_PER_CTA;
+    ctx->units[1] = ctx->ctas[1] * WARPS_PER_CTA;
   }
   *out = ctx;
   return MK_OK;
@@ -632,9 +842,11 @@ extern "C" int mk_ctx_destroy(mk_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->d_work) cudaFree(ctx->d_work);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
-  for (int i = 0; i < 6; ++i)
+  for (int i = 0; i < 8; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   if (ctx->scratch.d) cudaFree(ctx->scratch.d);
+  for (int c = 0; c < 2; ++c)
+    if (ctx->side[c]) cudaStreamDestroy(ctx->side[c]);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return MK_OK;
@@ -659,7 +871,6 @@ static int ensure(mk_ctx* ctx, void** buf, size_t* cap, size_t need) {
   *cap = want;
   return MK_OK;
 }
-
 
 static int upload_set(mk_ctx* ctx, const mk_problem_set* set, mk_dset* ds) {
   const int nprob = set->nprob;
@@ -689,7 +900,7 @@ static int upload_set(mk_ctx* ctx, const mk_problem_set* set, mk_dset* ds) {
   ds->o_inc = place(sizeof(Incumbent) * (nprob + 1));
   ds->o_pend = place(sizeof(int) * (nprob + 1));
   ds->o_stats = place(sizeof(DevStats));
-  ds->o_counts = place(sizeof(int) * 4);
+  ds->o_counts = place(sizeof(int) * 8);
   int rc = ensure(ctx, &ds->d, &ds->cap, off);
   if (rc) return rc;
   ds->nprob = nprob;
@@ -712,6 +923,19 @@ static int upload_set(mk_ctx* ctx, const mk_problem_set* set, mk_dset* ds) {
   CK(h2d(ds->o_vhi, set->var_hi, sizeof(mk_i128) * (size_t)set->nvar_total));
   return MK_OK;
 }
+
+// one persistent search class (0 = wide / int128, 1 = narrow / int64)
+struct ClassRun {
+  void* tasks;
+  void* dump;
+  long long ntasks;
+  int* ctl;
+  void* stacks;
+  void* leafbuf;
+  long long cap;
+  int launches;
+  double ms;
+};
 
 static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* status,
                    mk_i128* point, mk_stats* stats, std::chrono::steady_clock::time_point t0) {
@@ -752,14 +976,20 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   int* d_pend = reinterpret_cast<int*>(base + ds->o_pend);
   int rc = MK_OK;
 
-  // ---- work buffers: stack, child/leaf staging, flags, cub scratch
-  size_t cap_boxes = ((size_t)3 << 30) / box_bytes;  // 3 GiB of box stack in HBM
+  // ---- work buffers: pre-split stack, child/leaf staging, flags, cub
+  // scratch, and per class: task/dump buffers, unit stacks, leaf lists
+  size_t cap_boxes = ((size_t)2 << 30) / box_bytes;  // 2 GiB of pre-split stack in HBM
   if (cap_boxes < (size_t)nprob + (size_t)chunk * K) cap_boxes = (size_t)nprob + (size_t)chunk * K;
+  // per class c (0 = wide / int128 storage, 1 = narrow / int64 storage)
+  const size_t cbytes[2] = {box_bytes_of<i128>(S), box_bytes_of<int64_t>(S)};
+  size_t cls_cap[2];
+  for (int c = 0; c < 2; ++c) cls_cap[c] = ((size_t)2 << 30) / cbytes[c];  // 2 GiB per task / dump buffer
+  size_t scan_n = (size_t)chunk * K;
+  if (scan_n < cap_boxes) scan_n = cap_boxes;
   size_t cub_bytes = 0;
   {
     size_t t1 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, t1, (const int*)nullptr, (int*)nullptr,
-                                  (int)((size_t)chunk * K), s);
+    cub::DeviceScan::ExclusiveSum(nullptr, t1, (const int*)nullptr, (int*)nullptr, (int)scan_n, s);
     cub_bytes = t1;
   }
   size_t w = 0;
@@ -770,25 +1000,28 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   };
   size_t w_stack = wplace(box_bytes * cap_boxes);
   size_t w_child = wplace(box_bytes * (size_t)chunk * K);
-  size_t w_cflag = wplace(sizeof(int) * (size_t)chunk * K);
-  size_t w_cpos = wplace(sizeof(int) * (size_t)chunk * K);
+  size_t w_cflag = wplace(sizeof(int) * scan_n);
+  size_t w_cpos = wplace(sizeof(int) * scan_n);
   size_t w_leaf = wplace(box_bytes * (size_t)chunk);
   size_t w_lflag = wplace(sizeof(int) * (size_t)chunk);
   size_t w_lpos = wplace(sizeof(int) * (size_t)chunk);
   size_t w_leaves = wplace(box_bytes * (size_t)chunk);
   size_t w_cub = wplace(cub_bytes + 256);
-  // persistent search: per-CTA stacks and leaf lists
-  const int grid_max = ctx->search_ctas;
-  long long cta_cap = (long long)(((size_t)6 << 30) / ((size_t)grid_max * box_bytes));
-  if (cta_cap > 65536) cta_cap = 65536;
-  if (cta_cap < 4 * SEARCH_THREADS) cta_cap = 4 * SEARCH_THREADS;
-  size_t w_cstack = wplace(box_bytes * (size_t)cta_cap * grid_max);
-  size_t w_cleaf = wplace(box_bytes * (size_t)SEARCH_THREADS * grid_max);
-  size_t w_tctr = wplace(sizeof(int) * 8);
-  // redistribution buffer: the dump of one launch is the task list of the
-  // next; it alternates with the pre-split stack (both cap_boxes)
-  size_t w_dump = wplace(box_bytes * cap_boxes);
-  const long long dump_cap = (long long)cap_boxes;
+  size_t w_cls[2][6];
+  long long unit_cap[2];
+  for (int c = 0; c < 2; ++c) {
+    const int units = ctx->units[c];
+    long long cap = (long long)(((size_t)4 << 30) / ((size_t)units * cbytes[c]));
+    if (cap > 16384) cap = 16384;
+    if (cap < 8 * 32) cap = 8 * 32;
+    if (lim && lim->unit_stack > 0) cap = lim->unit_stack < 32 ? 32 : lim->unit_stack;
+    unit_cap[c] = cap;
+    w_cls[c][0] = wplace(cbytes[c] * cls_cap[c]);                    // tasks
+    w_cls[c][1] = wplace(cbytes[c] * cls_cap[c]);                    // dump
+    w_cls[c][2] = wplace(cbytes[c] * (size_t)cap * units);           // unit stacks
+    w_cls[c][3] = wplace(cbytes[c] * (size_t)32 * units);            // unit leaf lists
+    w_cls[c][4] = wplace(sizeof(int) * 8);                           // control block
+  }
   rc = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, w);
   if (rc) return rc;
   char* wb = static_cast<char*>(ctx->d_work);
@@ -801,15 +1034,25 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   int* lpos = reinterpret_cast<int*>(wb + w_lpos);
   char* leaves = wb + w_leaves;
   void* cub_tmp = wb + w_cub;
-  void* cta_stacks = wb + w_cstack;
-  void* cta_leaves = wb + w_cleaf;
-  int* ctl = reinterpret_cast<int*>(wb + w_tctr);
-  void* cta_dump = wb + w_dump;
-  // pre-split until every CTA of the persistent search has a task
-  const long long presplit_target = lim && lim->chunk < 0 ? 0 : (long long)grid_max;
+  ClassRun cls[2];
+  for (int c = 0; c < 2; ++c) {
+    cls[c].tasks = wb + w_cls[c][0];
+    cls[c].dump = wb + w_cls[c][1];
+    cls[c].stacks = wb + w_cls[c][2];
+    cls[c].leafbuf = wb + w_cls[c][3];
+    cls[c].ctl = reinterpret_cast<int*>(wb + w_cls[c][4]);
+    cls[c].cap = unit_cap[c];
+    cls[c].ntasks = 0;
+    cls[c].launches = 0;
+    cls[c].ms = 0.0;
+  }
+  // pre-split until every unit of the larger persistent grid has a task
+  const long long presplit_target =
+      lim && lim->chunk < 0 ? 0
+                            : (long long)(ctx->units[1] > ctx->units[0] ? ctx->units[1] : ctx->units[0]);
 
   k_roots<<<(nprob + 127) / 128, 128, 0, s>>>(D, nprob, stack);
-    ++launches;
+  ++launches;
   CK(cudaGetLastError());
   long long top = nprob;
   int64_t rounds = 0;
@@ -854,14 +1097,14 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
       k_scatter<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(
           child, cflag, cpos, nc, static_cast<char*>(stack) + (size_t)top * box_bytes, box_bytes,
           d_counts);
-    ++launches;
+      ++launches;
       CK(cudaGetLastError());
       tb = cub_bytes;
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, lflag, lpos, (int)n, s));
       ++launches;
       k_scatter<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(leafst, lflag, lpos, n, leaves,
                                                              box_bytes, d_counts + 1);
-    ++launches;
+      ++launches;
       CK(cudaGetLastError());
     }
     CK(cudaMemcpyAsync(h_counts, d_counts, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -873,8 +1116,8 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     bb_ms += ms;
     if (nleaf > 0) {
       CK(cudaEventRecord(ctx->ev[2], s));
-      k_leaf<<<(unsigned)nleaf, 256, 0, s>>>(D, leaves, (int)nleaf, d_st);
-    ++launches;
+      k_leaf<<<(unsigned)((nleaf + 3) / 4), 128, 0, s>>>(D, leaves, (int)nleaf, d_st);
+      ++launches;
       CK(cudaGetLastError());
       CK(cudaEventRecord(ctx->ev[3], s));
       CK(cudaEventSynchronize(ctx->ev[3]));
@@ -892,54 +1135,117 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
       }
     }
   }
+  // ---- split the remaining boxes into the two classes' task lists
+  if (!budget_hit && top > 0) {
+    if ((size_t)top > cls_cap[0] || (size_t)top > cls_cap[1]) {
+      budget_hit = true;
+    } else {
+      for (int c = 0; c < 2; ++c) {
+        k_class_flags<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, stack, top, c, cflag);
+        ++launches;
+        CK(cudaGetLastError());
+        size_t tb = cub_bytes;
+        CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, cflag, cpos, (int)top, s));
+        ++launches;
+        if (c == 0)
+          k_to_class<i128><<<(unsigned)((top + 127) / 128), 128, 0, s>>>(
+              D, static_cast<const char*>(stack), cflag, cpos, top,
+              static_cast<char*>(cls[c].tasks), d_counts + 2 + c);
+        else
+          k_to_class<int64_t><<<(unsigned)((top + 127) / 128), 128, 0, s>>>(
+              D, static_cast<const char*>(stack), cflag, cpos, top,
+              static_cast<char*>(cls[c].tasks), d_counts + 2 + c);
+        ++launches;
+        CK(cudaGetLastError());
+      }
+      CK(cudaMemcpyAsync(h_counts, d_counts + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      cls[0].ntasks = h_counts[0];
+      cls[1].ntasks = h_counts[1];
+      top = 0;
+    }
+  }
+  // ---- persistent search: both classes concurrently, bulk-synchronous
+  // redistribution of dumped subtrees between launches
+  CK(cudaEventRecord(ctx->ev[5], s));
+  for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(ctx->side[c], ctx->ev[5], 0));
   double search_ms = 0.0;
   int search_launches = 0;
-  void* tasks_buf = stack;
-  void* dump_buf = cta_dump;
-  while (!budget_hit && top > 0) {
+  while (!budget_hit && (cls[0].ntasks > 0 || cls[1].ntasks > 0)) {
     double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     double left = max_seconds - el;
     if (left <= 0) {
       budget_hit = true;
       break;
     }
-    // the wall budget is checked on the device against %globaltimer, stamped
-    // stream-ordered just before the launch
-    CK(cudaMemsetAsync(ctl, 0, sizeof(int) * 8, s));
-    k_stamp<<<1, 1, 0, s>>>(reinterpret_cast<unsigned long long*>(ctl + 4));
-    ++launches;
-    // always the full persistent grid: CTAs without a task idle at once,
-    // which is what triggers redistribution of a lone deep subtree
-    int grid = grid_max;
     CK(cudaEventRecord(ctx->ev[0], s));
-    k_search<<<grid, SEARCH_THREADS, 0, s>>>(
-        D, tasks_buf, (int)top, ctl, cta_stacks, cta_cap, cta_leaves, K, leaf_volume,
-        (unsigned long long)(left * 1e9), (unsigned long long)200000, dump_buf, dump_cap,
-        d_pend, d_st);
-    ++launches;
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(ctx->ev[1], s));
-    long long dumped = 0;
-    CK(cudaMemcpyAsync(&dumped, ctl + 2, sizeof(long long), cudaMemcpyDeviceToHost, s));
-    CK(cudaEventSynchronize(ctx->ev[1]));
-    CK(cudaStreamSynchronize(s));
+    for (int c = 0; c < 2; ++c) {
+      if (cls[c].ntasks <= 0) continue;
+      cudaStream_t cs = ctx->side[c];
+      CK(cudaStreamWaitEvent(cs, ctx->ev[0], 0));
+      CK(cudaMemsetAsync(cls[c].ctl, 0, sizeof(int) * 8, cs));
+      // the wall budget is checked on the device against %globaltimer,
+      // stamped stream-ordered just before the launch
+      k_stamp<<<1, 1, 0, cs>>>(reinterpret_cast<unsigned long long*>(cls[c].ctl + 4));
+      ++launches;
+      SearchArgs A;
+      A.tasks = cls[c].tasks;
+      A.ntasks = (int)cls[c].ntasks;
+      A.ctl = cls[c].ctl;
+      A.stacks = cls[c].stacks;
+      A.cap = cls[c].cap;
+      A.leafbuf = cls[c].leafbuf;
+      A.K = K;
+      A.leaf_volume = leaf_volume;
+      A.budget_ns = (unsigned long long)(left * 1e9);
+      A.slice_ns = 200000ull;
+      A.dump = cls[c].dump;
+      A.dump_cap = (long long)cls_cap[c];
+      A.box_bytes = cbytes[c];
+      A.pending = d_pend;
+      A.st = d_st;
+      A.units = ctx->units[c];
+      // always the full persistent grid: units without a task idle at once,
+      // which is what triggers redistribution of a lone deep subtree
+      if (c == 0) k_search<i128><<<ctx->ctas[0], SEARCH_THREADS, 0, cs>>>(D, A);
+      else k_search<int64_t><<<ctx->ctas[1], SEARCH_THREADS, 0, cs>>>(D, A);
+      ++launches;
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(h_counts + 4 + 2 * c, cls[c].ctl + 2, sizeof(long long),
+                         cudaMemcpyDeviceToHost, cs));
+      CK(cudaEventRecord(ctx->ev[6 + c], cs));
+      cls[c].launches++;
+    }
+    for (int c = 0; c < 2; ++c) {
+      if (cls[c].ntasks <= 0) continue;
+      CK(cudaEventSynchronize(ctx->ev[6 + c]));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[6 + c]);
+      cls[c].ms += ms;
+      long long dumped = *reinterpret_cast<long long*>(h_counts + 4 + 2 * c);
+      cls[c].ntasks = dumped;
+      void* tmp = cls[c].tasks;
+      cls[c].tasks = cls[c].dump;
+      cls[c].dump = tmp;
+      CK(cudaStreamWaitEvent(s, ctx->ev[6 + c], 0));
+    }
     float ms = 0.f;
+    CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaEventSynchronize(ctx->ev[1]));
     cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
     search_ms += ms;
     ++search_launches;
-    top = dumped;
-    void* tmp = tasks_buf;
-    tasks_buf = dump_buf;
-    dump_buf = tmp;
   }
-  if (budget_hit && top > 0 && tasks_buf != stack) {
-    k_mark_pending<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, tasks_buf, top, d_pend);
-    ++launches;
-    CK(cudaGetLastError());
-    top = 0;
+  for (int c = 0; c < 2; ++c) {
+    if (budget_hit && cls[c].ntasks > 0) {
+      k_mark_pending<<<(unsigned)((cls[c].ntasks + 255) / 256), 256, 0, s>>>(
+          cls[c].tasks, cbytes[c], cls[c].ntasks, d_pend);
+      ++launches;
+      CK(cudaGetLastError());
+    }
   }
   if (budget_hit && top > 0) {
-    k_mark_pending<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, stack, top, d_pend);
+    k_mark_pending<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(stack, box_bytes, top, d_pend);
     ++launches;
     CK(cudaGetLastError());
   }

@@ -18,6 +18,7 @@ LIB_NAME = "libmk_b200.so"
 DEFAULT_LIB = os.path.join(HERE, LIB_NAME)
 
 MK_UNSAT, MK_SAT, MK_UNKNOWN = 0, 1, 2
+MK_PF_NARROW = 1
 STATUS_NAME = {MK_UNSAT: "unsat", MK_SAT: "sat", MK_UNKNOWN: "unknown"}
 
 EXPORTS = ("mk_abi_version", "mk_device_count", "mk_ctx_create", "mk_ctx_destroy",
@@ -36,7 +37,7 @@ INSN = np.dtype([("op", "<u2"), ("dst", "<u2"), ("a", "<u2"), ("b", "<u2"),
 PROBLEM = np.dtype([("nvars", "<i4"), ("ninsn", "<i4"), ("nregs", "<i4"), ("natoms", "<i4"),
                     ("nconst", "<i4"), ("nrows", "<i4"), ("var_off", "<i4"),
                     ("insn_off", "<i4"), ("const_off", "<i4"), ("atom_off", "<i4"),
-                    ("row_off", "<i4"), ("pad", "<i4"), ("maxmask", "<u8")])
+                    ("row_off", "<i4"), ("flags", "<i4"), ("maxmask", "<u8")])
 ROW = np.dtype([("rel", "<i4"), ("nterms", "<i4"), ("term_off", "<i4"), ("pad", "<i4"),
                 ("c0", I128)])
 ROW_TERM = np.dtype([("var", "<i4"), ("pad0", "<i4"), ("pad1", "<i8"), ("coef", I128)])
@@ -59,7 +60,8 @@ class ProblemSet(ctypes.Structure):
 class Limits(ctypes.Structure):
     _fields_ = [("max_rounds", ctypes.c_int64), ("max_boxes", ctypes.c_int64),
                 ("max_seconds", ctypes.c_double), ("split_k", ctypes.c_int32),
-                ("chunk", ctypes.c_int32), ("leaf_volume", ctypes.c_int64)]
+                ("chunk", ctypes.c_int32), ("leaf_volume", ctypes.c_int64),
+                ("unit_stack", ctypes.c_int64)]
 
 
 class Stats(ctypes.Structure):
@@ -152,6 +154,7 @@ class PackedSet:
                 if mx:
                     m |= 1 << k
             rec["maxmask"] = m
+            rec["flags"] = MK_PF_NARROW if getattr(p, "narrow", False) else 0
             lo.extend(p.lo)
             hi.extend(p.hi)
             insns.extend(p.insns)
@@ -227,7 +230,7 @@ class Engine:
 
     def solve_packed(self, packed: PackedSet, limits: Optional[dict] = None
                      ) -> List[Tuple[str, Optional[List[int]]]]:
-        lim = Limits(0, 0, 0.0, 0, 0, 0)
+        lim = Limits(0, 0, 0.0, 0, 0, 0, 0)
         for k, v in (limits or {}).items():
             setattr(lim, k, v)
         P = len(packed.problems)
@@ -279,7 +282,7 @@ class ResidentSet:
         self.point = np.zeros(max(packed.nvar_total, 1), dtype=I128)
 
     def run(self, limits: Optional[dict] = None) -> dict:
-        lim = Limits(0, 0, 0.0, 0, 0, 0)
+        lim = Limits(0, 0, 0.0, 0, 0, 0, 0)
         for k, v in (limits or {}).items():
             setattr(lim, k, v)
         st = Stats()

@@ -36,10 +36,113 @@ extern "C" int mk_ctx_destroy(mk_ctx* ctx) {
 extern "C" const char* mk_last_error(const mk_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 
 namespace {
+template <typename V>
 struct EBox {
   int prob;
-  std::vector<i128> lo, hi;
+  std::vector<V> lo, hi;
 };
+
+// one problem, serial depth-first in the device's order; V = int64_t for
+// problems flagged MK_PF_NARROW, i128 otherwise (the device's dispatch)
+template <typename V>
+void solve_problem(const mk_problem_set* set, int pid, int K, long long leaf_volume,
+                   double max_seconds, int64_t max_boxes,
+                   std::chrono::steady_clock::time_point t0, mk_stats& st, int& has, int& err,
+                   int& pend, std::vector<V>& best) {
+  typedef typename MkNum<V>::U U;
+  const mk_problem& p = set->probs[pid];
+  MkProb P = mk_prob_view(set->probs, pid, set->insns, set->consts, set->atom_regs,
+                          set->atom_masks, set->rows, set->row_terms);
+  std::vector<MkIvT<V>> R(MK_MAXR);
+  std::vector<MkCvT<V>> C(MK_MAXR);
+  const int nv = p.nvars;
+  std::vector<EBox<V>> stack;
+  EBox<V> root;
+  root.prob = pid;
+  for (int i = 0; i < nv; ++i) {
+    root.lo.push_back(MkNum<V>::ld(set->var_lo[p.var_off + i]));
+    root.hi.push_back(MkNum<V>::ld(set->var_hi[p.var_off + i]));
+  }
+  stack.push_back(root);
+  while (!stack.empty()) {
+    double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > max_seconds || st.boxes > max_boxes) {
+      pend = 1;
+      break;
+    }
+    EBox<V> b = stack.back();
+    stack.pop_back();
+    st.boxes++;
+    V c[MK_MAXV];
+    mk_corner(b.lo.data(), b.hi.data(), nv, p.maxmask, c);
+    if (has && !mk_lex_better(c, best.data(), nv, p.maxmask)) {
+      st.covered += mk_volume_f(b.lo.data(), b.hi.data(), nv);
+      continue;
+    }
+    double vol0 = mk_volume_f(b.lo.data(), b.hi.data(), nv);
+    if (!mk_contract(P, b.lo.data(), b.hi.data(), 4)) {
+      st.covered += vol0;
+      continue;
+    }
+    int64_t cnt = 0;
+    MkBoxVerdict v = mk_eval_box(P, b.lo.data(), b.hi.data(), R.data(), &cnt);
+    st.insns_bb += cnt;
+    if (v.any_false) {
+      st.covered += vol0;
+      continue;
+    }
+    if (v.all_true) {
+      mk_corner(b.lo.data(), b.hi.data(), nv, p.maxmask, c);
+      if (!has || mk_lex_better(c, best.data(), nv, p.maxmask)) {
+        best.assign(c, c + nv);
+        has = 1;
+      }
+      st.covered += vol0;
+      continue;
+    }
+    long long vol = mk_volume(b.lo.data(), b.hi.data(), nv);
+    if (vol <= leaf_volume) {
+      st.leaves++;
+      st.covered += (double)vol;
+      if (has) {
+        mk_corner(b.lo.data(), b.hi.data(), nv, p.maxmask, c);
+        if (!mk_lex_better(c, best.data(), nv, p.maxmask)) continue;
+      }
+      V x[MK_MAXV];
+      bool ovf = false;
+      int64_t c2 = 0;
+      for (long long idx = 0; idx < vol; ++idx) {
+        mk_decode(b.lo.data(), b.hi.data(), nv, p.maxmask, (uint64_t)idx, x);
+        st.points++;
+        if (mk_eval_point(P, x, C.data(), &ovf, &c2)) {
+          if (!has || mk_lex_better(x, best.data(), nv, p.maxmask)) {
+            best.assign(x, x + nv);
+            has = 1;
+          }
+          break;
+        }
+      }
+      st.insns_leaf += c2;
+      if (ovf) err = 1;
+      continue;
+    }
+    int sv = mk_pick_split(b.lo.data(), b.hi.data(), nv, v.und_mask, has != 0);
+    if (sv < 0) {
+      err = 1;
+      continue;
+    }
+    U size = (U)(b.hi[sv] - b.lo[sv]) + 1;
+    int m = size < (U)K ? (int)size : K;
+    bool mx = (p.maxmask >> sv) & 1;
+    // push worst first so the best piece is popped next
+    for (int t = m - 1; t >= 0; --t) {
+      EBox<V> ch = b;
+      mk_piece(b.lo[sv], b.hi[sv], m, t, mx, &ch.lo[sv], &ch.hi[sv]);
+      stack.push_back(ch);
+    }
+    st.rounds++;
+  }
+}
 }  // namespace
 
 extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_limits* lim,
@@ -52,109 +155,30 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   long long leaf_volume = lim && lim->leaf_volume > 0 ? lim->leaf_volume : 4096;
   double max_seconds = lim && lim->max_seconds > 0 ? lim->max_seconds : 30.0;
   int64_t max_boxes = lim && lim->max_boxes > 0 ? lim->max_boxes : (int64_t)50000000;
-  std::vector<int> has(nprob, 0), err(nprob, 0), pend(nprob, 0);
-  std::vector<std::vector<i128>> best(nprob);
-  std::vector<MkIv> R(MK_MAXR);
-  std::vector<MkCv> C(MK_MAXR);
   for (int pid = 0; pid < nprob; ++pid) {
     const mk_problem& p = set->probs[pid];
     if (p.nvars > MK_MAXV || p.nregs > MK_MAXR) {
       ctx->err = "problem exceeds MK_MAXV symbols or MK_MAXR registers";
       return MK_EINVAL;
     }
-    MkProb P = mk_prob_view(set->probs, pid, set->insns, set->consts, set->atom_regs,
-                            set->atom_masks, set->rows, set->row_terms);
+  }
+  for (int pid = 0; pid < nprob; ++pid) {
+    const mk_problem& p = set->probs[pid];
     const int nv = p.nvars;
-    std::vector<EBox> stack;
-    EBox root;
-    root.prob = pid;
-    for (int i = 0; i < nv; ++i) {
-      root.lo.push_back(mk_ld(set->var_lo[p.var_off + i]));
-      root.hi.push_back(mk_ld(set->var_hi[p.var_off + i]));
+    int has = 0, err = 0, pend = 0;
+    std::vector<i128> best(nv, 0);
+    if (p.flags & MK_PF_NARROW) {
+      std::vector<int64_t> b64;
+      solve_problem<int64_t>(set, pid, K, leaf_volume, max_seconds, max_boxes, t0, st, has, err,
+                             pend, b64);
+      for (int i = 0; i < (int)b64.size(); ++i) best[i] = b64[i];
+    } else {
+      solve_problem<i128>(set, pid, K, leaf_volume, max_seconds, max_boxes, t0, st, has, err,
+                          pend, best);
     }
-    stack.push_back(root);
-    while (!stack.empty()) {
-      double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      if (el > max_seconds || st.boxes > max_boxes) {
-        pend[pid] = 1;
-        break;
-      }
-      EBox b = stack.back();
-      stack.pop_back();
-      st.boxes++;
-      i128 c[MK_MAXV];
-      mk_corner(b.lo.data(), b.hi.data(), nv, p.maxmask, c);
-      if (has[pid] && !mk_lex_better(c, best[pid].data(), nv, p.maxmask)) {
-        st.covered += mk_volume_f(b.lo.data(), b.hi.data(), nv);
-        continue;
-      }
-      double vol0 = mk_volume_f(b.lo.data(), b.hi.data(), nv);
-      if (!mk_contract(P, b.lo.data(), b.hi.data(), 4)) {
-        st.covered += vol0;
-        continue;
-      }
-      int64_t cnt = 0;
-      MkBoxVerdict v = mk_eval_box(P, b.lo.data(), b.hi.data(), R.data(), &cnt);
-      st.insns_bb += cnt;
-      if (v.any_false) {
-        st.covered += vol0;
-        continue;
-      }
-      if (v.all_true) {
-        mk_corner(b.lo.data(), b.hi.data(), nv, p.maxmask, c);
-        if (!has[pid] || mk_lex_better(c, best[pid].data(), nv, p.maxmask)) {
-          best[pid].assign(c, c + nv);
-          has[pid] = 1;
-        }
-        st.covered += vol0;
-        continue;
-      }
-      long long vol = mk_volume(b.lo.data(), b.hi.data(), nv);
-      if (vol <= leaf_volume) {
-        st.leaves++;
-        st.covered += (double)vol;
-        if (has[pid]) {
-          mk_corner(b.lo.data(), b.hi.data(), nv, p.maxmask, c);
-          if (!mk_lex_better(c, best[pid].data(), nv, p.maxmask)) continue;
-        }
-        i128 x[MK_MAXV];
-        bool ovf = false;
-        int64_t c2 = 0;
-        for (long long idx = 0; idx < vol; ++idx) {
-          mk_decode(b.lo.data(), b.hi.data(), nv, p.maxmask, (uint64_t)idx, x);
-          st.points++;
-          if (mk_eval_point(P, x, C.data(), &ovf, &c2)) {
-            if (!has[pid] || mk_lex_better(x, best[pid].data(), nv, p.maxmask)) {
-              best[pid].assign(x, x + nv);
-              has[pid] = 1;
-            }
-            break;
-          }
-        }
-        st.insns_leaf += c2;
-        if (ovf) err[pid] = 1;
-        continue;
-      }
-      int sv = mk_pick_split(b.lo.data(), b.hi.data(), nv, v.und_mask, has[pid] != 0);
-      if (sv < 0) {
-        err[pid] = 1;
-        continue;
-      }
-      i128 size = b.hi[sv] - b.lo[sv] + 1;
-      int m = size < (i128)K ? (int)size : K;
-      bool mx = (p.maxmask >> sv) & 1;
-      // push worst first so the best piece is popped next
-      for (int t = m - 1; t >= 0; --t) {
-        EBox ch = b;
-        mk_piece(b.lo[sv], b.hi[sv], m, t, mx, &ch.lo[sv], &ch.hi[sv]);
-        stack.push_back(ch);
-      }
-      st.rounds++;
-    }
-    if (err[pid] || pend[pid]) status[pid] = MK_UNKNOWN;
-    else status[pid] = has[pid] ? MK_SAT : MK_UNSAT;
-    for (int i = 0; i < nv; ++i)
-      point[p.var_off + i] = mk_st(has[pid] ? best[pid][i] : (i128)0);
+    if (err || pend) status[pid] = MK_UNKNOWN;
+    else status[pid] = has ? MK_SAT : MK_UNSAT;
+    for (int i = 0; i < nv; ++i) point[p.var_off + i] = mk_st(has ? best[i] : (i128)0);
   }
   st.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (stats) *stats = st;

@@ -38,3 +38,31 @@ def test_engine_loaded_from_tree():
     lib = native.load_library()
     assert native.DEFAULT_LIB in [p for p in native._LIBS]
     assert lib.mk_abi_version() == 1
+
+
+@pytest.mark.parametrize("name", ["paged_attention_v1", "fused_add_rms_norm", "racy"])
+def test_batch_equals_solo(checker, name):
+    """Every problem's verdict and lexicographic optimum must not depend on
+    what else shares the launch (task redistribution, stack spills and the
+    two concurrent value-type classes all move boxes between units)."""
+    from paper_2603_24595_b200.engine import compile_all
+
+    probs = [p for c, _ in compile_all(queries(load(name))) if c for p in c.problems]
+    eng = checker.engine
+    batch = eng.solve(probs, {"max_seconds": 600.0})
+    solo = [eng.solve([p], {"max_seconds": 600.0})[0] for p in probs]
+    assert [i for i, (a, b) in enumerate(zip(batch, solo)) if a != b] == []
+    assert all(s != "unknown" for s, _ in batch)
+
+
+def test_tiny_stacks_spill_without_loss(checker):
+    """Per-unit stacks far too small for the search force constant spills to
+    the next launch's task list: verdicts and optima must be unchanged."""
+    from paper_2603_24595_b200.engine import compile_all
+
+    doc = load("fused_add_rms_norm")
+    probs = [p for c, _ in compile_all(queries(doc)) if c for p in c.problems]
+    eng = checker.engine
+    ref = eng.solve(probs, {"max_seconds": 600.0})
+    tiny = eng.solve(probs, {"max_seconds": 600.0, "unit_stack": 600})
+    assert tiny == ref
