@@ -534,25 +534,22 @@ struct SearchArgs {
 enum { TASK_DONE = 0, TASK_ABORT = 1, TASK_DUMPED = 2 };
 
 // copy the unit's stack [0, top) to the global dump buffer; returns false
-// (and reserves nothing) when the dump buffer cannot take it
+// when the dump buffer cannot take it.  The reservation is one atomicAdd (no
+// CAS retry storm when every unit dumps at once); a reservation that runs past
+// the buffer end marks its in-range slots empty (prob = -1) so the next
+// launch skips them, and the host clamps the count to the capacity.
 __device__ bool dump_stack(const SearchArgs& A, const DevSet& D, char* stack, long long top) {
   const int lane = threadIdx.x & 31;
-  unsigned long long off = ~0ull;
-  if (lane == 0) {
-    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(A.ctl + 2);
-    unsigned long long cur = *((volatile unsigned long long*)ctr);
-    for (;;) {
-      if (cur + (unsigned long long)top > (unsigned long long)A.dump_cap) break;
-      unsigned long long prev = atomicCAS(ctr, cur, cur + (unsigned long long)top);
-      if (prev == cur) {
-        off = cur;
-        break;
-      }
-      cur = prev;
-    }
-  }
+  unsigned long long off = 0;
+  if (lane == 0)
+    off = atomicAdd(reinterpret_cast<unsigned long long*>(A.ctl + 2), (unsigned long long)top);
   off = __shfl_sync(FULL, off, 0);
-  if (off == ~0ull) return false;
+  const unsigned long long cap = (unsigned long long)A.dump_cap;
+  if (off + (unsigned long long)top > cap) {
+    for (unsigned long long i = off + lane; i < cap; i += 32)
+      box_at(A.dump, A.box_bytes, (size_t)i)->prob = -1;
+    return false;
+  }
   const size_t words = A.box_bytes / sizeof(int4);
   const int4* src = reinterpret_cast<const int4*>(stack);
   int4* dst = reinterpret_cast<int4*>(static_cast<char*>(A.dump) + (size_t)off * A.box_bytes);
@@ -687,6 +684,7 @@ __global__ void __launch_bounds__(SEARCH_THREADS, MinBlocks<V>::value)
     }
     __syncwarp();
     const int pid = tb->prob;
+    if (pid < 0) continue;  // hole left by a dump that did not fit
     const mk_problem p = D.probs[pid];
     if (globaltimer_ns() > t_start + A.budget_ns) {
       if (lane == 0) A.pending[pid] = 1;
@@ -706,7 +704,7 @@ __global__ void k_mark_pending(const void* stack, size_t box_bytes, long long to
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= top) return;
   const Box* b = box_at(const_cast<void*>(stack), box_bytes, (size_t)i);
-  pending[b->prob] = 1;
+  if (b->prob >= 0) pending[b->prob] = 1;
 }
 
 // flag[i] = box i belongs to a problem of class `narrow` (1) / wide (0)
@@ -1223,6 +1221,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
       cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[6 + c]);
       cls[c].ms += ms;
       long long dumped = *reinterpret_cast<long long*>(h_counts + 4 + 2 * c);
+      if (dumped > (long long)cls_cap[c]) dumped = (long long)cls_cap[c];
       cls[c].ntasks = dumped;
       void* tmp = cls[c].tasks;
       cls[c].tasks = cls[c].dump;

@@ -10,6 +10,7 @@ reference's meaning: ``sat`` + canonical witness (engine/report.py:147-174),
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Dict, List, Optional, Sequence, Tuple
@@ -17,6 +18,7 @@ from typing import Callable, Dict, List, Optional, Sequence, Tuple
 from . import ir
 from .compiler import CompileError, CompiledQuery, compile_query
 from .native import Engine, PackedSet
+from .order import OriginLookup
 
 DEFAULT_LIMITS = {"max_seconds": 30.0}   # Budget.query_timeout_s (engine/state.py:38)
 
@@ -38,30 +40,91 @@ class BatchStats:
     device: Dict[str, float] = field(default_factory=dict)
 
 
+def _compile_one(item) -> Tuple[Optional[CompiledQuery], Optional[str]]:
+    assertions, origin_of = item
+    try:
+        return compile_query(assertions, origin_of), None
+    except CompileError as exc:
+        return None, str(exc)
+
+
 def compile_all(queries: Sequence[Tuple[Sequence[ir.Node], Callable[[str], str]]]
                 ) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
-    out = []
-    for assertions, origin_of in queries:
-        try:
-            out.append((compile_query(assertions, origin_of), None))
-        except CompileError as exc:
-            out.append((None, str(exc)))
-    return out
+    return [_compile_one(q) for q in queries]
+
+
+def _portable(query):
+    """(assertions, origin map) with a picklable origin lookup."""
+    assertions, origin_of = query
+    if isinstance(origin_of, OriginLookup):
+        return assertions, origin_of
+    names: Dict[str, str] = {}
+    for a in assertions:
+        ir.symbols_of(a, names)
+    return assertions, OriginLookup({n.rstrip("'"): origin_of(n) for n in names})
+
+
+class CompilePool:
+    """Host-side site compilation across worker processes.
+
+    Sites are independent, so a batch of queries is compiled in parallel on
+    the host cores (the compiler is pure Python; one process per core side
+    steps the GIL).  Workers are forked once per checker and only ever run
+    the pure-Python compiler (they never touch the parent's CUDA context)."""
+
+    def __init__(self, workers: int) -> None:
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+
+        ctx = mp.get_context("fork")
+        self.workers = workers
+        self.pool = ProcessPoolExecutor(workers, mp_context=ctx)
+        # start every worker now, outside any timed region
+        list(self.pool.map(_compile_one, [([], OriginLookup({}))] * workers))
+
+    def compile(self, queries) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
+        items = [_portable(q) for q in queries]
+        chunk = max(1, -(-len(items) // (self.workers * 4)))
+        return list(self.pool.map(_compile_one, items, chunksize=chunk))
+
+    def close(self) -> None:
+        self.pool.shutdown(wait=False, cancel_futures=True)
+
+
+def default_workers() -> int:
+    n = os.cpu_count() or 1
+    return max(1, min(16, n // 2))
 
 
 class SiteChecker:
     """Holds one device context; decides compiled queries in batches."""
 
+    # batches at least this large are compiled on the worker pool
+    POOL_MIN_BATCH = 8
+
     def __init__(self, device: int = 0, lib_path: Optional[str] = None,
-                 limits: Optional[dict] = None) -> None:
+                 limits: Optional[dict] = None, compile_workers: Optional[int] = None) -> None:
         self.engine = Engine(device, lib_path)
         self.limits = dict(DEFAULT_LIMITS)
         if limits:
             self.limits.update(limits)
         self.stats = BatchStats()
+        # 0 / 1: compile inline; None: one worker per two host cores
+        self.compile_workers = default_workers() if compile_workers is None else compile_workers
+        self._pool: Optional[CompilePool] = None
 
     def close(self) -> None:
+        if self._pool is not None:
+            self._pool.close()
+            self._pool = None
         self.engine.close()
+
+    def compile(self, queries) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
+        if self.compile_workers > 1 and len(queries) >= self.POOL_MIN_BATCH:
+            if self._pool is None:
+                self._pool = CompilePool(self.compile_workers)
+            return self._pool.compile(queries)
+        return compile_all(queries)
 
     def pack(self, compiled: Sequence[Optional[CompiledQuery]]) -> Tuple[PackedSet, List[int]]:
         problems, offsets = [], []
@@ -105,7 +168,7 @@ class SiteChecker:
     def check_queries(self, queries: Sequence[Tuple[Sequence[ir.Node], Callable[[str], str]]]
                       ) -> List[QueryResult]:
         t0 = time.perf_counter()
-        compiled = compile_all(queries)
+        compiled = self.compile(queries)
         self.stats.compile_s += time.perf_counter() - t0
         return self.decide(compiled)
 

@@ -22,10 +22,21 @@ ORIGIN_SCALAR = "scalar-arg"   # engine/state.py:29
 ORIGIN_LOOP = "loop-index"     # engine/state.py:26
 
 
+class OriginLookup:
+    """``origin_of`` over a recorded {symbol: origin} map (picklable, so a
+    query can be compiled in a worker process)."""
+
+    __slots__ = ("origins",)
+
+    def __init__(self, origins: Mapping[str, str]) -> None:
+        self.origins = dict(origins)
+
+    def __call__(self, name: str) -> str:
+        return self.origins.get(name.rstrip("'"), "unknown")
+
+
 def origin_lookup(origins: Mapping[str, str]) -> Callable[[str], str]:
-    def origin_of(name: str) -> str:
-        return origins.get(name.rstrip("'"), "unknown")
-    return origin_of
+    return OriginLookup(origins)
 
 
 def optimization_order(names: Iterable[str],

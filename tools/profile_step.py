@@ -1,0 +1,33 @@
+"""One resident checking step between cudaProfilerStart/Stop, for
+``ncu --profile-from-start off`` (tools/gpu_profile.sh).  Prints the step's
+engine statistics as one JSON line so the ncu counters can be normalised
+per box / per instance (tools/summarize_ncu.py)."""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import torch  # noqa: E402
+from goldens import load, queries  # noqa: E402
+from paper_2603_24595_b200.engine import SiteChecker, compile_all  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "rotary_embedding"
+torch.cuda.set_device(0)
+chk = SiteChecker(device=0, compile_workers=0)
+compiled = compile_all(queries(load(name)))
+packed, _ = chk.pack([c for c, _ in compiled])
+res = chk.engine.upload(packed)
+lim = {"max_seconds": 600.0}
+for _ in range(3):
+    res.run(lim)
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
+st = res.run(lim)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
+print(json.dumps({"workload": name, "stats": st}))
+res.free()
+chk.close()
