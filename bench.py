@@ -151,13 +151,30 @@ def _reference_checker_sample(queries, per_site, budget_s):
     return done, sum(per_site[:done]), dt
 
 
+def _ref_job(name):
+    """One reference job (kernel x model entry): every site query through the
+    reference's Solver.check + canonicalize_witness; returns seconds."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from refbridge import reference_check_queries
+
+    _, queries = _load_workload(name)
+    t0 = time.perf_counter()
+    done, _ = reference_check_queries(queries)
+    assert done == len(queries)
+    return time.perf_counter() - t0
+
+
 def run_reference(args):
-    """--impl reference: the unmodified reference checker on the host cores."""
+    """--impl reference: the unmodified reference checker on the host cores.
+    At N ranks the arm checks the same N corpus entries as the B200 arm, one
+    reference process per entry (the reference is single-threaded per job,
+    SURVEY.md section 8d); only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "tools"))
-    from refbridge import have_reference, reference_check_queries
+    from refbridge import have_reference
 
     if not have_reference():
         print(json.dumps({"impl": "reference",
@@ -165,35 +182,63 @@ def run_reference(args):
         return
     from paper_2603_24595_b200.engine import compile_all
 
-    doc, queries = _load_workload(args.workload)
-    per_site = _instances(compile_all(queries))
-    total = sum(per_site)
+    if world > 1:
+        names = ([args.workload] * world if args.workload != DEFAULT_WORKLOAD
+                 else [CORPUS[i % len(CORPUS)] for i in range(world)])
+    else:
+        names = [args.workload]
+    total = 0
+    nsites = 0
+    for n in names:
+        _, queries = _load_workload(n)
+        total += sum(_instances(compile_all(queries)))
+        nsites += len(queries)
+    cores = min(len(names), os.cpu_count() or 1)
+    pool = None
+    if len(names) > 1:
+        import multiprocessing as mp
+
+        pool = mp.get_context("fork").Pool(cores)
     times = []
     for step in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        done, _ = reference_check_queries(queries)
+        if pool is None:
+            _ref_job(names[0])
+        else:
+            pool.map(_ref_job, names)
         dt = time.perf_counter() - t0
-        assert done == len(queries)
         if step >= args.warmup:
             times.append(dt)
+    if pool is not None:
+        pool.close()
     avg = sum(times) / len(times)
     value = total / avg
     out = {
         "impl": "reference",
         "metric": "checked (thread, input) access instances/sec; time-to-verdict per kernel x model",
-        "value": value, "unit": "instances/s", "n_gpus": args.gpus, "steps": args.steps,
+        "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": avg * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int128 (mathematical integers)",
         "data": "recorded reference site queries", "time_to_verdict_ms": avg * 1e3,
-        "config": {"workload": args.workload, "description": CONFIG_NAMES.get(args.workload),
-                   "sites": len(queries)},
-        "cpu_baseline": {"value": value, "unit": "instances/s", "cores": 1, "kind": "reference",
-                         "sample": f"all {len(queries)} {args.workload} site queries per step, "
-                                   "reference Solver.check + canonicalize_witness, 1 thread"},
+        "config": {"workload": args.workload if world == 1 else "kernel x model corpus",
+                   "description": CONFIG_NAMES.get(args.workload), "entries": names,
+                   "sites": nsites},
+        "cpu_baseline": {"value": value, "unit": "instances/s", "cores": cores,
+                         "kind": "reference",
+                         "sample": f"all {nsites} site queries of {len(names)} corpus entr"
+                                   f"{'y' if len(names) == 1 else 'ies'} per step, reference "
+                                   "Solver.check + canonicalize_witness, one process per entry"},
         "e2e": {"value": value, "unit": "instances/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
+
+
+# BASELINE.json configs[4]: the kernel x model corpus of the rotary port,
+# dealt one entry per rank under torchrun (weak scaling, no data-path
+# collective); entry 0 is the N=1 headline workload (configs[1]).
+CORPUS = ["rotary_embedding", "rotary_llama2_7b", "rotary_mistral_7b", "rotary_llama3_70b",
+          "rotary_qwen2_7b", "rotary_llama2_13b", "rotary_mixtral_8x7b", "rotary_gemma_7b"]
 
 
 def run_b200(args):
@@ -207,10 +252,18 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    from paper_2603_24595_b200 import shard
     from paper_2603_24595_b200.engine import SiteChecker, compile_all
-    from paper_2603_24595_b200.native import PackedSet
 
-    doc, queries = _load_workload(args.workload)
+    if world > 1:
+        if args.workload != DEFAULT_WORKLOAD:
+            names = [args.workload] * world
+        else:
+            names = [CORPUS[i % len(CORPUS)] for i in range(world)]
+    else:
+        names = [args.workload]
+    my_name = names[rank]
+    doc, queries = _load_workload(my_name)
     compiled = compile_all(queries)
     per_site = _instances(compiled)
     instances = sum(per_site)
@@ -229,7 +282,7 @@ def run_b200(args):
     results = chk.decide(compiled, packed, offsets)
     bad = mismatches(doc, results)
     if bad:
-        raise SystemExit(f"parity failure on sites {bad[:10]}")
+        raise SystemExit(f"parity failure on {my_name} sites {bad[:10]}")
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     for _ in range(args.warmup):
@@ -255,20 +308,37 @@ def run_b200(args):
         dist.barrier()
     clk = clocks.stop()
     ms_step = sum(dev_ms) / len(dev_ms)
+    total_instances = float(instances)
     if world > 1:
         t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-    value = world * instances / (ms_step / 1e3)
+        t = torch.tensor([float(instances)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        total_instances = float(t.item())
+    value = total_instances / (ms_step / 1e3)
 
-    # e2e through the public API with host buffers (compile + H2D + search + D2H);
-    # warm-up calls start the host compile workers outside the timed steps
+    # e2e through the public API with host buffers (compile + H2D + search +
+    # D2H + witness assembly); at N>1 the corpus call deals one entry per rank
+    # and all-gathers every result to every rank.  Warm-up calls start the
+    # host compile workers outside the timed steps.
+    entries = None
+    if world > 1:
+        entries = [_load_workload(n)[1] for n in names]
+
+    def e2e_call():
+        if entries is None:
+            return chk.check_queries(queries)
+        return shard.check_corpus(chk, entries)
+
     for _ in range(args.warmup):
-        chk.check_queries(queries)
+        e2e_call()
     e2e_t = []
     for step in range(max(1, args.steps)):
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        res = chk.check_queries(queries)
+        res = e2e_call()
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = sum(e2e_t) / len(e2e_t)
     if world > 1:
@@ -300,7 +370,7 @@ def run_b200(args):
         ops = "bytecode instructions executed (no ncu calibration committed)"
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         try:
             from refbridge import have_reference, reference_check_queries
@@ -324,14 +394,19 @@ def run_b200(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int128 (mathematical integers)",
             "data": "site queries recorded from the reference front end on the workload port",
-            "config": {"workload": args.workload, "description": CONFIG_NAMES.get(args.workload),
-                       "sites": len(queries), "instances_per_step": instances,
+            "config": {"workload": args.workload if world == 1 else "kernel x model corpus",
+                       "description": CONFIG_NAMES.get(args.workload) if world == 1 else
+                       "rotary_embedding port under one model context per rank",
+                       "entries": names,
+                       "sites": len(queries), "instances_per_step": total_instances,
                        "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": f"{world} independent replicas of the kernel x model check"},
+                       "parallelism": "1 GPU" if world == 1 else
+                       f"{world} ranks, one corpus entry each (no data-path collective; "
+                       "results all-gathered in e2e)"},
             "time_to_verdict_ms": ms_step,
             "wall_ms_per_step": 1e3 * sum(wall) / len(wall),
             "evaluated_per_step": {"boxes": stats_acc["boxes"] / n, "points": stats_acc["points"] / n},
-            "e2e": {"value": world * instances / e2e_s, "unit": "instances/s",
+            "e2e": {"value": total_instances / e2e_s, "unit": "instances/s",
                     "h2d_bytes_per_step": packed.host_bytes(),
                     "d2h_bytes_per_step": resident.d2h_bytes(), "ms_per_step": e2e_s * 1e3},
             "roofline": {"bound": "int32-issue", "achieved": achieved / 1e9,

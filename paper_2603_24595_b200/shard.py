@@ -1,0 +1,213 @@
+"""Multi-GPU checking: one process per GPU (torch.distributed), two ways to
+split the work.
+
+``check_corpus``  -- kernel x model sweep (BASELINE.json configs[4]): every
+    corpus entry (one kernel port under one model context, i.e. one site set)
+    is an independent unit; entries are dealt to ranks by estimated cost and
+    each rank decides its own entries with no data-path collective.  One
+    ``all_gather_object`` hands every rank the full result list at the end.
+
+``check_slabbed`` -- one site set, every problem's root box cut into
+    ``world`` slabs along its first splittable symbol; rank r searches slab r
+    (so one hard query uses every GPU).  The per-problem results are combined
+    exactly: the canonical witness is the lexicographic optimum, in witness
+    order, over the slabs' optima (engine/report.py:147-203), ``unknown`` if
+    any slab is undecided, ``unsat`` if every slab is.  The combination is a
+    single all-gather of a fixed-width int64 record per problem (status +
+    128-bit point words), an NCCL collective over NVLink on the GPU path and
+    gloo in the CPU tests.
+
+Both entry points reuse one ``SiteChecker`` per rank; on the GPU path the
+checker is bound to ``cuda:<local_rank>``.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
+
+from . import ir
+from .compiler import CompiledQuery, Problem
+from .engine import QueryResult, SiteChecker
+
+Query = Tuple[Sequence[ir.Node], Callable[[str], str]]
+
+_STATUS = {"unsat": 0, "sat": 1, "unknown": 2}
+_STATUS_NAME = {v: k for k, v in _STATUS.items()}
+_MASK64 = (1 << 64) - 1
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def _world(group=None) -> Tuple[int, int]:
+    dist = _dist()
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+# -- corpus sharding --------------------------------------------------------------------
+
+def entry_cost(queries: Sequence[Query]) -> float:
+    """Static cost estimate of one corpus entry (sites x atoms), used only to
+    balance the deal; any estimate gives the same results."""
+    return float(sum(1 + len(a) for a, _ in queries))
+
+
+def deal(costs: Sequence[float], world: int) -> List[List[int]]:
+    """Longest-processing-time-first assignment of entries to ranks."""
+    loads = [0.0] * world
+    out: List[List[int]] = [[] for _ in range(world)]
+    for i in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        r = min(range(world), key=lambda k: (loads[k], k))
+        out[r].append(i)
+        loads[r] += costs[i]
+    for lst in out:
+        lst.sort()
+    return out
+
+
+def check_corpus(checker: SiteChecker, entries: Sequence[Sequence[Query]], group=None
+                 ) -> List[List[QueryResult]]:
+    """Decide every entry of a kernel x model corpus across the ranks of
+    ``group``; every rank returns the full, ordered result list."""
+    rank, world = _world(group)
+    mine = deal([entry_cost(e) for e in entries], world)[rank]
+    local: Dict[int, List[QueryResult]] = {}
+    for i in mine:
+        local[i] = checker.check_queries(entries[i])
+    if world == 1:
+        return [local[i] for i in range(len(entries))]
+    dist = _dist()
+    gathered: List[Optional[Dict[int, List[QueryResult]]]] = [None] * world
+    dist.all_gather_object(gathered, local, group=group)
+    merged: Dict[int, List[QueryResult]] = {}
+    for part in gathered:
+        merged.update(part or {})
+    return [merged[i] for i in range(len(entries))]
+
+
+# -- slab sharding ----------------------------------------------------------------------
+
+def slab(p: Problem, rank: int, world: int) -> Optional[Problem]:
+    """The rank-th of ``world`` slabs of ``p``'s root box along its first
+    symbol (witness order) with at least two values, pieces ordered best
+    first in that symbol's direction; None when the slab is empty."""
+    v = next((i for i in range(p.nvars) if p.hi[i] > p.lo[i]), None)
+    if v is None:
+        return p if rank == 0 else None
+    size = p.hi[v] - p.lo[v] + 1
+    q, rem = divmod(size, world)
+    j = (world - 1 - rank) if p.maximize[v] else rank   # ascending piece index
+    start = j * q + min(j, rem)
+    length = q + (1 if j < rem else 0)
+    if length <= 0:
+        return None
+    lo, hi = list(p.lo), list(p.hi)
+    lo[v] = p.lo[v] + start
+    hi[v] = lo[v] + length - 1
+    return dataclasses.replace(p, lo=lo, hi=hi)
+
+
+def _better(x: Sequence[int], y: Sequence[int], maximize: Sequence[bool]) -> bool:
+    for a, b, mx in zip(x, y, maximize):
+        if a != b:
+            return a > b if mx else a < b
+    return False
+
+
+def combine_slabs(problems: Sequence[Problem],
+                  per_rank: Sequence[Sequence[Tuple[str, Optional[List[int]]]]]
+                  ) -> List[Tuple[str, Optional[List[int]]]]:
+    """Exact combination of the slab results of every problem."""
+    out = []
+    for k, p in enumerate(problems):
+        rs = [r[k] for r in per_rank]
+        if any(s == "unknown" for s, _ in rs):
+            out.append(("unknown", None))
+            continue
+        best = None
+        for s, pt in rs:
+            if s == "sat" and (best is None or _better(pt, best, p.maximize)):
+                best = pt
+        out.append(("sat", list(best)) if best is not None else ("unsat", None))
+    return out
+
+
+def _encode(problems: Sequence[Problem], results) -> List[int]:
+    rec: List[int] = []
+    for p, (s, pt) in zip(problems, results):
+        rec.append(_STATUS[s])
+        vals = pt if pt is not None else [0] * p.nvars
+        for v in vals:
+            rec.append(v & _MASK64)          # low word
+            rec.append(v >> 64)              # high word (signed)
+    return rec
+
+
+def _decode(problems: Sequence[Problem], rec: Sequence[int]):
+    out, i = [], 0
+    for p in problems:
+        s = _STATUS_NAME[int(rec[i])]
+        i += 1
+        pt = []
+        for _ in range(p.nvars):
+            lo, hi = int(rec[i]) & _MASK64, int(rec[i + 1])
+            pt.append((hi << 64) | lo)
+            i += 2
+        out.append((s, pt if s == "sat" else None))
+    return out
+
+
+def _all_gather_records(rec: List[int], device, group=None) -> List[List[int]]:
+    import torch
+
+    dist = _dist()
+    _, world = _world(group)
+    # int64 words: the low 64-bit halves travel as their two's complement
+    words = [w - (1 << 64) if w >= (1 << 63) else w for w in rec]
+    t = torch.tensor(words, dtype=torch.int64, device=device)
+    outs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(outs, t, group=group)
+    return [[int(x) for x in o.cpu().tolist()] for o in outs]
+
+
+def check_slabbed(checker: SiteChecker, queries: Sequence[Query], group=None,
+                  device=None) -> List[QueryResult]:
+    """Decide one site set with every problem's root box split across the
+    ranks of ``group``; every rank returns the same results."""
+    rank, world = _world(group)
+    compiled = checker.compile(queries)
+    problems: List[Problem] = []
+    offsets: List[int] = []
+    for cq, _ in compiled:
+        offsets.append(len(problems))
+        if cq is not None:
+            problems.extend(cq.problems)
+    mine = [slab(p, rank, world) for p in problems]
+    run = [p for p in mine if p is not None]
+    lim = dict(checker.limits)
+    lim["max_seconds"] = min(checker.limits["max_seconds"] * max(len(queries), 1), 3600.0)
+    solved = checker.engine.solve(run, lim) if run else []
+    it = iter(solved)
+    local = [next(it) if p is not None else ("unsat", None) for p in mine]
+    if world > 1:
+        if device is None:
+            device = "cpu"
+        recs = _all_gather_records(_encode(problems, local), device, group)
+        per_rank = [_decode(problems, r) for r in recs]
+    else:
+        per_rank = [local]
+    results = combine_slabs(problems, per_rank)
+    out: List[QueryResult] = []
+    for (cq, err), off in zip(compiled, offsets):
+        if cq is None:
+            out.append(QueryResult("unknown", {}, err))
+            continue
+        status, witness = cq.assemble(results[off:off + len(cq.problems)])
+        out.append(QueryResult(status, witness))
+    return out
