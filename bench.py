@@ -241,6 +241,40 @@ CORPUS = ["rotary_embedding", "rotary_llama2_7b", "rotary_mistral_7b", "rotary_l
           "rotary_qwen2_7b", "rotary_llama2_13b", "rotary_mixtral_8x7b", "rotary_gemma_7b"]
 
 
+def _race_sweep_line(chk, args, peaks, src):
+    """K2 (sort-based race sweep, include/mk_b200.h mk_race_sweep) on config
+    1's output store (rms_norm, Llama-2-7B hidden 4096: out[blockIdx.x *
+    hidden + idx]) replayed at a full concrete launch: every (thread, loop
+    iteration) access of the launch is generated, radix-sorted by byte
+    offset in HBM and scanned for conflicts.  HBM roofline: algorithmic bytes
+    = 4 x tuple bytes per access / device time."""
+    from paper_2603_24595_b200 import race
+
+    doc, queries = _load_workload("rms_norm")
+    T = args.race_tokens
+    launch = {"BS": 1, "SL": T, "TC": T, "blockDim.x": 1024, "blockDim.y": 1, "blockDim.z": 1,
+              "gridDim.x": T, "gridDim.y": 1, "gridDim.z": 1}
+    progs = [race.race_program(a, o, launch) for s, (a, o) in zip(doc["sites"], queries)
+             if s["site"] == "store_site" and s["line"] == 20]
+    prog = max(progs, key=lambda p: p.instances)
+    for _ in range(2):
+        chk.engine.race_sweep(prog)
+    runs = [chk.engine.race_sweep(prog) for _ in range(3)]
+    ms = sum(r["gen_ms"] + r["sort_ms"] + r["scan_ms"] for r in runs) / len(runs)
+    r = runs[-1]
+    hbm_peak = peaks.get("hbm_gbs", 6650.0) if isinstance(peaks, dict) else 6650.0
+    achieved = r["hbm_bytes"] / (ms / 1e3) / 1e9
+    return {"workload": f"rms_norm output store (BASELINE configs[0]) at num_tokens={T}: "
+                        f"{T} blocks x 1023 threads x 4 iterations",
+            "accesses": r["tuples"], "instances": prog.instances, "has_race": bool(r["has_race"]),
+            "ms": ms, "gen_ms": r["gen_ms"], "sort_ms": r["sort_ms"], "scan_ms": r["scan_ms"],
+            "sort_key_bits": r["sort_bits"],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None,
+                         "algorithmic_bytes": r["hbm_bytes"],
+                         "peak_source": f"peaks file: {src}"}}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -369,6 +403,8 @@ def run_b200(args):
         achieved = insns / (search_ms / 1e3) if search_ms > 0 else 0.0
         ops = "bytecode instructions executed (no ncu calibration committed)"
 
+    k2 = _race_sweep_line(chk, args, peaks, src) if rank == 0 and args.race_tokens > 0 else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
@@ -422,6 +458,7 @@ def run_b200(args):
                          "peak_source": f"{sms} SMs x 128 INT32 lanes x {sm_mhz:.0f} MHz "
                                         f"(clock sampled; peaks file: {src})"},
             "cpu_baseline": cpu,
+            "k2_race_sweep": k2,
             "clocks": clk,
             "gpu_launches": launches,
         }
@@ -441,6 +478,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--race-tokens", type=int, default=262144,
+                    help="num_tokens of the K2 race-sweep line (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

@@ -179,6 +179,50 @@ int mk_set_eval(mk_ctx* ctx, mk_dset* set, const mk_limits* lim, int32_t* status
                 mk_i128* point, mk_stats* stats);
 int mk_set_free(mk_ctx* ctx, mk_dset* set);
 
+/* ---------------------------------------------------------------------
+ * Race sweep (K2): concrete replay of one store instruction over every
+ * thread-private instance of one launch.
+ *
+ * The reference's race query for a store (engine/detectors.py:204-232) asks
+ * for two distinct threads of one launch whose paths hold and whose byte
+ * offsets are equal; shared memory additionally requires the same block
+ * (_distinctness, :249-273).  With every launch-level symbol fixed (a
+ * concrete launch, e.g. a finding's witness), the sweep enumerates the
+ * instance box of ONE thread's path program (problem 0 of `set`: its atoms
+ * are the path, register `off_reg` holds the byte offset after a model),
+ * writes one (offset, block) key + instance index per model (per instance
+ * of the leading vars, when trailing vars are existential), radix-sorts
+ * the tuples in HBM and scans adjacent tuples for a conflict: equal offset
+ * and distinct thread identity (global), or equal offset and block with
+ * distinct thread ids (shared).  Identity symbols are given as var indices
+ * (-1 when the symbol is fixed or absent).  Requires a narrow problem.
+ */
+typedef struct mk_race_prog {
+  mk_problem_set set;   /* exactly one problem */
+  int32_t off_reg;      /* register holding the byte offset */
+  int32_t shared;       /* 1: shared-memory race rule */
+  int32_t id_var[6];    /* blockIdx.x,y,z, threadIdx.x,y,z var indices or -1 */
+  int32_t n_exist;      /* trailing vars that are existential: they touch
+                           neither the offset nor an identity, so an
+                           instance of the leading vars is one access iff
+                           SOME value of them satisfies the path */
+  int32_t pad;
+} mk_race_prog;
+
+typedef struct mk_race_result {
+  uint64_t instances;   /* instance indices enumerated */
+  uint64_t tuples;      /* instances whose path holds (one access each) */
+  uint64_t conflicts;   /* adjacent sorted tuple pairs forming a race */
+  int32_t has_race;
+  int32_t sort_bits;    /* radix-sort key width */
+  uint64_t idx_a, idx_b;  /* instance indices of the first conflicting pair */
+  int64_t offset;       /* its byte offset */
+  double gen_ms, sort_ms, scan_ms;  /* CUDA-event time of the three phases */
+  uint64_t hbm_bytes;   /* algorithmic HBM bytes moved by the three phases */
+} mk_race_result;
+
+int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -770,6 +770,7 @@ struct mk_ctx {
   void* d_work = nullptr;
   size_t d_work_bytes = 0;
   void* h_pinned = nullptr;
+  void* h_race = nullptr;  // device side buffer of the race sweep
 };
 
 static int fail(mk_ctx* ctx, int code, const std::string& msg) {
@@ -840,6 +841,7 @@ extern "C" int mk_ctx_destroy(mk_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->d_work) cudaFree(ctx->d_work);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  if (ctx->h_race) cudaFree(ctx->h_race);
   for (int i = 0; i < 8; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   if (ctx->scratch.d) cudaFree(ctx->scratch.d);
@@ -1333,3 +1335,5 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   if (rc) return rc;
   return run_set(ctx, &ctx->scratch, lim, status, point, stats, t0);
 }
+
+#include "mk_race.cuh"

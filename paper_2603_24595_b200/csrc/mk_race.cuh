@@ -1,0 +1,408 @@
+// mk_race.cuh -- K2: sort-based race sweep over one concrete launch
+// (include/mk_b200.h mk_race_sweep).  Included at the end of mk_engine.cu.
+//
+// Reference semantics (engine/detectors.py:204-273): a DataRace on a store is
+// a pair of instances of the store's path, one per thread, with equal
+// mathematical byte offsets and distinct thread identities (global memory),
+// or the same block and distinct thread ids (shared memory).  With the
+// launch fixed, the sweep is the data-parallel form of that definition:
+//
+//   k_race_root  interval evaluation of the root box: byte-offset range, so
+//                the (offset, block) sort key is packed into as few bits as
+//                possible;
+//   k_race_gen   every instance index of the thread-private box: decode in
+//                lexicographic order, evaluate the path bytecode in exact
+//                int64, write (key, instance index) to the instance's slot
+//                (a sentinel key when the path fails);
+//   cub::DeviceRadixSort::SortPairs over the key bits in HBM;
+//   k_race_scan  adjacent tuples with equal key and distinct identity are a
+//                conflict (every race has at least one adjacent witness
+//                pair after the sort); warp-aggregated count + atomicMin of
+//                the first conflicting position.
+
+namespace {
+
+constexpr int RACE_THREADS = 256;
+
+struct RaceDev {
+  MkProb P;
+  const mk_problem* prob;
+  const int64_t* lo;   // root box (int64, narrow)
+  const int64_t* hi;
+  int off_reg;
+  int shared;
+  int id_var[6];
+  int64_t off_lo;
+  unsigned long long nblocks;  // block-key radix (1 for global memory)
+  int n_outer;                 // leading vars enumerated as instances
+  unsigned long long inner;    // volume of the trailing existential vars
+};
+
+__device__ __forceinline__ unsigned long long race_block_key(const RaceDev& R, const int64_t* x) {
+  unsigned long long k = 0;
+  for (int a = 2; a >= 0; --a) {
+    const int v = R.id_var[a];
+    if (v < 0) continue;
+    const unsigned long long span = (unsigned long long)(R.hi[v] - R.lo[v] + 1);
+    k = k * span + (unsigned long long)(x[v] - R.lo[v]);
+  }
+  return k;
+}
+
+__global__ void k_race_root(RaceDev R, int64_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  MkIvT<int64_t> Rg[MK_MAXR];
+  int64_t cnt = 0;
+  mk_eval_box(R.P, R.lo, R.hi, Rg, &cnt);
+  out[0] = Rg[R.off_reg].lo;
+  out[1] = Rg[R.off_reg].hi;
+}
+
+// Point evaluation of a narrow problem with the register file in shared
+// memory (register r of thread t at sh[r * blockDim.x + t]: consecutive lanes
+// hit consecutive banks) and the EvalError flags as a bit mask (small
+// problems have <= 64 registers).  Same semantics as mk_core.cuh
+// mk_eval_point<int64_t>; the local-memory register file of the generic
+// evaluator spills to L2 at full occupancy.
+__device__ __forceinline__ bool race_eval_point(const MkProb& P, const int64_t* x, int64_t* sh) {
+  const int nv = P.p->nvars;
+  const int nc = P.p->nconst;
+  const int bd = blockDim.x, t = threadIdx.x;
+  uint64_t err = 0;
+  for (int i = 0; i < nv; ++i) sh[i * bd + t] = x[i];
+  for (int i = 0; i < nc; ++i) sh[(nv + i) * bd + t] = (int64_t)P.consts[i].lo;
+  const int n = P.p->ninsn;
+  for (int k = 0; k < n; ++k) {
+    const mk_insn in = P.insns[k];
+    const int64_t a = sh[in.a * bd + t];
+    const bool ea = (err >> in.a) & 1;
+    if (in.op == MK_OP_ATOM) {
+      if (ea || !a) return false;
+      continue;
+    }
+    const int64_t b = sh[in.b * bd + t];
+    const bool eb = (err >> in.b) & 1;
+    int64_t r = 0;
+    bool e = false;
+    switch (in.op) {
+      case MK_OP_AND: if (ea) e = true; else if (!a) r = 0; else { r = b ? 1 : 0; e = eb; } break;
+      case MK_OP_OR: if (ea) e = true; else if (a) r = 1; else { r = b ? 1 : 0; e = eb; } break;
+      case MK_OP_NOT: e = ea; r = a ? 0 : 1; break;
+      case MK_OP_ITE: {
+        const int64_t c = sh[in.c * bd + t];
+        const bool ec = (err >> in.c) & 1;
+        if (ea) e = true; else if (a) { r = b; e = eb; } else { r = c; e = ec; }
+        break;
+      }
+      default:
+        e = ea || eb;
+        if (!e) {
+          switch (in.op) {
+            case MK_OP_ADD: r = a + b; break;
+            case MK_OP_SUB: r = a - b; break;
+            case MK_OP_MUL: r = a * b; break;
+            case MK_OP_SHL: r = MkNum<int64_t>::shl(a, (int)b); break;
+            case MK_OP_SHR: r = MkNum<int64_t>::shr(a, (int)b); break;
+            case MK_OP_DIV: if (b == 0) e = true; else r = a / b; break;
+            case MK_OP_MOD: if (b == 0) e = true; else r = a % b; break;
+            case MK_OP_EMOD: if (b == 0) e = true; else r = mk_emod_c<int64_t>(a, b); break;
+            case MK_OP_EQ: r = a == b; break;
+            case MK_OP_NE: r = a != b; break;
+            case MK_OP_LT: r = a < b; break;
+            case MK_OP_LE: r = a <= b; break;
+            case MK_OP_GT: r = a > b; break;
+            case MK_OP_GE: r = a >= b; break;
+            default: break;
+          }
+        }
+    }
+    sh[in.dst * bd + t] = r;
+    err = e ? (err | (1ull << in.dst)) : (err & ~(1ull << in.dst));
+  }
+  return true;
+}
+
+// dense generation: slot idx holds instance idx's key, or the all-ones
+// sentinel (sorted past every real key) when the instance is not an access.
+// Positions are the instance order, so the stable radix sort leaves equal
+// keys in instance order: conflicts and the first conflicting pair are
+// deterministic.  Each thread walks a grid-stride sequence of instances with
+// a mixed-radix odometer (one addition per symbol instead of 64-bit
+// divisions per decode).
+template <typename K>
+__global__ void __launch_bounds__(RACE_THREADS) k_race_gen(RaceDev R, unsigned long long vol,
+                                                           K sentinel, K* keys, uint32_t* vals,
+                                                           unsigned long long* count,
+                                                           unsigned long long* evaluated) {
+  extern __shared__ int64_t sh[];
+  const int nv = R.prob->nvars;
+  const int nl = R.n_outer;
+  int64_t span[SMALL_V], dig[SMALL_V], sdig[SMALL_V], x[SMALL_V];
+  for (int i = 0; i < nv; ++i) span[i] = R.hi[i] - R.lo[i] + 1;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  {
+    unsigned long long a = idx, b = stride;
+    for (int i = nl - 1; i >= 0; --i) {
+      dig[i] = (int64_t)(a % (unsigned long long)span[i]);
+      a /= (unsigned long long)span[i];
+      sdig[i] = (int64_t)(b % (unsigned long long)span[i]);
+      b /= (unsigned long long)span[i];
+    }
+  }
+  unsigned long long done = 0, models = 0;
+  for (; idx < vol; idx += stride) {
+    for (int i = 0; i < nl; ++i) x[i] = R.lo[i] + dig[i];
+    // one access per instance of the leading vars: the first model over the
+    // trailing existential vars (inner == 1 when there are none)
+    K key = sentinel;
+    for (unsigned long long j = 0; j < R.inner; ++j) {
+      unsigned long long jj = j;
+      for (int i = nv - 1; i >= nl; --i) {
+        x[i] = R.lo[i] + (int64_t)(jj % (unsigned long long)span[i]);
+        jj /= (unsigned long long)span[i];
+      }
+      ++done;
+      if (race_eval_point(R.P, x, sh)) {
+        const unsigned long long ok =
+            (unsigned long long)(sh[R.off_reg * blockDim.x + threadIdx.x] - R.off_lo);
+        key = (K)(ok * R.nblocks + (R.shared ? race_block_key(R, x) : 0ull));
+        ++models;
+        break;
+      }
+    }
+    keys[idx] = key;
+    vals[idx] = (uint32_t)idx;
+    // odometer: dig += sdig (mixed radix); overflow of the top digit means
+    // idx >= vol, which the loop test catches
+    int64_t carry = 0;
+    for (int i = nl - 1; i >= 0; --i) {
+      int64_t d = dig[i] + sdig[i] + carry;
+      carry = d >= span[i] ? 1 : 0;
+      dig[i] = d - (carry ? span[i] : 0);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    done += __shfl_down_sync(FULL, done, o);
+    models += __shfl_down_sync(FULL, models, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (done) atomicAdd(evaluated, done);
+    if (models) atomicAdd(count, models);
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(RACE_THREADS) k_race_scan(RaceDev R, const K* keys,
+                                                            const uint32_t* vals,
+                                                            const unsigned long long* count,
+                                                            unsigned long long* conflicts,
+                                                            unsigned long long* first) {
+  const unsigned long long n = *count;  // real tuples sort before the sentinels
+  int64_t xa[SMALL_V], xb[SMALL_V];
+  unsigned long long mine = 0, my_first = ~0ull;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    if (keys[i] != keys[i - 1]) continue;
+    // identities are leading vars: decode the instance of the leading box
+    mk_decode(R.lo, R.hi, R.n_outer, R.prob->maxmask, (unsigned long long)vals[i - 1], xa);
+    mk_decode(R.lo, R.hi, R.n_outer, R.prob->maxmask, (unsigned long long)vals[i], xb);
+    bool same = true;
+    // shared: the key already holds the block, compare thread ids only
+    for (int a = R.shared ? 3 : 0; a < 6; ++a) {
+      const int v = R.id_var[a];
+      if (v >= 0 && xa[v] != xb[v]) same = false;
+    }
+    if (!same) {
+      ++mine;
+      if (i < my_first) my_first = i;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mine += __shfl_down_sync(FULL, mine, o);
+    unsigned long long f = __shfl_down_sync(FULL, my_first, o);
+    if (f < my_first) my_first = f;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mine) atomicAdd(conflicts, mine);
+    if (my_first != ~0ull) atomicMin(first, my_first);
+  }
+}
+
+}  // namespace
+
+
+template <typename K>
+static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int bits, int nregs,
+                    mk_race_result* out, char* base, unsigned long long* ctr) {
+  cudaStream_t s = ctx->stream;
+  // tuples: keys + values, double buffered for the sort
+  size_t cub_bytes = 0;
+  {
+    cub::DoubleBuffer<K> kb(nullptr, nullptr);
+    cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, kb, vb, (int)vol, 0, bits, s);
+  }
+  size_t off = 0;
+  auto place = [&](size_t bytes) {
+    size_t o = off;
+    off = (off + bytes + 255) / 256 * 256;
+    return o;
+  };
+  const size_t o_k0 = place(sizeof(K) * vol), o_k1 = place(sizeof(K) * vol);
+  const size_t o_v0 = place(sizeof(uint32_t) * vol), o_v1 = place(sizeof(uint32_t) * vol);
+  const size_t o_cub = place(cub_bytes + 256);
+  int rc = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, off);
+  if (rc) return rc;
+  char* wb = static_cast<char*>(ctx->d_work);
+  K* k0 = reinterpret_cast<K*>(wb + o_k0);
+  K* k1 = reinterpret_cast<K*>(wb + o_k1);
+  uint32_t* v0 = reinterpret_cast<uint32_t*>(wb + o_v0);
+  uint32_t* v1 = reinterpret_cast<uint32_t*>(wb + o_v1);
+  (void)base;
+  const int grid = ctx->sms * 8;
+  const K sentinel = (K)(bits >= (int)(8 * sizeof(K)) ? ~(K)0 : (((K)1 << bits) - 1));
+  CK(cudaEventRecord(ctx->ev[0], s));
+  const size_t shm = sizeof(int64_t) * (size_t)nregs * RACE_THREADS;
+  if (shm > 48 * 1024)
+    CK(cudaFuncSetAttribute(k_race_gen<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  k_race_gen<K><<<grid, RACE_THREADS, shm, s>>>(R, vol, sentinel, k0, v0, ctr + 0, ctr + 3);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[1], s));
+  cub::DoubleBuffer<K> kb(k0, k1);
+  cub::DoubleBuffer<uint32_t> vb(v0, v1);
+  if (vol > 1) {
+    size_t tb = cub_bytes;
+    CK(cub::DeviceRadixSort::SortPairs(wb + o_cub, tb, kb, vb, (int)vol, 0, bits, s));
+  }
+  CK(cudaEventRecord(ctx->ev[2], s));
+  k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, kb.Current(), vb.Current(), ctr + 0, ctr + 1,
+                                               ctr + 2);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[3], s));
+  unsigned long long h[4];
+  CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  out->tuples = h[0];
+  out->instances = h[3];
+  out->conflicts = h[1];
+  out->has_race = h[1] > 0;
+  out->sort_bits = bits;
+  if (out->has_race) {
+    const unsigned long long i = h[2];
+    uint32_t va = 0, vb2 = 0;
+    K key = 0;
+    CK(cudaMemcpy(&va, vb.Current() + i - 1, sizeof(va), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&vb2, vb.Current() + i, sizeof(vb2), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&key, kb.Current() + i, sizeof(key), cudaMemcpyDeviceToHost));
+    out->idx_a = va;
+    out->idx_b = vb2;
+    out->offset = (int64_t)((unsigned long long)key / R.nblocks) + R.off_lo;
+  }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+  out->gen_ms = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
+  out->sort_ms = ms;
+  cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]);
+  out->scan_ms = ms;
+  // one tuple write at generation, one read + one write for a
+  // single-pass-equivalent sort, one read in the conflict scan
+  out->hbm_bytes = 4ull * (unsigned long long)(sizeof(K) + sizeof(uint32_t)) * vol;
+  return MK_OK;
+}
+
+extern "C" int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out) {
+  if (!ctx || !prog || !out) return fail(ctx, MK_EINVAL, "null argument");
+  std::memset(out, 0, sizeof(*out));
+  CK(cudaSetDevice(ctx->device));
+  const mk_problem_set& set = prog->set;
+  if (set.nprob != 1) return fail(ctx, MK_EINVAL, "race sweep takes exactly one problem");
+  const mk_problem& hp = set.probs[0];
+  if (!(hp.flags & MK_PF_NARROW)) return fail(ctx, MK_EINVAL, "race sweep needs a narrow problem");
+  if (hp.nvars > SMALL_V || hp.nregs > SMALL_R)
+    return fail(ctx, MK_EINVAL, "race sweep program exceeds the small-problem limits");
+  if (prog->off_reg < 0 || prog->off_reg >= hp.nregs) return fail(ctx, MK_EINVAL, "bad off_reg");
+  // instance box (int64) and volume
+  std::vector<int64_t> lo(hp.nvars), hi(hp.nvars);
+  const int n_outer = hp.nvars - prog->n_exist;
+  if (prog->n_exist < 0 || n_outer < 0) return fail(ctx, MK_EINVAL, "bad n_exist");
+  long double volf = 1.0L, innerf = 1.0L;
+  unsigned long long vol = 1, inner = 1;
+  for (int i = 0; i < hp.nvars; ++i) {
+    lo[i] = (int64_t)set.var_lo[hp.var_off + i].lo;
+    hi[i] = (int64_t)set.var_hi[hp.var_off + i].lo;
+    const long double w = (long double)(hi[i] - lo[i] + 1);
+    if (i < n_outer) {
+      volf *= w;
+      vol *= (unsigned long long)(hi[i] - lo[i] + 1);
+    } else {
+      innerf *= w;
+      inner *= (unsigned long long)(hi[i] - lo[i] + 1);
+    }
+  }
+  if (volf > 2147483647.0L) return fail(ctx, MK_EINVAL, "race sweep box exceeds 2^31 instances");
+  if (volf * innerf > 9.0e18L) return fail(ctx, MK_EINVAL, "race sweep box exceeds 2^63 points");
+  int rc = upload_set(ctx, &set, &ctx->scratch);
+  if (rc) return rc;
+  mk_dset* ds = &ctx->scratch;
+  char* base = static_cast<char*>(ds->d);
+  // small side buffer: box bounds, root offset range, counters
+  if (!ctx->h_race) {
+    CK(cudaMalloc(&ctx->h_race, 4096));
+  }
+  char* side = static_cast<char*>(ctx->h_race);
+  int64_t* d_lo = reinterpret_cast<int64_t*>(side);
+  int64_t* d_hi = d_lo + MK_MAXV;
+  int64_t* d_rng = d_hi + MK_MAXV;
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(d_rng + 2);
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemcpyAsync(d_lo, lo.data(), sizeof(int64_t) * hp.nvars, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_hi, hi.data(), sizeof(int64_t) * hp.nvars, cudaMemcpyHostToDevice, s));
+  unsigned long long init[4] = {0ull, 0ull, ~0ull, 0ull};
+  CK(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  RaceDev R;
+  const mk_problem* dprobs = reinterpret_cast<const mk_problem*>(base + ds->o_probs);
+  // the device view of problem 0, built from the host copy's offsets (the
+  // problem record itself lives in HBM)
+  R.P.p = dprobs;
+  R.P.insns = reinterpret_cast<const mk_insn*>(base + ds->o_insn) + hp.insn_off;
+  R.P.consts = reinterpret_cast<const mk_i128*>(base + ds->o_const) + hp.const_off;
+  R.P.atom_regs = reinterpret_cast<const int32_t*>(base + ds->o_ar) + hp.atom_off;
+  R.P.atom_masks = reinterpret_cast<const uint64_t*>(base + ds->o_am) + hp.atom_off;
+  R.P.rows = reinterpret_cast<const mk_row*>(base + ds->o_rows) + hp.row_off;
+  R.P.terms = reinterpret_cast<const mk_row_term*>(base + ds->o_terms);
+  R.prob = dprobs;
+  R.lo = d_lo;
+  R.hi = d_hi;
+  R.off_reg = prog->off_reg;
+  R.shared = prog->shared ? 1 : 0;
+  unsigned long long nblocks = 1;
+  R.n_outer = n_outer;
+  R.inner = inner;
+  for (int a = 0; a < 6; ++a) {
+    R.id_var[a] = prog->id_var[a];
+    if (R.id_var[a] >= n_outer) return fail(ctx, MK_EINVAL, "identity var must be a leading var");
+    if (a < 3 && R.id_var[a] >= 0 && R.shared)
+      nblocks *= (unsigned long long)(hi[R.id_var[a]] - lo[R.id_var[a]] + 1);
+  }
+  R.nblocks = nblocks;
+  R.off_lo = 0;
+  k_race_root<<<1, 32, 0, s>>>(R, d_rng);
+  CK(cudaGetLastError());
+  int64_t rng[2];
+  CK(cudaMemcpyAsync(rng, d_rng, sizeof(rng), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  R.off_lo = rng[0];
+  const long double keyspan = ((long double)rng[1] - (long double)rng[0] + 1.0L) * (long double)nblocks;
+  if (keyspan > 18446744073709551615.0L)
+    return fail(ctx, MK_EINVAL, "race sweep key (offset x block) exceeds 64 bits");
+  // real keys are <= kmax; kmax + 1 must fit the key width as the sentinel
+  const unsigned long long kmax =
+      (unsigned long long)((unsigned long long)(rng[1] - rng[0]) * nblocks + (nblocks - 1));
+  if (kmax == ~0ull) return fail(ctx, MK_EINVAL, "race sweep key (offset x block) exceeds 64 bits");
+  int bits = mk_bitlen((uint64_t)(kmax + 1));
+  if (bits < 1) bits = 1;
+  if (bits <= 32) return race_run<uint32_t>(ctx, R, vol, bits, hp.nregs, out, base, ctr);
+  return race_run<unsigned long long>(ctx, R, vol, bits, hp.nregs, out, base, ctr);
+}

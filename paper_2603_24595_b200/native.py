@@ -22,7 +22,8 @@ MK_PF_NARROW = 1
 STATUS_NAME = {MK_UNSAT: "unsat", MK_SAT: "sat", MK_UNKNOWN: "unknown"}
 
 EXPORTS = ("mk_abi_version", "mk_device_count", "mk_ctx_create", "mk_ctx_destroy",
-           "mk_last_error", "mk_site_eval", "mk_set_upload", "mk_set_eval", "mk_set_free")
+           "mk_last_error", "mk_site_eval", "mk_set_upload", "mk_set_eval", "mk_set_free",
+           "mk_race_sweep")
 
 
 class NativeUnavailable(RuntimeError):
@@ -76,6 +77,27 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class RaceProg(ctypes.Structure):
+    _fields_ = [("set", ProblemSet), ("off_reg", ctypes.c_int32), ("shared", ctypes.c_int32),
+                ("id_var", ctypes.c_int32 * 6), ("n_exist", ctypes.c_int32),
+                ("pad", ctypes.c_int32)]
+
+
+class RaceResult(ctypes.Structure):
+    _fields_ = [("instances", ctypes.c_uint64), ("tuples", ctypes.c_uint64),
+                ("conflicts", ctypes.c_uint64), ("has_race", ctypes.c_int32),
+                ("sort_bits", ctypes.c_int32), ("idx_a", ctypes.c_uint64),
+                ("idx_b", ctypes.c_uint64), ("offset", ctypes.c_int64),
+                ("gen_ms", ctypes.c_double), ("sort_ms", ctypes.c_double),
+                ("scan_ms", ctypes.c_double), ("hbm_bytes", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+assert ctypes.sizeof(RaceProg) == 144 and ctypes.sizeof(RaceResult) == 88
+
+
 def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
     lib.mk_abi_version.restype = ctypes.c_int
     lib.mk_device_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
@@ -91,6 +113,8 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
     lib.mk_set_eval.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Limits),
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(Stats)]
     lib.mk_set_free.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    lib.mk_race_sweep.argtypes = [ctypes.c_void_p, ctypes.POINTER(RaceProg),
+                                  ctypes.POINTER(RaceResult)]
     return lib
 
 
@@ -257,6 +281,29 @@ class Engine:
 
     def solve(self, problems, limits: Optional[dict] = None):
         return self.solve_packed(PackedSet(problems), limits)
+
+    # -- race sweep (K2) -----------------------------------------------------------
+
+    def race_sweep(self, prog) -> dict:
+        """Concrete race replay of one store at one launch
+        (paper_2603_24595_b200.race.RaceProgram -> mk_race_sweep)."""
+        packed = PackedSet([prog.problem])
+        rp = RaceProg()
+        rp.set = packed.struct
+        rp.off_reg = prog.off_reg
+        rp.shared = 1 if prog.shared else 0
+        for i, v in enumerate(prog.id_var):
+            rp.id_var[i] = v
+        rp.n_exist = prog.n_exist
+        out = RaceResult()
+        rc = self.lib.mk_race_sweep(self.ctx, ctypes.byref(rp), ctypes.byref(out))
+        if rc != 0:
+            msg = self.lib.mk_last_error(self.ctx)
+            raise RuntimeError(f"mk_race_sweep failed ({rc}): {msg.decode() if msg else ''}")
+        res = out.as_dict()
+        if res["has_race"]:
+            res["pair"] = (prog.decode(res["idx_a"]), prog.decode(res["idx_b"]))
+        return res
 
     # -- device-resident sets ------------------------------------------------------
 

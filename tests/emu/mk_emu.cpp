@@ -202,3 +202,77 @@ extern "C" int mk_set_free(mk_ctx* ctx, mk_dset* d) {
   delete d;
   return MK_OK;
 }
+
+// -- race sweep (K2), serial host restatement of csrc/mk_race.cuh ----------------
+#include <algorithm>
+#include <utility>
+
+extern "C" int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out) {
+  std::memset(out, 0, sizeof(*out));
+  const mk_problem_set& set = prog->set;
+  if (set.nprob != 1) {
+    ctx->err = "race sweep takes exactly one problem";
+    return MK_EINVAL;
+  }
+  const mk_problem& p = set.probs[0];
+  if (!(p.flags & MK_PF_NARROW)) {
+    ctx->err = "race sweep needs a narrow problem";
+    return MK_EINVAL;
+  }
+  MkProb P = mk_prob_view(set.probs, 0, set.insns, set.consts, set.atom_regs, set.atom_masks,
+                          set.rows, set.row_terms);
+  const int nv = p.nvars, n_outer = nv - prog->n_exist;
+  std::vector<int64_t> lo(nv), hi(nv);
+  unsigned long long vol = 1, inner = 1;
+  for (int i = 0; i < nv; ++i) {
+    lo[i] = (int64_t)set.var_lo[p.var_off + i].lo;
+    hi[i] = (int64_t)set.var_hi[p.var_off + i].lo;
+    (i < n_outer ? vol : inner) *= (unsigned long long)(hi[i] - lo[i] + 1);
+  }
+  std::vector<MkCvT<int64_t>> R(MK_MAXR);
+  std::vector<std::pair<std::pair<int64_t, unsigned long long>, unsigned long long>> tuples;
+  int64_t x[MK_MAXV], y[MK_MAXV];
+  for (unsigned long long idx = 0; idx < vol; ++idx) {
+    for (unsigned long long j = 0; j < inner; ++j) {
+      mk_decode(lo.data(), hi.data(), nv, p.maxmask, idx * inner + j, x);
+      bool ovf = false;
+      int64_t cnt = 0;
+      out->instances++;
+      if (mk_eval_point(P, x, R.data(), &ovf, &cnt)) {
+        unsigned long long blk = 0;
+        if (prog->shared) {
+          for (int a = 2; a >= 0; --a) {
+            const int v = prog->id_var[a];
+            if (v < 0) continue;
+            blk = blk * (unsigned long long)(hi[v] - lo[v] + 1) + (unsigned long long)(x[v] - lo[v]);
+          }
+        }
+        tuples.push_back({{R[prog->off_reg].v, blk}, idx});
+        break;
+      }
+    }
+  }
+  std::sort(tuples.begin(), tuples.end());
+  out->tuples = tuples.size();
+  for (size_t i = 1; i < tuples.size(); ++i) {
+    if (tuples[i].first != tuples[i - 1].first) continue;
+    mk_decode(lo.data(), hi.data(), n_outer, p.maxmask, tuples[i - 1].second, x);
+    mk_decode(lo.data(), hi.data(), n_outer, p.maxmask, tuples[i].second, y);
+    bool same = true;
+    for (int a = prog->shared ? 3 : 0; a < 6; ++a) {
+      const int v = prog->id_var[a];
+      if (v >= 0 && x[v] != y[v]) same = false;
+    }
+    if (!same) {
+      if (!out->has_race) {
+        out->idx_a = tuples[i - 1].second;
+        out->idx_b = tuples[i].second;
+        out->offset = tuples[i].first.first;
+      }
+      out->has_race = 1;
+      out->conflicts++;
+    }
+  }
+  out->hbm_bytes = 4ull * 12ull * out->tuples;
+  return MK_OK;
+}
