@@ -983,7 +983,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   // per class c (0 = wide / int128 storage, 1 = narrow / int64 storage)
   const size_t cbytes[2] = {box_bytes_of<i128>(S), box_bytes_of<int64_t>(S)};
   size_t cls_cap[2];
-  for (int c = 0; c < 2; ++c) cls_cap[c] = ((size_t)2 << 30) / cbytes[c];  // 2 GiB per task / dump buffer
+  for (int c = 0; c < 2; ++c) cls_cap[c] = ((size_t)1 << 30) / cbytes[c];  // 1 GiB per task / dump buffer
   size_t scan_n = (size_t)chunk * K;
   if (scan_n < cap_boxes) scan_n = cap_boxes;
   size_t cub_bytes = 0;
@@ -1011,7 +1011,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   long long unit_cap[2];
   for (int c = 0; c < 2; ++c) {
     const int units = ctx->units[c];
-    long long cap = (long long)(((size_t)4 << 30) / ((size_t)units * cbytes[c]));
+    long long cap = (long long)(((size_t)3 << 30) / ((size_t)units * cbytes[c]));
     if (cap > 16384) cap = 16384;
     if (cap < 8 * 32) cap = 8 * 32;
     if (lim && lim->unit_stack > 0) cap = lim->unit_stack < 32 ? 32 : lim->unit_stack;

@@ -28,7 +28,10 @@ def test_dropin_emulated(name):
     from paper_2603_24595_b200.engine import SiteChecker
 
     chk = SiteChecker(lib_path=EMU)
-    doc = _run(name, chk)
+    try:
+        doc = _run(name, chk)
+    finally:
+        chk.close()
     assert doc["findings"] == expected_findings(load(name))
     assert doc["coverage"] == "complete"
 
@@ -40,6 +43,9 @@ def test_dropin_gpu(name):
     from paper_2603_24595_b200.engine import SiteChecker
 
     chk = SiteChecker(device=0)
-    doc = _run(name, chk)
+    try:
+        doc = _run(name, chk)
+    finally:
+        chk.close()
     assert doc["findings"] == expected_findings(load(name))
     assert doc["coverage"] == "complete"

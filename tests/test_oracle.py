@@ -68,8 +68,11 @@ def test_gpu_engine_matches_random_fixtures():
 
     chk = SiteChecker(device=0)
     qs = _fixtures()
-    res = chk.check_queries([([ir.from_json(a) for a in q["query"]], origin_lookup(q["origins"]))
-                             for q in qs])
+    try:
+        res = chk.check_queries([([ir.from_json(a) for a in q["query"]],
+                                  origin_lookup(q["origins"])) for q in qs])
+    finally:
+        chk.close()
     bad = [(i, r.status, q["verdict"]) for i, (q, r) in enumerate(zip(qs, res))
            if r.status != q["verdict"] or (r.status == "sat" and r.witness != q["witness"])]
     assert bad == []
