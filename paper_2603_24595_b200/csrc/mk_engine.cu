@@ -39,12 +39,18 @@
 
 #include "mk_b200.h"
 #include "mk_core.cuh"
+#include "mk_shreg.cuh"
 
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SMALL_V = 8;    // free symbols of a "small" problem
 constexpr int SMALL_R = 64;   // registers of a "small" problem
+constexpr int SH_R = 24;      // registers of a narrow problem evaluated from shared memory
+constexpr int SH_BYTES = 2 * SH_R * 128 * (int)sizeof(int64_t);  // per 128-thread CTA
+
+// dynamic shared memory of k_search<int64_t>: lo / hi interval register files
+extern __shared__ int64_t mk_dyn_sh[];
 
 struct Box {
   int32_t prob;
@@ -119,6 +125,9 @@ __device__ __forceinline__ bool is_narrow(const mk_problem& p) {
 }
 __device__ __forceinline__ bool is_small(const mk_problem& p) {
   return p.nvars <= SMALL_V && p.nregs <= SMALL_R;
+}
+__device__ __forceinline__ bool is_shreg(const mk_problem& p) {
+  return is_narrow(p) && p.nvars <= SMALL_V && p.nregs <= SH_R;
 }
 
 __device__ __forceinline__ Box* box_at(void* base, size_t box_bytes, size_t i) {
@@ -291,7 +300,7 @@ struct Act {
 
 // lo/hi: the box (contracted in place).  Prunes, accepts the best corner of an
 // all-true box, hands small boxes to enumeration, or chooses a split.
-template <typename V, int CAPV, int CAPR>
+template <typename V, int CAPV, int CAPR, int SH = 0>
 __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo, V* hi, int K,
                            long long leaf_volume, LaneStats& st) {
   const int nv = p.nvars;
@@ -312,9 +321,14 @@ __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo,
     st.covered += vol0;
     return a;
   }
-  MkIvT<V> R[CAPR];
   int64_t cnt = 0;
-  MkBoxVerdict v = mk_eval_box(P, lo, hi, R, &cnt);
+  MkBoxVerdict v;
+  if constexpr (SH != 0) {
+    v = sh_eval_box(P, lo, hi, mk_dyn_sh, mk_dyn_sh + SH_R * blockDim.x, &cnt);
+  } else {
+    MkIvT<V> R[CAPR];
+    v = mk_eval_box(P, lo, hi, R, &cnt);
+  }
   st.insns_bb += (unsigned long long)cnt;
   if (v.any_false) {
     st.covered += vol0;
@@ -425,7 +439,7 @@ __global__ void __launch_bounds__(128) k_bb(DevSet D, const void* chunk, int n, 
 // 32*r + l of round r (index order == witness order); the first round with a
 // model gives the lexicographic optimum of the box (lowest such lane).
 
-template <typename T, typename V, int CAPV, int CAPR>
+template <typename T, typename V, int CAPV, int CAPR, int SH = 0>
 __device__ void warp_enumerate(const DevSet& D, int pid, const mk_problem& p, const Box* box,
                                LaneStats& st) {
   const int lane = threadIdx.x & 31;
@@ -445,7 +459,7 @@ __device__ void warp_enumerate(const DevSet& D, int pid, const mk_problem& p, co
   }
   if (skip) return;
   const MkProb P = view(D, pid);
-  MkCvT<V> R[CAPR];
+  MkCvT<V> R[SH ? 1 : CAPR];
   int64_t cnt = 0;
   bool ovf = false;
   unsigned long long found = ~0ull;
@@ -455,7 +469,12 @@ __device__ void warp_enumerate(const DevSet& D, int pid, const mk_problem& p, co
     if (idx < vol) {
       mk_decode(lo, hi, nv, p.maxmask, idx, x);
       st.points++;
-      model = mk_eval_point(P, x, R, &ovf, &cnt);
+      if constexpr (SH != 0) {
+        model = sh_eval_point(P, x, mk_dyn_sh);
+        cnt += p.ninsn;
+      } else {
+        model = mk_eval_point(P, x, R, &ovf, &cnt);
+      }
     }
     unsigned m = __ballot_sync(FULL, model);
     if (m) {
@@ -527,6 +546,9 @@ struct SearchArgs {
   DevStats* st;
   int units;
   size_t box_bytes;  // class storage (Store<V>)
+  int width;         // boxes popped per step (32; 1 in a dive)
+  int max_steps;     // steps per task (0: unbounded)
+  int dive;          // incumbent dive: no spills, dumps or pending marks
 };
 
 // TASK_DUMPED: redistribution (every task has been handed out), the unit
@@ -558,7 +580,7 @@ __device__ bool dump_stack(const SearchArgs& A, const DevSet& D, char* stack, lo
   return true;
 }
 
-template <typename V, int CAPV, int CAPR>
+template <typename V, int CAPV, int CAPR, int SH = 0>
 __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const mk_problem& p,
                            char* stack, char* leaves, unsigned long long t_start,
                            LaneStats& st) {
@@ -567,11 +589,13 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
   const int K = A.K;
   const unsigned long long deadline_ns = t_start + A.budget_ns;
   long long top = 1;
+  int steps = 0;
   while (top > 0) {
     long long room = A.cap - top;
-    long long n = top < 32 ? top : 32;
+    long long n = top < A.width ? top : A.width;
     long long fit = room / (K - 1);
     if (fit < n) n = fit;
+    if (n < 1 && A.dive) return TASK_DONE;
     if (n < 1) {
       // stack full: the bottom (worst) half goes to the next launch's task
       // list, the unit keeps searching its best half
@@ -597,7 +621,7 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
     a.sv = -1;
     if (lane < n) {
       load_box<V, V>(box_at(stack, A.box_bytes, (size_t)(base + lane)), nv, D.stride, lo, hi);
-      a = process_box<V, CAPV, CAPR>(D, pid, p, lo, hi, K, A.leaf_volume, st);
+      a = process_box<V, CAPV, CAPR, SH>(D, pid, p, lo, hi, K, A.leaf_volume, st);
     }
     const int nch = a.kind == ACT_SPLIT ? a.m : 0;
     int incl = nch;
@@ -626,16 +650,18 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
     top = base + ctot;
     const int nleaf = __popc(leafmask);
     for (int l = 0; l < nleaf; ++l)
-      warp_enumerate<V, V, CAPV, CAPR>(D, pid, p, box_at(leaves, A.box_bytes, l), st);
+      warp_enumerate<V, V, CAPV, CAPR, SH>(D, pid, p, box_at(leaves, A.box_bytes, l), st);
     int ctlw = 0;
     if (lane == 0) {
       unsigned long long now = globaltimer_ns();
       if (now > deadline_ns) ctlw = 1;
       // hand the remaining subtrees back when a quarter of the units idles
       int idle = *((volatile int*)(A.ctl + 1));
-      if (!ctlw && top > 0 && idle * 4 >= A.units && now > t_start + A.slice_ns) ctlw = 2;
+      if (!ctlw && !A.dive && top > 0 && idle * 4 >= A.units && now - t_start > A.slice_ns)
+        ctlw = 2;
     }
     ctlw = __shfl_sync(FULL, ctlw, 0);
+    if (A.max_steps && ++steps >= A.max_steps) return TASK_DONE;
     if (ctlw == 1) return top > 0 ? TASK_ABORT : TASK_DONE;
     // a redistribution dump that does not fit simply keeps searching
     if (ctlw == 2 && dump_stack(A, D, stack, top)) return TASK_DUMPED;
@@ -687,13 +713,19 @@ __global__ void __launch_bounds__(SEARCH_THREADS, MinBlocks<V>::value)
     if (pid < 0) continue;  // hole left by a dump that did not fit
     const mk_problem p = D.probs[pid];
     if (globaltimer_ns() > t_start + A.budget_ns) {
-      if (lane == 0) A.pending[pid] = 1;
+      if (lane == 0 && !A.dive) A.pending[pid] = 1;
       continue;
     }
     int r;
-    if (is_small(p)) r = search_task<V, SMALL_V, SMALL_R>(A, D, pid, p, stack, leaves, t_start, st);
-    else r = search_task<V, MK_MAXV, MK_MAXR>(A, D, pid, p, stack, leaves, t_start, st);
-    if (r == TASK_ABORT && lane == 0) A.pending[pid] = 1;
+    if constexpr (!MkNum<V>::kWide) {
+      if (is_shreg(p)) r = search_task<V, SMALL_V, SH_R, 1>(A, D, pid, p, stack, leaves, t_start, st);
+      else if (is_small(p)) r = search_task<V, SMALL_V, SMALL_R>(A, D, pid, p, stack, leaves, t_start, st);
+      else r = search_task<V, MK_MAXV, MK_MAXR>(A, D, pid, p, stack, leaves, t_start, st);
+    } else {
+      if (is_small(p)) r = search_task<V, SMALL_V, SMALL_R>(A, D, pid, p, stack, leaves, t_start, st);
+      else r = search_task<V, MK_MAXV, MK_MAXR>(A, D, pid, p, stack, leaves, t_start, st);
+    }
+    if (r == TASK_ABORT && lane == 0 && !A.dive) A.pending[pid] = 1;
     if (r == TASK_DUMPED) break;  // this launch ends for the unit; the host redistributes
   }
   st.flush_warp(A.st);
@@ -823,7 +855,7 @@ extern "C" int mk_ctx_create(int device, mk_ctx** out) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_wide, k_search<i128>, SEARCH_THREADS, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_narrow, k_search<int64_t>, SEARCH_THREADS,
-                                                  0);
+                                                  SH_BYTES);
     if (per_wide < 1) per_wide = 1;
     if (per_narrow < 1) per_narrow = 1;
     ctx->sms = sms;
@@ -949,6 +981,10 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   int K = lim && lim->split_k > 1 ? lim->split_k : 16;
   int chunk = lim && lim->chunk > 0 ? lim->chunk : 65536;
   long long leaf_volume = lim && lim->leaf_volume > 0 ? lim->leaf_volume : 4096;
+  // incumbent dive: steps of width 1 from every root before the search
+  // (mk_limits.chunk < -1 disables it; a model found early prunes the
+  // parallel search, whose units would otherwise explore worse subtrees)
+  const int dive_steps = lim && lim->chunk < -1 ? 0 : 48;
   const size_t box_bytes = sizeof(Box) + 2 * sizeof(mk_i128) * (size_t)S;
   char* base = static_cast<char*>(ds->d);
   cudaStream_t s = ctx->stream;
@@ -1055,9 +1091,124 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   ++launches;
   CK(cudaGetLastError());
   long long top = nprob;
+  int* h_counts = static_cast<int*>(ctx->h_pinned);
+
+  // split boxes [0, n) of the int128 stack into the two classes' task lists
+  // (class storage); ntasks = -1 when they do not fit
+  auto partition = [&](long long n) -> int {
+    if ((size_t)n > cls_cap[0] || (size_t)n > cls_cap[1]) {
+      cls[0].ntasks = cls[1].ntasks = -1;
+      return MK_OK;
+    }
+    for (int c = 0; c < 2; ++c) {
+      k_class_flags<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(D, stack, n, c, cflag);
+      ++launches;
+      CK(cudaGetLastError());
+      size_t tb = cub_bytes;
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, cflag, cpos, (int)n, s));
+      ++launches;
+      if (c == 0)
+        k_to_class<i128><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
+            D, static_cast<const char*>(stack), cflag, cpos, n, static_cast<char*>(cls[c].tasks),
+            d_counts + 2 + c);
+      else
+        k_to_class<int64_t><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
+            D, static_cast<const char*>(stack), cflag, cpos, n, static_cast<char*>(cls[c].tasks),
+            d_counts + 2 + c);
+      ++launches;
+      CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(h_counts, d_counts + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cls[0].ntasks = h_counts[0];
+    cls[1].ntasks = h_counts[1];
+    return MK_OK;
+  };
+  // one launch of both classes' persistent grids on their streams; a dive
+  // follows only the best box of each root for a few steps (width 1, no
+  // spills or dumps) to seed the incumbents
+  auto search_round = [&](double left, bool dive, float* out_ms) -> int {
+    CK(cudaEventRecord(ctx->ev[0], s));
+    for (int c = 0; c < 2; ++c) {
+      if (cls[c].ntasks <= 0) continue;
+      cudaStream_t cs = ctx->side[c];
+      CK(cudaStreamWaitEvent(cs, ctx->ev[0], 0));
+      CK(cudaMemsetAsync(cls[c].ctl, 0, sizeof(int) * 8, cs));
+      // the wall budget is checked on the device against %globaltimer,
+      // stamped stream-ordered just before the launch
+      k_stamp<<<1, 1, 0, cs>>>(reinterpret_cast<unsigned long long*>(cls[c].ctl + 4));
+      ++launches;
+      SearchArgs A;
+      A.tasks = cls[c].tasks;
+      A.ntasks = (int)cls[c].ntasks;
+      A.ctl = cls[c].ctl;
+      A.stacks = cls[c].stacks;
+      A.cap = cls[c].cap;
+      A.leafbuf = cls[c].leafbuf;
+      A.K = K;
+      // a dive enumerates only boxes of at most one warp round of points:
+      // larger ones are split further (one box per step is cheap), so a
+      // dive never stalls a warp on a long unsat enumeration
+      A.leaf_volume = dive ? 32 : leaf_volume;
+      A.budget_ns = (unsigned long long)(left * 1e9);
+      A.slice_ns = 200000ull;
+      A.dump = cls[c].dump;
+      A.dump_cap = (long long)cls_cap[c];
+      A.box_bytes = cbytes[c];
+      A.pending = d_pend;
+      A.st = d_st;
+      A.units = ctx->units[c];
+      A.width = dive ? 1 : 32;
+      A.max_steps = dive ? dive_steps : 0;
+      A.dive = dive ? 1 : 0;
+      // always the full persistent grid: units without a task idle at once,
+      // which is what triggers redistribution of a lone deep subtree
+      if (c == 0) k_search<i128><<<ctx->ctas[0], SEARCH_THREADS, 0, cs>>>(D, A);
+      else k_search<int64_t><<<ctx->ctas[1], SEARCH_THREADS, SH_BYTES, cs>>>(D, A);
+      ++launches;
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(h_counts + 4 + 2 * c, cls[c].ctl + 2, sizeof(long long),
+                         cudaMemcpyDeviceToHost, cs));
+      CK(cudaEventRecord(ctx->ev[6 + c], cs));
+      cls[c].launches++;
+    }
+    for (int c = 0; c < 2; ++c) {
+      if (cls[c].ntasks <= 0) continue;
+      CK(cudaEventSynchronize(ctx->ev[6 + c]));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[6 + c]);
+      cls[c].ms += ms;
+      long long dumped = dive ? 0 : *reinterpret_cast<long long*>(h_counts + 4 + 2 * c);
+      if (dumped > (long long)cls_cap[c]) dumped = (long long)cls_cap[c];
+      cls[c].ntasks = dumped;
+      void* tmp = cls[c].tasks;
+      cls[c].tasks = cls[c].dump;
+      cls[c].dump = tmp;
+      CK(cudaStreamWaitEvent(s, ctx->ev[6 + c], 0));
+    }
+    CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaEventSynchronize(ctx->ev[1]));
+    cudaEventElapsedTime(out_ms, ctx->ev[0], ctx->ev[1]);
+    return MK_OK;
+  };
+
+  // ---- incumbent dive from every root (the roots stay on the stack)
+  double dive_ms = 0.0;
+  if (dive_steps > 0) {
+    rc = partition(top);
+    if (rc) return rc;
+    if (cls[0].ntasks >= 0) {
+      CK(cudaEventRecord(ctx->ev[5], s));
+      for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(ctx->side[c], ctx->ev[5], 0));
+      float ms = 0.f;
+      rc = search_round(max_seconds, true, &ms);
+      if (rc) return rc;
+      dive_ms = ms;
+    }
+    cls[0].ntasks = cls[1].ntasks = 0;
+  }
   int64_t rounds = 0;
   double bb_ms = 0.0, leaf_ms = 0.0;
-  int* h_counts = static_cast<int*>(ctx->h_pinned);
   bool budget_hit = false;
   while (top > 0) {
     double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1135,42 +1286,18 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
       }
     }
   }
-  // ---- split the remaining boxes into the two classes' task lists
-  if (!budget_hit && top > 0) {
-    if ((size_t)top > cls_cap[0] || (size_t)top > cls_cap[1]) {
-      budget_hit = true;
-    } else {
-      for (int c = 0; c < 2; ++c) {
-        k_class_flags<<<(unsigned)((top + 255) / 256), 256, 0, s>>>(D, stack, top, c, cflag);
-        ++launches;
-        CK(cudaGetLastError());
-        size_t tb = cub_bytes;
-        CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, cflag, cpos, (int)top, s));
-        ++launches;
-        if (c == 0)
-          k_to_class<i128><<<(unsigned)((top + 127) / 128), 128, 0, s>>>(
-              D, static_cast<const char*>(stack), cflag, cpos, top,
-              static_cast<char*>(cls[c].tasks), d_counts + 2 + c);
-        else
-          k_to_class<int64_t><<<(unsigned)((top + 127) / 128), 128, 0, s>>>(
-              D, static_cast<const char*>(stack), cflag, cpos, top,
-              static_cast<char*>(cls[c].tasks), d_counts + 2 + c);
-        ++launches;
-        CK(cudaGetLastError());
-      }
-      CK(cudaMemcpyAsync(h_counts, d_counts + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      cls[0].ntasks = h_counts[0];
-      cls[1].ntasks = h_counts[1];
-      top = 0;
-    }
-  }
   // ---- persistent search: both classes concurrently, bulk-synchronous
   // redistribution of dumped subtrees between launches
-  CK(cudaEventRecord(ctx->ev[5], s));
-  for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(ctx->side[c], ctx->ev[5], 0));
   double search_ms = 0.0;
   int search_launches = 0;
+  if (!budget_hit && top > 0) {
+    rc = partition(top);
+    if (rc) return rc;
+    if (cls[0].ntasks < 0) budget_hit = true;
+    else top = 0;
+  }
+  CK(cudaEventRecord(ctx->ev[5], s));
+  for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(ctx->side[c], ctx->ev[5], 0));
   while (!budget_hit && (cls[0].ntasks > 0 || cls[1].ntasks > 0)) {
     double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     double left = max_seconds - el;
@@ -1178,62 +1305,9 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
       budget_hit = true;
       break;
     }
-    CK(cudaEventRecord(ctx->ev[0], s));
-    for (int c = 0; c < 2; ++c) {
-      if (cls[c].ntasks <= 0) continue;
-      cudaStream_t cs = ctx->side[c];
-      CK(cudaStreamWaitEvent(cs, ctx->ev[0], 0));
-      CK(cudaMemsetAsync(cls[c].ctl, 0, sizeof(int) * 8, cs));
-      // the wall budget is checked on the device against %globaltimer,
-      // stamped stream-ordered just before the launch
-      k_stamp<<<1, 1, 0, cs>>>(reinterpret_cast<unsigned long long*>(cls[c].ctl + 4));
-      ++launches;
-      SearchArgs A;
-      A.tasks = cls[c].tasks;
-      A.ntasks = (int)cls[c].ntasks;
-      A.ctl = cls[c].ctl;
-      A.stacks = cls[c].stacks;
-      A.cap = cls[c].cap;
-      A.leafbuf = cls[c].leafbuf;
-      A.K = K;
-      A.leaf_volume = leaf_volume;
-      A.budget_ns = (unsigned long long)(left * 1e9);
-      A.slice_ns = 200000ull;
-      A.dump = cls[c].dump;
-      A.dump_cap = (long long)cls_cap[c];
-      A.box_bytes = cbytes[c];
-      A.pending = d_pend;
-      A.st = d_st;
-      A.units = ctx->units[c];
-      // always the full persistent grid: units without a task idle at once,
-      // which is what triggers redistribution of a lone deep subtree
-      if (c == 0) k_search<i128><<<ctx->ctas[0], SEARCH_THREADS, 0, cs>>>(D, A);
-      else k_search<int64_t><<<ctx->ctas[1], SEARCH_THREADS, 0, cs>>>(D, A);
-      ++launches;
-      CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(h_counts + 4 + 2 * c, cls[c].ctl + 2, sizeof(long long),
-                         cudaMemcpyDeviceToHost, cs));
-      CK(cudaEventRecord(ctx->ev[6 + c], cs));
-      cls[c].launches++;
-    }
-    for (int c = 0; c < 2; ++c) {
-      if (cls[c].ntasks <= 0) continue;
-      CK(cudaEventSynchronize(ctx->ev[6 + c]));
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[6 + c]);
-      cls[c].ms += ms;
-      long long dumped = *reinterpret_cast<long long*>(h_counts + 4 + 2 * c);
-      if (dumped > (long long)cls_cap[c]) dumped = (long long)cls_cap[c];
-      cls[c].ntasks = dumped;
-      void* tmp = cls[c].tasks;
-      cls[c].tasks = cls[c].dump;
-      cls[c].dump = tmp;
-      CK(cudaStreamWaitEvent(s, ctx->ev[6 + c], 0));
-    }
     float ms = 0.f;
-    CK(cudaEventRecord(ctx->ev[1], s));
-    CK(cudaEventSynchronize(ctx->ev[1]));
-    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    rc = search_round(left, false, &ms);
+    if (rc) return rc;
     search_ms += ms;
     ++search_launches;
   }
@@ -1272,7 +1346,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   local_stats.covered = dst.covered;
   local_stats.insns_bb = (int64_t)dst.insns_bb;
   local_stats.insns_leaf = (int64_t)dst.insns_leaf;
-  local_stats.bb_ms = bb_ms + search_ms;
+  local_stats.bb_ms = bb_ms + search_ms + dive_ms;
   local_stats.leaf_ms = leaf_ms;
   local_stats.seconds =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -58,70 +58,6 @@ __global__ void k_race_root(RaceDev R, int64_t* out) {
   out[1] = Rg[R.off_reg].hi;
 }
 
-// Point evaluation of a narrow problem with the register file in shared
-// memory (register r of thread t at sh[r * blockDim.x + t]: consecutive lanes
-// hit consecutive banks) and the EvalError flags as a bit mask (small
-// problems have <= 64 registers).  Same semantics as mk_core.cuh
-// mk_eval_point<int64_t>; the local-memory register file of the generic
-// evaluator spills to L2 at full occupancy.
-__device__ __forceinline__ bool race_eval_point(const MkProb& P, const int64_t* x, int64_t* sh) {
-  const int nv = P.p->nvars;
-  const int nc = P.p->nconst;
-  const int bd = blockDim.x, t = threadIdx.x;
-  uint64_t err = 0;
-  for (int i = 0; i < nv; ++i) sh[i * bd + t] = x[i];
-  for (int i = 0; i < nc; ++i) sh[(nv + i) * bd + t] = (int64_t)P.consts[i].lo;
-  const int n = P.p->ninsn;
-  for (int k = 0; k < n; ++k) {
-    const mk_insn in = P.insns[k];
-    const int64_t a = sh[in.a * bd + t];
-    const bool ea = (err >> in.a) & 1;
-    if (in.op == MK_OP_ATOM) {
-      if (ea || !a) return false;
-      continue;
-    }
-    const int64_t b = sh[in.b * bd + t];
-    const bool eb = (err >> in.b) & 1;
-    int64_t r = 0;
-    bool e = false;
-    switch (in.op) {
-      case MK_OP_AND: if (ea) e = true; else if (!a) r = 0; else { r = b ? 1 : 0; e = eb; } break;
-      case MK_OP_OR: if (ea) e = true; else if (a) r = 1; else { r = b ? 1 : 0; e = eb; } break;
-      case MK_OP_NOT: e = ea; r = a ? 0 : 1; break;
-      case MK_OP_ITE: {
-        const int64_t c = sh[in.c * bd + t];
-        const bool ec = (err >> in.c) & 1;
-        if (ea) e = true; else if (a) { r = b; e = eb; } else { r = c; e = ec; }
-        break;
-      }
-      default:
-        e = ea || eb;
-        if (!e) {
-          switch (in.op) {
-            case MK_OP_ADD: r = a + b; break;
-            case MK_OP_SUB: r = a - b; break;
-            case MK_OP_MUL: r = a * b; break;
-            case MK_OP_SHL: r = MkNum<int64_t>::shl(a, (int)b); break;
-            case MK_OP_SHR: r = MkNum<int64_t>::shr(a, (int)b); break;
-            case MK_OP_DIV: if (b == 0) e = true; else r = a / b; break;
-            case MK_OP_MOD: if (b == 0) e = true; else r = a % b; break;
-            case MK_OP_EMOD: if (b == 0) e = true; else r = mk_emod_c<int64_t>(a, b); break;
-            case MK_OP_EQ: r = a == b; break;
-            case MK_OP_NE: r = a != b; break;
-            case MK_OP_LT: r = a < b; break;
-            case MK_OP_LE: r = a <= b; break;
-            case MK_OP_GT: r = a > b; break;
-            case MK_OP_GE: r = a >= b; break;
-            default: break;
-          }
-        }
-    }
-    sh[in.dst * bd + t] = r;
-    err = e ? (err | (1ull << in.dst)) : (err & ~(1ull << in.dst));
-  }
-  return true;
-}
-
 // dense generation: slot idx holds instance idx's key, or the all-ones
 // sentinel (sorted past every real key) when the instance is not an access.
 // Positions are the instance order, so the stable radix sort leaves equal
@@ -163,7 +99,7 @@ __global__ void __launch_bounds__(RACE_THREADS) k_race_gen(RaceDev R, unsigned l
         jj /= (unsigned long long)span[i];
       }
       ++done;
-      if (race_eval_point(R.P, x, sh)) {
+      if (sh_eval_point(R.P, x, sh)) {
         const unsigned long long ok =
             (unsigned long long)(sh[R.off_reg * blockDim.x + threadIdx.x] - R.off_lo);
         key = (K)(ok * R.nblocks + (R.shared ? race_block_key(R, x) : 0ull));
