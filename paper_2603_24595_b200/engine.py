@@ -92,8 +92,11 @@ class CompilePool:
 
 
 def default_workers() -> int:
+    """Host cores per GPU process (torchrun's LOCAL_WORLD_SIZE ranks share the
+    host), one left for the process itself, at most 16."""
     n = os.cpu_count() or 1
-    return max(1, min(16, n // 2))
+    local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    return max(1, min(16, n // local - 1))
 
 
 class SiteChecker:
@@ -109,7 +112,7 @@ class SiteChecker:
         if limits:
             self.limits.update(limits)
         self.stats = BatchStats()
-        # 0 / 1: compile inline; None: one worker per two host cores
+        # 0 / 1: compile inline; None: default_workers()
         self.compile_workers = default_workers() if compile_workers is None else compile_workers
         self._pool: Optional[CompilePool] = None
 

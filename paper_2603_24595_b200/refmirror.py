@@ -380,9 +380,17 @@ def _replace_all(e: Node, old: Node, new: Node) -> Node:
 
 def count_paths(assertions: Sequence[Node], cap: int) -> int:
     """Restates boolean_paths' traversal and cap check; returns the number of
-    surviving paths or raises GiveUp exactly when the reference raises."""
+    surviving paths or raises GiveUp exactly when the reference raises.
+
+    Pending conjunct lists are persistent cons lists ((head, tail) pairs,
+    None at the end): the reference's ``[x] + pending`` prepends and
+    ``pending.pop(0)`` become O(1) while the traversal order, and so every
+    ``len(work) + done > cap`` check, is unchanged."""
     done = 0
-    work: List[List[Node]] = [list(assertions)]
+    pend0 = None
+    for a in reversed(list(assertions)):
+        pend0 = (a, pend0)
+    work: List[object] = [pend0]
     simp: Dict[Node, Node] = {}
     # integer if-then-else never appears unless the input has one
     has_ite = any(_find_any_ite(a) for a in assertions)
@@ -391,8 +399,8 @@ def count_paths(assertions: Sequence[Node], cap: int) -> int:
             raise GiveUp(f"more than {cap} case splits")
         pending = work.pop()
         alive = True
-        while pending:
-            raw = pending.pop(0)
+        while pending is not None:
+            raw, pending = pending
             e = simp.get(raw)
             if e is None:
                 e = ir.simplify(raw)
@@ -407,18 +415,19 @@ def count_paths(assertions: Sequence[Node], cap: int) -> int:
                 break
             if t == "o":
                 if e[1] == "and":
-                    pending = list(e[2]) + pending
+                    for arm in reversed(e[2]):
+                        pending = (arm, pending)
                     continue
                 if e[1] == "not":
-                    pending.insert(0, _negate(e[2][0]))
+                    pending = (_negate(e[2][0]), pending)
                     continue
                 for arm in reversed(e[2]):
-                    work.append([arm] + pending)
+                    work.append((arm, pending))
                 alive = False
                 break
             if t == "i":
-                work.append([_negate(e[1]), e[3]] + pending)
-                work.append([e[1], e[2]] + pending)
+                work.append((_negate(e[1]), (e[3], pending)))
+                work.append((e[1], (e[2], pending)))
                 alive = False
                 break
             if t == "s":
@@ -430,13 +439,13 @@ def count_paths(assertions: Sequence[Node], cap: int) -> int:
                 if ite is not None:
                     then_atom = _replace_all(e, ite, ite[2])
                     else_atom = _replace_all(e, ite, ite[3])
-                    work.append([_negate(ite[1]), else_atom] + pending)
-                    work.append([ite[1], then_atom] + pending)
+                    work.append((_negate(ite[1]), (else_atom, pending)))
+                    work.append((ite[1], (then_atom, pending)))
                     alive = False
                     break
                 if e[1] == "ne":
-                    work.append([("p", "gt", e[2], e[3])] + pending)
-                    work.append([("p", "lt", e[2], e[3])] + pending)
+                    work.append((("p", "gt", e[2], e[3]), pending))
+                    work.append((("p", "lt", e[2], e[3]), pending))
                     alive = False
                     break
                 continue
