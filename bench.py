@@ -241,6 +241,39 @@ CORPUS = ["rotary_embedding", "rotary_llama2_7b", "rotary_mistral_7b", "rotary_l
           "rotary_qwen2_7b", "rotary_llama2_13b", "rotary_mixtral_8x7b", "rotary_gemma_7b"]
 
 
+def _heavy_line(chk, args, int_peak, sm_mhz, sms):
+    """The search kernels at scale: BASELINE configs[2] (paged attention,
+    Mistral-7B), whose step is ~4e8 boxes, timed resident like the headline
+    step; roofline from the same ncu calibration scheme."""
+    doc, queries = _load_workload(args.heavy)
+    from paper_2603_24595_b200.engine import compile_all
+
+    compiled = compile_all(queries)
+    packed, _ = chk.pack([c for c, _ in compiled])
+    resident = chk.engine.upload(packed)
+    lim = dict(chk.limits)
+    lim["max_seconds"] = 600.0
+    resident.run(lim)
+    runs = [resident.run(lim) for _ in range(2)]
+    resident.free()
+    ms = sum(r["bb_ms"] + r["leaf_ms"] for r in runs) / len(runs)
+    step_ms = sum(r["device_ms"] for r in runs) / len(runs)
+    units = sum(r["boxes"] + r["points"] for r in runs) / len(runs)
+    cal = _calibration(args.heavy)
+    per_unit = cal.get("thread_inst_per_unit")
+    achieved = units * per_unit / (ms / 1e3) if per_unit and ms > 0 else None
+    return {"workload": args.heavy, "description": CONFIG_NAMES.get(args.heavy),
+            "device_ms_per_step": step_ms, "boxes_and_instances_per_step": units,
+            "roofline": {"bound": "int32-issue",
+                         "achieved": achieved / 1e9 if achieved else None,
+                         "peak": int_peak / 1e9, "unit": "Gop/s",
+                         "frac": achieved / int_peak if achieved else None,
+                         "kernel": "k_search (+k_bb, k_leaf)", "kernel_ms_per_step": ms,
+                         "ops": f"SASS thread instructions per box/instance: {per_unit} (ncu, "
+                                f"profiles/ncu_{args.heavy}_summary.json)",
+                         "ncu_issue_active_pct": cal.get("k_search_issue_active_pct")}}
+
+
 def _race_sweep_line(chk, args, peaks, src):
     """K2 (sort-based race sweep, include/mk_b200.h mk_race_sweep) on config
     1's output store (rms_norm, Llama-2-7B hidden 4096: out[blockIdx.x *
@@ -404,6 +437,8 @@ def run_b200(args):
         ops = "bytecode instructions executed (no ncu calibration committed)"
 
     k2 = _race_sweep_line(chk, args, peaks, src) if rank == 0 and args.race_tokens > 0 else None
+    heavy = (_heavy_line(chk, args, int_peak, sm_mhz, sms)
+             if rank == 0 and world == 1 and args.heavy and args.heavy != args.workload else None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -459,6 +494,7 @@ def run_b200(args):
                                         f"(clock sampled; peaks file: {src})"},
             "cpu_baseline": cpu,
             "k2_race_sweep": k2,
+            "k1_heavy": heavy,
             "clocks": clk,
             "gpu_launches": launches,
         }
@@ -478,6 +514,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--heavy", default="paged_attention_v1",
+                    help="workload of the k1_heavy line ('' to skip)")
     ap.add_argument("--race-tokens", type=int, default=262144,
                     help="num_tokens of the K2 race-sweep line (0: skip)")
     args = ap.parse_args()

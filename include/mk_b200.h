@@ -154,6 +154,7 @@ typedef struct mk_stats {
   int64_t insns_leaf;   /* bytecode instructions executed by the leaf kernel */
   double device_ms;     /* CUDA-event time of the whole call on the engine stream */
   int64_t launches;     /* kernels launched by the call */
+  int64_t steps;        /* warp search steps (boxes / steps = lanes busy per step) */
 } mk_stats;
 
 typedef struct mk_ctx mk_ctx;

@@ -48,6 +48,7 @@ constexpr int SMALL_V = 8;    // free symbols of a "small" problem
 constexpr int SMALL_R = 64;   // registers of a "small" problem
 constexpr int SH_R = 24;      // registers of a narrow problem evaluated from shared memory
 constexpr int SH_BYTES = 2 * SH_R * 128 * (int)sizeof(int64_t);  // per 128-thread CTA
+constexpr int DIVE_CAP = 1024;  // boxes per speculative-dive stack
 
 // dynamic shared memory of k_search<int64_t>: lo / hi interval register files
 extern __shared__ int64_t mk_dyn_sh[];
@@ -87,19 +88,20 @@ struct DevSet {
 };
 
 struct DevStats {
-  unsigned long long boxes, leaves, points, insns_bb, insns_leaf;
+  unsigned long long boxes, leaves, points, insns_bb, insns_leaf, steps;
   double covered;
 };
 
 // per-lane counters, flushed to DevStats once per unit
 struct LaneStats {
-  unsigned long long boxes, leaves, points, insns_bb, insns_leaf;
+  unsigned long long boxes, leaves, points, insns_bb, insns_leaf, steps;
   double covered;
   __device__ void zero() {
-    boxes = leaves = points = insns_bb = insns_leaf = 0;
+    boxes = leaves = points = insns_bb = insns_leaf = steps = 0;
     covered = 0.0;
   }
   __device__ void flush(DevStats* st) {
+    if (steps) atomicAdd(&st->steps, steps);
     if (boxes) atomicAdd(&st->boxes, boxes);
     if (leaves) atomicAdd(&st->leaves, leaves);
     if (points) atomicAdd(&st->points, points);
@@ -114,6 +116,7 @@ struct LaneStats {
       points += __shfl_down_sync(FULL, points, o);
       insns_bb += __shfl_down_sync(FULL, insns_bb, o);
       insns_leaf += __shfl_down_sync(FULL, insns_leaf, o);
+      steps += __shfl_down_sync(FULL, steps, o);
       covered += __shfl_down_sync(FULL, covered, o);
     }
     if ((threadIdx.x & 31) == 0) flush(st);
@@ -549,6 +552,7 @@ struct SearchArgs {
   int width;         // boxes popped per step (32; 1 in a dive)
   int max_steps;     // steps per task (0: unbounded)
   int dive;          // incumbent dive: no spills, dumps or pending marks
+  const int* stop;   // dive: the main search has finished (polled per step)
 };
 
 // TASK_DUMPED: redistribution (every task has been handed out), the unit
@@ -614,6 +618,7 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
       continue;
     }
     const long long base = top - n;
+    if (lane == 0) st.steps++;
     V lo[CAPV], hi[CAPV];
     Act a;
     a.kind = ACT_DONE;
@@ -660,7 +665,9 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
       if (!ctlw && !A.dive && top > 0 && idle * 4 >= A.units && now - t_start > A.slice_ns)
         ctlw = 2;
     }
+    if (A.dive && lane == 0 && *((volatile const int*)A.stop)) ctlw = 3;
     ctlw = __shfl_sync(FULL, ctlw, 0);
+    if (ctlw == 3) return TASK_DONE;
     if (A.max_steps && ++steps >= A.max_steps) return TASK_DONE;
     if (ctlw == 1) return top > 0 ? TASK_ABORT : TASK_DONE;
     // a redistribution dump that does not fit simply keeps searching
@@ -796,7 +803,8 @@ struct mk_ctx {
   std::string err;
   cudaStream_t stream = nullptr;
   cudaStream_t side[2] = {nullptr, nullptr};
-  cudaEvent_t ev[8] = {};
+  cudaStream_t dive[2] = {nullptr, nullptr};  // speculative incumbent dives
+  cudaEvent_t ev[12] = {};
   // growable device buffers
   mk_dset scratch;
   void* d_work = nullptr;
@@ -848,7 +856,8 @@ extern "C" int mk_ctx_create(int device, mk_ctx** out) {
     return MK_ECUDA;
   }
   for (int c = 0; c < 2; ++c) cudaStreamCreateWithFlags(&ctx->side[c], cudaStreamNonBlocking);
-  for (int i = 0; i < 8; ++i) cudaEventCreate(&ctx->ev[i]);
+  for (int c = 0; c < 2; ++c) cudaStreamCreateWithFlags(&ctx->dive[c], cudaStreamNonBlocking);
+  for (int i = 0; i < 12; ++i) cudaEventCreate(&ctx->ev[i]);
   cudaMallocHost(&ctx->h_pinned, 4096);
   {
     int sms = 0, per_wide = 0, per_narrow = 0;
@@ -874,11 +883,13 @@ extern "C" int mk_ctx_destroy(mk_ctx* ctx) {
   if (ctx->d_work) cudaFree(ctx->d_work);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   if (ctx->h_race) cudaFree(ctx->h_race);
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 12; ++i)
     if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
   if (ctx->scratch.d) cudaFree(ctx->scratch.d);
   for (int c = 0; c < 2; ++c)
     if (ctx->side[c]) cudaStreamDestroy(ctx->side[c]);
+  for (int c = 0; c < 2; ++c)
+    if (ctx->dive[c]) cudaStreamDestroy(ctx->dive[c]);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return MK_OK;
@@ -984,7 +995,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   // incumbent dive: steps of width 1 from every root before the search
   // (mk_limits.chunk < -1 disables it; a model found early prunes the
   // parallel search, whose units would otherwise explore worse subtrees)
-  const int dive_steps = lim && lim->chunk < -1 ? 0 : 48;
+  const int dive_steps = lim && lim->chunk < -1 ? 0 : 4096;
   const size_t box_bytes = sizeof(Box) + 2 * sizeof(mk_i128) * (size_t)S;
   char* base = static_cast<char*>(ds->d);
   cudaStream_t s = ctx->stream;
@@ -1044,6 +1055,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   size_t w_leaves = wplace(box_bytes * (size_t)chunk);
   size_t w_cub = wplace(cub_bytes + 256);
   size_t w_cls[2][6];
+  size_t w_dive[2][4];
   long long unit_cap[2];
   for (int c = 0; c < 2; ++c) {
     const int units = ctx->units[c];
@@ -1057,7 +1069,12 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     w_cls[c][2] = wplace(cbytes[c] * (size_t)cap * units);           // unit stacks
     w_cls[c][3] = wplace(cbytes[c] * (size_t)32 * units);            // unit leaf lists
     w_cls[c][4] = wplace(sizeof(int) * 8);                           // control block
+    w_dive[c][0] = wplace(cbytes[c] * (size_t)(nprob + 1));          // dive tasks (roots)
+    w_dive[c][1] = wplace(cbytes[c] * (size_t)DIVE_CAP * (nprob + 4)); // dive stacks
+    w_dive[c][2] = wplace(cbytes[c] * (size_t)32 * (nprob + 4));     // dive leaf lists
+    w_dive[c][3] = wplace(sizeof(int) * 8);                          // dive control block
   }
+  const size_t w_stop = wplace(sizeof(int) * 8);
   rc = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, w);
   if (rc) return rc;
   char* wb = static_cast<char*>(ctx->d_work);
@@ -1070,6 +1087,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   int* lpos = reinterpret_cast<int*>(wb + w_lpos);
   char* leaves = wb + w_leaves;
   void* cub_tmp = wb + w_cub;
+  int* d_stop = reinterpret_cast<int*>(wb + w_stop);
   ClassRun cls[2];
   for (int c = 0; c < 2; ++c) {
     cls[c].tasks = wb + w_cls[c][0];
@@ -1092,12 +1110,16 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   CK(cudaGetLastError());
   long long top = nprob;
   int* h_counts = static_cast<int*>(ctx->h_pinned);
+  double dive_ms = 0.0;
+  bool diving = false;
+  int dive_ctas[2] = {0, 0};
+  const unsigned long long dive_budget_ns = 3000000ull;
 
   // split boxes [0, n) of the int128 stack into the two classes' task lists
   // (class storage); ntasks = -1 when they do not fit
-  auto partition = [&](long long n) -> int {
+  auto partition_to = [&](long long n, void* const dst[2], long long out[2]) -> int {
     if ((size_t)n > cls_cap[0] || (size_t)n > cls_cap[1]) {
-      cls[0].ntasks = cls[1].ntasks = -1;
+      out[0] = out[1] = -1;
       return MK_OK;
     }
     for (int c = 0; c < 2; ++c) {
@@ -1109,20 +1131,28 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
       ++launches;
       if (c == 0)
         k_to_class<i128><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
-            D, static_cast<const char*>(stack), cflag, cpos, n, static_cast<char*>(cls[c].tasks),
+            D, static_cast<const char*>(stack), cflag, cpos, n, static_cast<char*>(dst[c]),
             d_counts + 2 + c);
       else
         k_to_class<int64_t><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(
-            D, static_cast<const char*>(stack), cflag, cpos, n, static_cast<char*>(cls[c].tasks),
+            D, static_cast<const char*>(stack), cflag, cpos, n, static_cast<char*>(dst[c]),
             d_counts + 2 + c);
       ++launches;
       CK(cudaGetLastError());
     }
     CK(cudaMemcpyAsync(h_counts, d_counts + 2, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    cls[0].ntasks = h_counts[0];
-    cls[1].ntasks = h_counts[1];
+    out[0] = h_counts[0];
+    out[1] = h_counts[1];
     return MK_OK;
+  };
+  auto partition = [&](long long n) -> int {
+    void* const dst[2] = {cls[0].tasks, cls[1].tasks};
+    long long out[2];
+    int r = partition_to(n, dst, out);
+    cls[0].ntasks = out[0];
+    cls[1].ntasks = out[1];
+    return r;
   };
   // one launch of both classes' persistent grids on their streams; a dive
   // follows only the best box of each root for a few steps (width 1, no
@@ -1161,10 +1191,17 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
       A.width = dive ? 1 : 32;
       A.max_steps = dive ? dive_steps : 0;
       A.dive = dive ? 1 : 0;
+      A.stop = d_stop;
       // always the full persistent grid: units without a task idle at once,
       // which is what triggers redistribution of a lone deep subtree
-      if (c == 0) k_search<i128><<<ctx->ctas[0], SEARCH_THREADS, 0, cs>>>(D, A);
-      else k_search<int64_t><<<ctx->ctas[1], SEARCH_THREADS, SH_BYTES, cs>>>(D, A);
+      // the persistent grid leaves the slots of a running dive free, so
+      // every CTA of it is resident at once
+      if (dive_ctas[c] && cudaEventQuery(ctx->ev[8 + c]) == cudaSuccess) dive_ctas[c] = 0;
+      int grid = ctx->ctas[c] - dive_ctas[c];
+      if (grid < ctx->sms) grid = ctx->sms;
+      A.units = grid * WARPS_PER_CTA;
+      if (c == 0) k_search<i128><<<grid, SEARCH_THREADS, 0, cs>>>(D, A);
+      else k_search<int64_t><<<grid, SEARCH_THREADS, SH_BYTES, cs>>>(D, A);
       ++launches;
       CK(cudaGetLastError());
       CK(cudaMemcpyAsync(h_counts + 4 + 2 * c, cls[c].ctl + 2, sizeof(long long),
@@ -1192,21 +1229,63 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     return MK_OK;
   };
 
-  // ---- incumbent dive from every root (the roots stay on the stack)
-  double dive_ms = 0.0;
+  // ---- speculative incumbent dives, one warp per root, concurrent with the
+  // pre-split and the parallel search: width-1 best-first DFS (the serial
+  // search order) that offers models as soon as it meets them, so the wide
+  // search prunes by them; stopped through d_stop when the search is done
+
+  CK(cudaMemsetAsync(d_stop, 0, sizeof(int), s));
   if (dive_steps > 0) {
-    rc = partition(top);
+    void* const dst[2] = {wb + w_dive[0][0], wb + w_dive[1][0]};
+    long long nt[2];
+    rc = partition_to(top, dst, nt);
     if (rc) return rc;
-    if (cls[0].ntasks >= 0) {
+    if (nt[0] >= 0) {
       CK(cudaEventRecord(ctx->ev[5], s));
-      for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(ctx->side[c], ctx->ev[5], 0));
-      float ms = 0.f;
-      rc = search_round(max_seconds, true, &ms);
-      if (rc) return rc;
-      dive_ms = ms;
+      for (int c = 0; c < 2; ++c) {
+        if (nt[c] <= 0) continue;
+        cudaStream_t ds = ctx->dive[c];
+        CK(cudaStreamWaitEvent(ds, ctx->ev[5], 0));
+        int* dctl = reinterpret_cast<int*>(wb + w_dive[c][3]);
+        CK(cudaMemsetAsync(dctl, 0, sizeof(int) * 8, ds));
+        k_stamp<<<1, 1, 0, ds>>>(reinterpret_cast<unsigned long long*>(dctl + 4));
+        ++launches;
+        SearchArgs A;
+        A.tasks = dst[c];
+        A.ntasks = (int)nt[c];
+        A.ctl = dctl;
+        A.stacks = wb + w_dive[c][1];
+        A.cap = DIVE_CAP;
+        A.leafbuf = wb + w_dive[c][2];
+        A.K = K;
+        A.leaf_volume = 32;
+        // a dive is a heuristic: a fixed time budget bounds what it can
+        // cost the step (it exits earlier when its tree is exhausted)
+        A.budget_ns = dive_budget_ns;
+        A.slice_ns = 200000ull;
+        A.dump = nullptr;
+        A.dump_cap = 0;
+        A.box_bytes = cbytes[c];
+        A.pending = d_pend;
+        A.st = d_st;
+        const int grid = (int)((nt[c] + WARPS_PER_CTA - 1) / WARPS_PER_CTA);
+        A.units = grid * WARPS_PER_CTA;
+        A.width = 1;
+        A.max_steps = dive_steps;
+        A.dive = 1;
+        A.stop = d_stop;
+        if (c == 0) k_search<i128><<<grid, SEARCH_THREADS, 0, ds>>>(D, A);
+        else k_search<int64_t><<<grid, SEARCH_THREADS, SH_BYTES, ds>>>(D, A);
+        ++launches;
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ctx->ev[8 + c], ds));
+      }
+      diving = true;
+      for (int c = 0; c < 2; ++c)
+        dive_ctas[c] = nt[c] > 0 ? (int)((nt[c] + WARPS_PER_CTA - 1) / WARPS_PER_CTA) : 0;
     }
-    cls[0].ntasks = cls[1].ntasks = 0;
   }
+
   int64_t rounds = 0;
   double bb_ms = 0.0, leaf_ms = 0.0;
   bool budget_hit = false;
@@ -1311,6 +1390,10 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     search_ms += ms;
     ++search_launches;
   }
+  if (diving) {
+    CK(cudaMemsetAsync(d_stop, 1, sizeof(int), s));
+    for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(s, ctx->ev[8 + c], 0));
+  }
   for (int c = 0; c < 2; ++c) {
     if (budget_hit && cls[c].ntasks > 0) {
       k_mark_pending<<<(unsigned)((cls[c].ntasks + 255) / 256), 256, 0, s>>>(
@@ -1356,6 +1439,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     local_stats.device_ms = dms;
   }
   local_stats.launches = launches;
+  local_stats.steps = (int64_t)dst.steps;
   if (stats) *stats = local_stats;
   return MK_OK;
 }

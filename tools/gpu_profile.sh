@@ -11,6 +11,6 @@ timeout 600 python bench.py --impl reference --workload $W --steps 3 --warmup 1 
 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum,smsp__thread_inst_executed.sum,smsp__inst_executed.sum \
     --clock-control none --csv --log-file gpurun_out/launches_$W.csv \
     python tools/profile_step.py $W > gpurun_out/step_$W.json 2> gpurun_out/step_$W.err
-timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_search -c 1 \
+timeout 1500 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:k_search -s 2 -c 2 \
     -o gpurun_out/prof_$W -f python tools/profile_step.py $W > gpurun_out/ncu_full_$W.log 2>&1
 ls -la gpurun_out

@@ -20,5 +20,5 @@ for i in want:
     lim = {"max_seconds": 60.0, **extra}
     r = eng.solve([probs[i]], lim)
     st = eng.last_stats
-    print(i, r, {k: st[k] for k in ("boxes", "leaves", "points", "rounds", "device_ms", "launches")},
+    print(i, r, {k: st[k] for k in ("boxes", "leaves", "points", "rounds", "device_ms", "launches", "steps")},
           flush=True)

@@ -64,7 +64,10 @@ def full(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    # the longest captured launch (the steady-state search, not the dive)
+    it = hdr.index("gpu__time_duration.sum")
+    vals = max(rows[2:], key=lambda r: float(r[it].replace(",", "") or 0))
     want = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "smsp__issue_active.avg.pct_of_peak_sustained_active",
             "sm__warps_active.avg.pct_of_peak_sustained_active",
