@@ -507,6 +507,41 @@ def _truth(e: Node, ivl: "_Ivl") -> str:
     return "?"
 
 
+def linear_truth(a: Node, ivl: "_Ivl") -> str:
+    """Truth of a comparison atom over a box with the comparison's two sides
+    cancelled as one exact linear form (``(1024*k + t) - t`` is ``1024*k``):
+    symbols contribute exact ranges, opaque nonlinear terms interval ones.
+    'T' / 'F' when decided on the whole box, '?' otherwise."""
+    if a[0] != "p":
+        return "?"
+    try:
+        terms, c0 = _lin_add(_Lin({}).lin(a[2]), _Lin({}).lin(a[3]), -1)
+    except CompileError:
+        return "?"
+    lo = hi = c0
+    for k, c in terms.items():
+        r = ivl.bounds.get(k, (None, None)) if isinstance(k, str) else ivl(k)
+        if r[0] is None or r[1] is None:
+            return "?"
+        x, y = c * r[0], c * r[1]
+        lo += min(x, y)
+        hi += max(x, y)
+    op = a[1]
+    if op == "le":
+        return "T" if hi <= 0 else ("F" if lo > 0 else "?")
+    if op == "lt":
+        return "T" if hi < 0 else ("F" if lo >= 0 else "?")
+    if op == "ge":
+        return "T" if lo >= 0 else ("F" if hi < 0 else "?")
+    if op == "gt":
+        return "T" if lo > 0 else ("F" if hi <= 0 else "?")
+    if op == "eq":
+        return "T" if lo == hi == 0 else ("F" if lo > 0 or hi < 0 else "?")
+    if op == "ne":
+        return "T" if lo > 0 or hi < 0 else ("F" if lo == hi == 0 else "?")
+    return "?"
+
+
 def _form_key(terms: Dict[object, int]) -> Tuple[Tuple, int]:
     """(normalised form, factor) with terms == factor * form, the form
     gcd-reduced with its first coefficient positive."""
@@ -1274,7 +1309,8 @@ def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
     # interval proof, no possible EvalError) leaves the model set unchanged:
     # drop it (typically the far side of an overflow pin, x <= 2^63 - 1)
     ivl = _Ivl({n: (a, b) for n, a, b in zip(var_names, lo, hi)})
-    atoms = [a for a in atoms if _may_err(a) or _truth(a, ivl) != "T"]
+    atoms = [a for a in atoms
+             if _may_err(a) or (_truth(a, ivl) != "T" and linear_truth(a, ivl) != "T")]
     # cheap linear rows first: a definitely-false atom ends evaluation early
     atoms = sorted(atoms, key=lambda a: (0 if a[0] == "p" and a[1] in ("le", "eq") else 1))
     for i, a in enumerate(atoms):

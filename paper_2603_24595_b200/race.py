@@ -28,7 +28,7 @@ from typing import Callable, Dict, List, Mapping, Optional, Sequence, Tuple
 
 from . import ir
 from .compiler import (CompileError, Problem, _Emitter, _Ivl, _Lin, _Presolve, _may_err,
-                       _truth, narrow_proof)
+                       _truth, linear_truth, narrow_proof)
 
 THREAD_PRIVATE = frozenset({"thread-id", "loop-index", "havoc"})   # engine/state.py:32
 ID_NAMES = ("blockIdx.x", "blockIdx.y", "blockIdx.z", "threadIdx.x", "threadIdx.y", "threadIdx.z")
@@ -290,7 +290,8 @@ def race_program(assertions: Sequence[ir.Node], origin_of: Callable[[str], str],
         bounds[n] = b
     # atoms that hold without error on the whole box (sound interval proof)
     ivl = _Ivl(dict(bounds))
-    atoms = [a for a in atoms if _may_err(a) or _truth(a, ivl) != "T"]
+    atoms = [a for a in atoms
+             if _may_err(a) or (_truth(a, ivl) != "T" and linear_truth(a, ivl) != "T")]
     # components touching neither the offset nor a thread identity only
     # gate feasibility: decide them once and drop them
     relevant = set(ir.symbols_of(offset)) | {n for n in ID_NAMES if n in free}
