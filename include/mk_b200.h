@@ -220,6 +220,8 @@ typedef struct mk_race_result {
   int64_t offset;       /* its byte offset */
   double gen_ms, sort_ms, scan_ms;  /* CUDA-event time of the three phases */
   uint64_t hbm_bytes;   /* algorithmic HBM bytes moved by the three phases */
+  int32_t jit;          /* 1: generator specialised at run time (NVRTC), 0: interpreted */
+  int32_t sorted;       /* 1: the keys arrived in order and the sort was skipped */
 } mk_race_result;
 
 int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out);

@@ -39,6 +39,7 @@
 
 #include "mk_b200.h"
 #include "mk_core.cuh"
+#include "mk_jit.cuh"
 #include "mk_shreg.cuh"
 
 namespace {
@@ -811,6 +812,7 @@ struct mk_ctx {
   size_t d_work_bytes = 0;
   void* h_pinned = nullptr;
   void* h_race = nullptr;  // device side buffer of the race sweep
+  mkjit::Cache jit;        // specialised race generators, by source
 };
 
 static int fail(mk_ctx* ctx, int code, const std::string& msg) {

@@ -20,6 +20,8 @@
 //                pair after the sort); warp-aggregated count + atomicMin of
 //                the first conflicting position.
 
+#include <thrust/iterator/transform_iterator.h>
+
 namespace {
 
 constexpr int RACE_THREADS = 256;
@@ -128,18 +130,26 @@ __global__ void __launch_bounds__(RACE_THREADS) k_race_gen(RaceDev R, unsigned l
   }
 }
 
+// Adjacent-conflict scan over n tuples (n read on the device).  When
+// `unsorted` is given the scan also reports whether the keys are out of order
+// (the sweep then sorts and scans again: results of an unsorted pass are
+// discarded).
 template <typename K>
 __global__ void __launch_bounds__(RACE_THREADS) k_race_scan(RaceDev R, const K* keys,
                                                             const uint32_t* vals,
                                                             const unsigned long long* count,
                                                             unsigned long long* conflicts,
-                                                            unsigned long long* first) {
-  const unsigned long long n = *count;  // real tuples sort before the sentinels
+                                                            unsigned long long* first,
+                                                            unsigned long long* unsorted) {
+  const unsigned long long n = *count;
   int64_t xa[SMALL_V], xb[SMALL_V];
   unsigned long long mine = 0, my_first = ~0ull;
+  bool down = false;
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    if (keys[i] != keys[i - 1]) continue;
+    const K a = keys[i - 1], b = keys[i];
+    if (b < a) down = true;
+    if (a != b) continue;
     // identities are leading vars: decode the instance of the leading box
     mk_decode(R.lo, R.hi, R.n_outer, R.prob->maxmask, (unsigned long long)vals[i - 1], xa);
     mk_decode(R.lo, R.hi, R.n_outer, R.prob->maxmask, (unsigned long long)vals[i], xb);
@@ -163,14 +173,22 @@ __global__ void __launch_bounds__(RACE_THREADS) k_race_scan(RaceDev R, const K* 
     if (mine) atomicAdd(conflicts, mine);
     if (my_first != ~0ull) atomicMin(first, my_first);
   }
+  if (unsorted && __any_sync(FULL, down) && (threadIdx.x & 31) == 0) atomicOr(unsorted, 1ull);
 }
+
+template <typename K>
+struct NotSentinel {
+  K sentinel;
+  __host__ __device__ bool operator()(const K& k) const { return k != sentinel; }
+};
 
 }  // namespace
 
 
 template <typename K>
 static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int bits, int nregs,
-                    mk_race_result* out, char* base, unsigned long long* ctr) {
+                    mk_race_result* out, char* base, unsigned long long* ctr,
+                    const mk_race_prog* prog, const int64_t* hlo, const int64_t* hhi) {
   cudaStream_t s = ctx->stream;
   // tuples: keys + values, double buffered for the sort
   size_t cub_bytes = 0;
@@ -178,6 +196,15 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
     cub::DoubleBuffer<K> kb(nullptr, nullptr);
     cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
     cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, kb, vb, (int)vol, 0, bits, s);
+    size_t t1 = 0, t2 = 0;
+    NotSentinel<K> pred{(K)0};
+    auto flags = thrust::make_transform_iterator((const K*)nullptr, pred);
+    cub::DeviceSelect::If(nullptr, t1, (const K*)nullptr, (K*)nullptr,
+                          (unsigned long long*)nullptr, (int)vol, pred, s);
+    cub::DeviceSelect::Flagged(nullptr, t2, (const uint32_t*)nullptr, flags, (uint32_t*)nullptr,
+                               (unsigned long long*)nullptr, (int)vol, s);
+    if (t1 > cub_bytes) cub_bytes = t1;
+    if (t2 > cub_bytes) cub_bytes = t2;
   }
   size_t off = 0;
   auto place = [&](size_t bytes) {
@@ -198,26 +225,73 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   (void)base;
   const int grid = ctx->sms * 8;
   const K sentinel = (K)(bits >= (int)(8 * sizeof(K)) ? ~(K)0 : (((K)1 << bits) - 1));
+  // specialised generator (NVRTC) when available, else the interpreter
+  cudaKernel_t jk = nullptr;
+  if (!getenv("MK_NO_JIT")) {
+    const mk_problem_set& set = prog->set;
+    const std::string src = mkjit::race_gen_source(
+        set.probs[0], set.insns + set.probs[0].insn_off, set.consts + set.probs[0].const_off,
+        R.n_outer, prog->off_reg, prog->shared, prog->id_var, hlo, hhi, sizeof(K) == 8);
+    jk = mkjit::get_kernel(ctx->jit, src, ctx->device);
+  }
+  out->jit = jk != nullptr;
   CK(cudaEventRecord(ctx->ev[0], s));
-  const size_t shm = sizeof(int64_t) * (size_t)nregs * RACE_THREADS;
-  if (shm > 48 * 1024)
-    CK(cudaFuncSetAttribute(k_race_gen<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-  k_race_gen<K><<<grid, RACE_THREADS, shm, s>>>(R, vol, sentinel, k0, v0, ctr + 0, ctr + 3);
+  if (jk) {
+    unsigned long long a_vol = vol, a_nb = R.nblocks;
+    K a_sent = sentinel;
+    K* a_keys = k0;
+    uint32_t* a_vals = v0;
+    unsigned long long* a_cnt = ctr + 0;
+    unsigned long long* a_eval = ctr + 3;
+    long long a_off = R.off_lo;
+    void* args[] = {&a_vol, &a_sent, &a_keys, &a_vals, &a_cnt, &a_eval, &a_off, &a_nb};
+    CK(cudaLaunchKernel((const void*)jk, dim3(grid), dim3(RACE_THREADS), args, 0, s));
+  } else {
+    const size_t shm = sizeof(int64_t) * (size_t)nregs * RACE_THREADS;
+    if (shm > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_race_gen<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)shm));
+    k_race_gen<K><<<grid, RACE_THREADS, shm, s>>>(R, vol, sentinel, k0, v0, ctr + 0, ctr + 3);
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[1], s));
-  cub::DoubleBuffer<K> kb(k0, k1);
-  cub::DoubleBuffer<uint32_t> vb(v0, v1);
-  if (vol > 1) {
+  // order-preserving compaction of the accesses (sentinels out), then one
+  // scan that also detects order: keys that already arrive non-decreasing
+  // (a coalesced access pattern: offsets grow with the thread index) need
+  // no sort, since equal keys are then already adjacent in instance order,
+  // exactly as the stable sort would leave them
+  {
+    NotSentinel<K> pred{sentinel};
+    auto flags = thrust::make_transform_iterator((const K*)k0, pred);
     size_t tb = cub_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(wb + o_cub, tb, kb, vb, (int)vol, 0, bits, s));
+    CK(cub::DeviceSelect::If(wb + o_cub, tb, k0, k1, ctr + 5, (int)vol, pred, s));
+    tb = cub_bytes;
+    CK(cub::DeviceSelect::Flagged(wb + o_cub, tb, v0, flags, v1, ctr + 5, (int)vol, s));
   }
-  CK(cudaEventRecord(ctx->ev[2], s));
-  k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, kb.Current(), vb.Current(), ctr + 0, ctr + 1,
-                                               ctr + 2);
+  k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, k1, v1, ctr + 5, ctr + 1, ctr + 2, ctr + 4);
   CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->ev[3], s));
-  unsigned long long h[4];
+  unsigned long long h[6];
   CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const unsigned long long n = h[5];
+  cub::DoubleBuffer<K> kb(k1, k0);
+  cub::DoubleBuffer<uint32_t> vb(v1, v0);
+  out->sorted = h[4] == 0;
+  CK(cudaEventRecord(ctx->ev[2], s));
+  if (h[4]) {
+    unsigned long long reset[2] = {0ull, ~0ull};
+    CK(cudaMemcpyAsync(ctr + 1, reset, sizeof(reset), cudaMemcpyHostToDevice, s));
+    if (n > 1) {
+      size_t tb = cub_bytes;
+      CK(cub::DeviceRadixSort::SortPairs(wb + o_cub, tb, kb, vb, (int)n, 0, bits, s));
+    }
+    CK(cudaEventRecord(ctx->ev[2], s));
+    k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, kb.Current(), vb.Current(), ctr + 5, ctr + 1,
+                                                 ctr + 2, nullptr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaEventRecord(ctx->ev[3], s));
   CK(cudaStreamSynchronize(s));
   out->tuples = h[0];
   out->instances = h[3];
@@ -244,7 +318,7 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   out->scan_ms = ms;
   // one tuple write at generation, one read + one write for a
   // single-pass-equivalent sort, one read in the conflict scan
-  out->hbm_bytes = 4ull * (unsigned long long)(sizeof(K) + sizeof(uint32_t)) * vol;
+  out->hbm_bytes = 4ull * (unsigned long long)(sizeof(K) + sizeof(uint32_t)) * h[0];
   return MK_OK;
 }
 
@@ -295,7 +369,9 @@ extern "C" int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_resu
   cudaStream_t s = ctx->stream;
   CK(cudaMemcpyAsync(d_lo, lo.data(), sizeof(int64_t) * hp.nvars, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(d_hi, hi.data(), sizeof(int64_t) * hp.nvars, cudaMemcpyHostToDevice, s));
-  unsigned long long init[4] = {0ull, 0ull, ~0ull, 0ull};
+  // [0] accesses, [1] conflicts, [2] first conflict, [3] evaluations,
+  // [4] unsorted flag, [5] compacted count
+  unsigned long long init[6] = {0ull, 0ull, ~0ull, 0ull, 0ull, 0ull};
   CK(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, s));
   RaceDev R;
   const mk_problem* dprobs = reinterpret_cast<const mk_problem*>(base + ds->o_probs);
@@ -339,6 +415,9 @@ extern "C" int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_resu
   if (kmax == ~0ull) return fail(ctx, MK_EINVAL, "race sweep key (offset x block) exceeds 64 bits");
   int bits = mk_bitlen((uint64_t)(kmax + 1));
   if (bits < 1) bits = 1;
-  if (bits <= 32) return race_run<uint32_t>(ctx, R, vol, bits, hp.nregs, out, base, ctr);
-  return race_run<unsigned long long>(ctx, R, vol, bits, hp.nregs, out, base, ctr);
+  if (bits <= 32)
+    return race_run<uint32_t>(ctx, R, vol, bits, hp.nregs, out, base, ctr, prog, lo.data(),
+                              hi.data());
+  return race_run<unsigned long long>(ctx, R, vol, bits, hp.nregs, out, base, ctr, prog, lo.data(),
+                                      hi.data());
 }

@@ -90,13 +90,14 @@ class RaceResult(ctypes.Structure):
                 ("sort_bits", ctypes.c_int32), ("idx_a", ctypes.c_uint64),
                 ("idx_b", ctypes.c_uint64), ("offset", ctypes.c_int64),
                 ("gen_ms", ctypes.c_double), ("sort_ms", ctypes.c_double),
-                ("scan_ms", ctypes.c_double), ("hbm_bytes", ctypes.c_uint64)]
+                ("scan_ms", ctypes.c_double), ("hbm_bytes", ctypes.c_uint64),
+                ("jit", ctypes.c_int32), ("sorted", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
-assert ctypes.sizeof(RaceProg) == 144 and ctypes.sizeof(RaceResult) == 88
+assert ctypes.sizeof(RaceProg) == 144 and ctypes.sizeof(RaceResult) == 96
 
 
 def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:

@@ -28,6 +28,6 @@ for T in [int(x) for x in sys.argv[1:]] or [4096, 65536, 131072]:
                 wall = time.perf_counter() - t0
             ms = got["gen_ms"] + got["sort_ms"] + got["scan_ms"]
             got.pop("pair", None)
-            print(json.dumps({"T": T, "instances": prog.instances, "wall_ms": wall * 1e3,
+            print(json.dumps({"T": T, "jit_env": os.environ.get("MK_NO_JIT"), "instances": prog.instances, "wall_ms": wall * 1e3,
                               "device_ms": ms, "algo_GBps": got["hbm_bytes"] / ms / 1e6, **got}),
                   flush=True)
