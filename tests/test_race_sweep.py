@@ -151,3 +151,29 @@ def test_device_sweep_full_launch_rms_norm():
             assert not got["has_race"] and got["conflicts"] == 0
             assert got["tuples"] in (T * 4, T * 1023 * 4)
     eng.close()
+
+
+@pytest.mark.gpu
+def test_device_sweep_paths_agree():
+    """The NVRTC-specialised generator and the interpreted one give the same
+    tuples, conflicts and first pair; both the in-order (no sort) and the
+    radix-sort paths are exercised."""
+    from paper_2603_24595_b200.native import Engine
+
+    eng = Engine(0)
+    keys = ("tuples", "conflicts", "has_race", "idx_a", "idx_b", "offset", "sorted")
+    seen_sorted = set()
+    for name, i, launch, expect, prog in _cases():
+        os.environ.pop("MK_NO_JIT", None)
+        a = eng.race_sweep(prog)
+        os.environ["MK_NO_JIT"] = "1"
+        try:
+            b = eng.race_sweep(prog)
+        finally:
+            os.environ.pop("MK_NO_JIT", None)
+        assert b["jit"] == 0
+        assert [a[k] for k in keys] == [b[k] for k in keys], (name, i)
+        if a["tuples"] > 1:
+            seen_sorted.add(bool(a["sorted"]))
+    assert seen_sorted == {True, False}
+    eng.close()
