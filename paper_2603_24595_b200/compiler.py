@@ -575,6 +575,7 @@ class _Presolve:
         self.agg_done: Set[Tuple] = set()
         self._canon_memo: Dict[Tuple, Node] = {}
         self.cuts: Set[Node] = set()
+        self._lin_memo = _Lin(self.widths)
 
     # symbols of an IR node (memo-free; atoms are small)
     @staticmethod
@@ -696,7 +697,9 @@ class _Presolve:
                 return
 
     def _pass(self) -> bool:
-        lin = _Lin(self.widths)
+        # linear forms are pure in the node (widths only grow: new lattice
+        # symbols), so one memo serves every pass of this presolve
+        lin = self._lin_memo
         ivl0 = _Ivl(self.bounds)
         # 1. normalise, split conjunctions, drop truths
         new_atoms: List[Node] = []
@@ -1454,6 +1457,12 @@ def _components(assertions: Sequence[Node]) -> List[List[Node]]:
 def compile_query(assertions: Sequence[Node],
                   origin_of: Callable[[str], str]) -> CompiledQuery:
     """Compile one checker query (a list of IR assertions)."""
+    with ir.compile_scope():
+        return _compile_query(assertions, origin_of)
+
+
+def _compile_query(assertions: Sequence[Node],
+                   origin_of: Callable[[str], str]) -> CompiledQuery:
     widths: Dict[str, str] = {}
     for a in assertions:
         ir.symbols_of(a, widths)

@@ -157,10 +157,50 @@ def not_(a: Node) -> Node:
 
 # -- traversal -------------------------------------------------------------------
 
+class CompileScope:
+    """Memo tables shared by every simplify / symbols_of call inside one site
+    compilation (``with ir.compile_scope(): ...``).  Both functions are pure,
+    so sharing within a query is exact; the scope ends with the query, so
+    nothing is reused across queries or calls."""
+
+    _active: Optional["CompileScope"] = None
+
+    def __init__(self) -> None:
+        self.simplify: Dict[Node, Node] = {}
+        self.symbols: Dict[Node, Tuple[Tuple[str, str], ...]] = {}
+        self.extra: Dict[Tuple, object] = {}     # other pure per-node helpers
+
+    def __enter__(self) -> "CompileScope":
+        self._prev = CompileScope._active
+        CompileScope._active = self
+        return self
+
+    def __exit__(self, *exc) -> None:
+        CompileScope._active = self._prev
+
+
+def compile_scope() -> CompileScope:
+    return CompileScope()
+
+
 def symbols_of(e: Node, out: Optional[Dict[str, str]] = None) -> Dict[str, str]:
     """name -> width, first-occurrence order (sym/expr.py:390-402)."""
     if out is None:
         out = {}
+    scope = CompileScope._active
+    if scope is not None:
+        got = scope.symbols.get(e)
+        if got is None:
+            got = tuple(_symbols_walk(e, {}).items())
+            scope.symbols[e] = got
+        for n, w in got:
+            if n not in out:
+                out[n] = w
+        return out
+    return _symbols_walk(e, out)
+
+
+def _symbols_walk(e: Node, out: Dict[str, str]) -> Dict[str, str]:
     stack = [e]
     # iterative pre-order keeping left-to-right first occurrence
     while stack:
@@ -466,7 +506,8 @@ def _simplify_node(e: Node) -> Node:
 
 
 def simplify(e: Node) -> Node:
-    memo: Dict[Node, Node] = {}
+    scope = CompileScope._active
+    memo: Dict[Node, Node] = scope.simplify if scope is not None else {}
 
     def go(n: Node) -> Node:
         got = memo.get(n)

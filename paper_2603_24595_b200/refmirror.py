@@ -353,6 +353,18 @@ def _negate(e: Node) -> Node:
 
 
 def _find_int_ite(e: Node) -> Optional[Node]:
+    scope = ir.CompileScope._active
+    if scope is None:
+        return _find_int_ite_walk(e)
+    key = ("int_ite", e)
+    if key in scope.extra:
+        return scope.extra[key]
+    got = _find_int_ite_walk(e)
+    scope.extra[key] = got
+    return got
+
+
+def _find_int_ite_walk(e: Node) -> Optional[Node]:
     if e[0] == "i" and e[4] != "bool":
         return e
     for c in ir.children(e):
