@@ -101,6 +101,10 @@ typedef struct mk_problem {
  * in (-2^61, 2^61): the engine evaluates the problem in exact 64-bit
  * arithmetic instead of saturating 128-bit arithmetic. */
 #define MK_PF_NARROW 1
+/* mk_problem.flags: any model will do (a feasibility check, e.g. branch
+ * screening): the search stops at the first model instead of proving the
+ * lexicographic optimum. */
+#define MK_PF_ANY 2
 
 /* Linear rows used for bound contraction inside a box:
  *   sum_k coef_k * x_var_k + c0  (rel 0: <= 0, rel 1: == 0) */

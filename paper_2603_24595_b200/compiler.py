@@ -85,6 +85,7 @@ class Problem:
     rows: List[Tuple[int, int, List[Tuple[int, int]]]] = field(default_factory=list)
     ops_per_point: int = 0         # instructions evaluated per instance
     narrow: bool = False           # exact in 64-bit arithmetic (narrow_proof)
+    any_model: bool = False        # feasibility only: stop at the first model
 
     @property
     def nvars(self) -> int:

@@ -204,6 +204,7 @@ __device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, con
   {
     unsigned long long kmin = *((volatile unsigned long long*)&I->key);
     if (kmin == ~0ull) return false;  // nothing offered yet
+    if (p.flags & MK_PF_ANY) return true;  // feasibility only: one model decides
     unsigned long long k = lex_key<V>(D, p, corner);
     if (k > kmin) return true;        // a strictly better model was offered
   }
@@ -236,8 +237,11 @@ __device__ void inc_offer(const DevSet& D, int pid, const mk_problem& p, const V
     unsigned long long k = lex_key<V>(D, p, x);
     unsigned long long old = atomicMin(&I->key, k);
     if (k > old) return;
+    // feasibility only: the first offer records the model (inc_dominates
+    // prunes everything once a key exists)
+    if ((p.flags & MK_PF_ANY) && old != ~0ull) return;
   }
-  if (inc_dominates<V>(D, pid, p, x)) return;
+  if (!(p.flags & MK_PF_ANY) && inc_dominates<V>(D, pid, p, x)) return;
   unsigned ns = 32;
   while (atomicCAS(&I->lock, 0, 1) != 0) {
     __nanosleep(ns);

@@ -64,6 +64,8 @@ class GpuDetectors:
     device: int = 0
     checker: Optional[SiteChecker] = None
     _cache: Dict[Tuple[str, ...], QueryResult] = field(default_factory=dict)
+    _screen_cache: Dict[Tuple[str, ...], str] = field(default_factory=dict)
+    screen_fallbacks: int = 0
 
     def __post_init__(self) -> None:
         if self.options is None:
@@ -255,13 +257,41 @@ class GpuDetectors:
         self._emit("InvalidDeref", line, col, text, addr.offset_bytes, res, state, key)
 
 
-def install(device: int = 0, checker: Optional[SiteChecker] = None):
+    # -- branch screening (engine/executor.py:489-492), SURVEY.md 8(f) row 1 --
+
+    SCREEN_BUDGET_S = 0.05
+
+    def screen(self, path, cond) -> str:
+        """sat | unsat | unknown for path + cond, as the executor's
+        ``_screen``: feasibility only (no canonical witness), render-keyed
+        cache like ``Solver.check`` (solver/interface.py:54-60).  The engine
+        gets a short budget; a query it cannot finish in time (interval
+        branch-and-prune is weak on some unsat cores the reference's LP
+        relaxation refutes at once) goes to the reference's own solver, so
+        the exploration, and with it every finding, is the reference's."""
+        E = self._E
+        assertions = list(path) + [cond]
+        key = ("screen",) + tuple(E.render(a) for a in assertions)
+        got = self._screen_cache.get(key)
+        if got is None:
+            res = self.checker.feasible([ir.from_ref(a) for a in assertions],
+                                        self.table.origin_of, max_seconds=self.SCREEN_BUDGET_S)
+            got = res.status
+            if got == "unknown" and res.reason == "budget":
+                got = self.solver.check(assertions).status
+                self.screen_fallbacks += 1
+            self._screen_cache[key] = got
+        return got
+
+
+def install(device: int = 0, checker: Optional[SiteChecker] = None, screening: bool = False):
     """Swap the checking stage of the reference executor for the B200 engine
-    (engine/executor.py:33 resolves ``Detectors`` at construction time).
-    Returns the previous class so callers can restore it."""
+    (engine/executor.py:33 resolves ``Detectors`` at construction time); with
+    ``screening`` the executor's branch screening (engine/executor.py:489-492)
+    also runs on the engine.  Returns what ``uninstall`` needs to restore."""
     import minikernel.engine.executor as X
 
-    prev = X.Detectors
+    prev = (X.Detectors, X.Executor._screen)
 
     class _Bound(GpuDetectors):
         def __init__(self, solver, table, kernel, options=None):
@@ -269,10 +299,23 @@ def install(device: int = 0, checker: Optional[SiteChecker] = None):
 
     _Bound.__name__ = "GpuDetectors"
     X.Detectors = _Bound
+    if screening:
+        orig = prev[1]
+
+        def _screen(self, state, cond):
+            det = getattr(self, "detectors", None)
+            if isinstance(det, GpuDetectors):
+                return det.screen(state.path, cond)
+            return orig(self, state, cond)
+
+        X.Executor._screen = _screen
     return prev
 
 
 def uninstall(prev) -> None:
     import minikernel.engine.executor as X
 
-    X.Detectors = prev
+    if isinstance(prev, tuple):
+        X.Detectors, X.Executor._screen = prev
+    else:
+        X.Detectors = prev

@@ -177,3 +177,29 @@ class SiteChecker:
 
     def check(self, assertions: Sequence[ir.Node], origin_of: Callable[[str], str]) -> QueryResult:
         return self.check_queries([(assertions, origin_of)])[0]
+
+    def feasible(self, assertions: Sequence[ir.Node], origin_of: Callable[[str], str],
+                 max_seconds: Optional[float] = None) -> QueryResult:
+        """Verdict only (sat / unsat / unknown), the reference's
+        ``Solver.check(...).status`` (solver/interface.py:49-86): the engine
+        stops at the first model (MK_PF_ANY) instead of the canonical one.
+        ``reason`` is "budget" when the device search ran out of time (the
+        query itself is decidable), else the compiler's give-up reason."""
+        t0 = time.perf_counter()
+        compiled = self.compile([(assertions, origin_of)])
+        self.stats.compile_s += time.perf_counter() - t0
+        cq = compiled[0][0]
+        if cq is not None:
+            for p in cq.problems:
+                p.any_model = True
+        saved = dict(self.limits)
+        if max_seconds is not None:
+            self.limits["max_seconds"] = max_seconds
+        try:
+            res = self.decide(compiled)[0]
+        finally:
+            self.limits = saved
+        if res.status == "unknown" and cq is not None and res.reason is None \
+                and not any(g.status == "unknown" for g in cq.groups):
+            res.reason = "budget"
+        return res

@@ -19,6 +19,7 @@ DEFAULT_LIB = os.path.join(HERE, LIB_NAME)
 
 MK_UNSAT, MK_SAT, MK_UNKNOWN = 0, 1, 2
 MK_PF_NARROW = 1
+MK_PF_ANY = 2
 STATUS_NAME = {MK_UNSAT: "unsat", MK_SAT: "sat", MK_UNKNOWN: "unknown"}
 
 EXPORTS = ("mk_abi_version", "mk_device_count", "mk_ctx_create", "mk_ctx_destroy",
@@ -180,7 +181,8 @@ class PackedSet:
                 if mx:
                     m |= 1 << k
             rec["maxmask"] = m
-            rec["flags"] = MK_PF_NARROW if getattr(p, "narrow", False) else 0
+            rec["flags"] = (MK_PF_NARROW if getattr(p, "narrow", False) else 0) | \
+                (MK_PF_ANY if getattr(p, "any_model", False) else 0)
             lo.extend(p.lo)
             hi.extend(p.hi)
             insns.extend(p.insns)

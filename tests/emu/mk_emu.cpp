@@ -70,6 +70,7 @@ void solve_problem(const mk_problem_set* set, int pid, int K, long long leaf_vol
       pend = 1;
       break;
     }
+    if (has && (p.flags & MK_PF_ANY)) break;  // feasibility only: one model decides
     EBox<V> b = stack.back();
     stack.pop_back();
     st.boxes++;

@@ -12,10 +12,10 @@ HAVE_REF = add_reference()
 EMU = os.path.join(ROOT, "tests", "emu", "libmk_emu.so")
 
 
-def _run(name, checker):
+def _run(name, checker, screening=False):
     from paper_2603_24595_b200.detectors import install, uninstall
 
-    prev = install(checker=checker)
+    prev = install(checker=checker, screening=screening)
     try:
         return analyze_workload(name)
     finally:
@@ -23,13 +23,14 @@ def _run(name, checker):
 
 
 @pytest.mark.skipif(not HAVE_REF, reason="reference front end not available")
+@pytest.mark.parametrize("screening", [False, True])
 @pytest.mark.parametrize("name", ["racy", "rms_norm", "fused_add_rms_norm"])
-def test_dropin_emulated(name):
+def test_dropin_emulated(name, screening):
     from paper_2603_24595_b200.engine import SiteChecker
 
     chk = SiteChecker(lib_path=EMU)
     try:
-        doc = _run(name, chk)
+        doc = _run(name, chk, screening)
     finally:
         chk.close()
     assert doc["findings"] == expected_findings(load(name))
@@ -38,13 +39,16 @@ def test_dropin_emulated(name):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not HAVE_REF, reason="reference front end not available")
+@pytest.mark.parametrize("screening", [False, True])
 @pytest.mark.parametrize("name", workloads())
-def test_dropin_gpu(name):
+def test_dropin_gpu(name, screening):
+    """Findings with the checking stage on the B200, and with the executor's
+    branch screening (engine/executor.py:489-492) on it as well."""
     from paper_2603_24595_b200.engine import SiteChecker
 
     chk = SiteChecker(device=0)
     try:
-        doc = _run(name, chk)
+        doc = _run(name, chk, screening)
     finally:
         chk.close()
     assert doc["findings"] == expected_findings(load(name))
