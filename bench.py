@@ -241,6 +241,40 @@ CORPUS = ["rotary_embedding", "rotary_llama2_7b", "rotary_mistral_7b", "rotary_l
           "rotary_qwen2_7b", "rotary_llama2_13b", "rotary_mixtral_8x7b", "rotary_gemma_7b"]
 
 
+def _analyze_line(chk, args, doc):
+    """BASELINE metric part 2, time-to-verdict per kernel x model: the
+    reference's own analyze() (parser, symbolic DFS, checking) on the
+    workload's kernel port and context, once with the B200 checking stage and
+    branch screening installed (GpuDetectors) and once unmodified; wall time
+    of each and whether the findings are the reference's."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from refpath import add_reference, analyze_workload
+    from goldens import expected_findings
+
+    if not add_reference():
+        return {"unavailable": "reference front end not installed under baseline/_ref"}
+    from paper_2603_24595_b200.detectors import install, uninstall
+
+    times = []
+    for _ in range(3):
+        prev = install(checker=chk, screening=True)
+        t0 = time.perf_counter()
+        try:
+            got = analyze_workload(args.workload)
+        finally:
+            uninstall(prev)
+        times.append(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    ref = analyze_workload(args.workload)
+    ref_s = time.perf_counter() - t0
+    return {"workload": args.workload, "b200_ms": 1e3 * min(times), "reference_ms": 1e3 * ref_s,
+            "speedup": ref_s / min(times),
+            "findings_equal_reference": got["findings"] == expected_findings(doc),
+            "reference_findings_equal_golden": ref["findings"] == doc["findings"],
+            "what": "analyze() wall time: reference front end (parser, DFS) + B200 checking "
+                    "stage and branch screening vs the unmodified reference, one core"}
+
+
 def _heavy_line(chk, args, int_peak, sm_mhz, sms):
     """The search kernels at scale: BASELINE configs[2] (paged attention,
     Mistral-7B), whose step is ~4e8 boxes, timed resident like the headline
@@ -437,6 +471,7 @@ def run_b200(args):
         ops = "bytecode instructions executed (no ncu calibration committed)"
 
     k2 = _race_sweep_line(chk, args, peaks, src) if rank == 0 and args.race_tokens > 0 else None
+    analyze = _analyze_line(chk, args, doc) if rank == 0 and world == 1 and args.analyze else None
     heavy = (_heavy_line(chk, args, int_peak, sm_mhz, sms)
              if rank == 0 and world == 1 and args.heavy and args.heavy != args.workload else None)
 
@@ -494,6 +529,7 @@ def run_b200(args):
                                         f"(clock sampled; peaks file: {src})"},
             "cpu_baseline": cpu,
             "k2_race_sweep": k2,
+            "time_to_verdict": analyze,
             "k1_heavy": heavy,
             "clocks": clk,
             "gpu_launches": launches,
@@ -514,6 +550,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-analyze", dest="analyze", action="store_false",
+                    help="skip the end-to-end analyze() time-to-verdict line")
     ap.add_argument("--heavy", default="paged_attention_v1",
                     help="workload of the k1_heavy line ('' to skip)")
     ap.add_argument("--race-tokens", type=int, default=262144,

@@ -172,6 +172,26 @@ def _lin_add(a: LinForm, b: LinForm, sign: int = 1) -> LinForm:
     return out, a[1] + sign * b[1]
 
 
+def _proportional(a: LinForm, b: LinForm) -> Optional[int]:
+    """k when a == k * b exactly (integer k, b non-constant), else None."""
+    terms_b, c_b = b
+    if not terms_b or set(a[0]) != set(terms_b):
+        return None
+    k = None
+    for t, cb in terms_b.items():
+        ca = a[0][t]
+        if ca % cb:
+            return None
+        q = ca // cb
+        if k is None:
+            k = q
+        elif q != k:
+            return None
+    if a[1] != k * c_b:
+        return None
+    return k
+
+
 def _lin_scale(a: LinForm, f: int) -> LinForm:
     if f == 0:
         return {}, 0
@@ -253,6 +273,14 @@ class _Lin:
                     return {}, ir.apply_binop(op, la[1], lb[1])
                 except ir.EvalError:
                     pass
+            if op in ("div", "mod", "emod") and lb[0]:
+                # k*B / B = k, k*B mod B = 0: exact wherever B != 0, and every
+                # symbolic divisor of a component carries the side atom
+                # B != 0 (compile_query; solver/linear.py:184-259), so no
+                # model is gained or lost
+                k = _proportional(la, lb)
+                if k is not None:
+                    return ({}, k) if op == "div" else ({}, 0)
             if op in ("div", "mod", "emod") and not lb[0] and lb[1] != 0:
                 c = lb[1]
                 if op == "emod":

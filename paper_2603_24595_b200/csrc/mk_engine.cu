@@ -302,21 +302,31 @@ enum { ACT_DONE = 0, ACT_LEAF = 1, ACT_SPLIT = 2 };
 
 struct Act {
   int kind;
-  int sv;  // split symbol
-  int m;   // number of children
+  int sv;   // split symbol
+  int m;    // pieces of sv
+  int sv2;  // second split symbol of a product split, -1 for none
+  int m2;   // pieces of sv2 (children: m * m2)
 };
+
+constexpr int MAX_CHILDREN = 32;  // product splits: at most one child per lane
 
 // lo/hi: the box (contracted in place).  Prunes, accepts the best corner of an
 // all-true box, hands small boxes to enumeration, or chooses a split.
+// `wide`: the unit's stack is too shallow to keep every lane busy: a split
+// whose symbol has fewer than K values also splits a second undecided symbol
+// (a product split of up to MAX_CHILDREN children), trading a little pruning
+// granularity for lanes that would otherwise idle
 template <typename V, int CAPV, int CAPR, int SH = 0>
 __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo, V* hi, int K,
-                           long long leaf_volume, LaneStats& st) {
+                           long long leaf_volume, LaneStats& st, bool wide = false) {
   const int nv = p.nvars;
   const MkProb P = view(D, pid);
   Act a;
   a.kind = ACT_DONE;
   a.sv = -1;
   a.m = 0;
+  a.sv2 = -1;
+  a.m2 = 1;
   V c[CAPV];
   st.boxes++;
   mk_corner(lo, hi, nv, p.maxmask, c);
@@ -362,6 +372,19 @@ __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo,
   a.kind = ACT_SPLIT;
   a.sv = sv;
   a.m = size < (U)K ? (int)size : K;
+  if (wide && a.m < K) {
+    const int sv2 = mk_pick_split(lo, hi, nv, v.und_mask & ~(1ull << sv),
+                                  *((volatile int*)&D.inc[pid].has) != 0);
+    if (sv2 >= 0) {
+      const int cap = MAX_CHILDREN / a.m;
+      U size2 = (U)(hi[sv2] - lo[sv2]) + 1;
+      const int m2 = size2 < (U)cap ? (int)size2 : cap;
+      if (m2 >= 2) {
+        a.sv2 = sv2;
+        a.m2 = m2;
+      }
+    }
+  }
   return a;
 }
 
@@ -602,7 +625,8 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
   while (top > 0) {
     long long room = A.cap - top;
     long long n = top < A.width ? top : A.width;
-    long long fit = room / (K - 1);
+    const bool wide = A.width > 1 && top < 2 * A.width;
+    long long fit = room / ((wide ? MAX_CHILDREN : K) - 1);
     if (fit < n) n = fit;
     if (n < 1 && A.dive) return TASK_DONE;
     if (n < 1) {
@@ -631,9 +655,9 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
     a.sv = -1;
     if (lane < n) {
       load_box<V, V>(box_at(stack, A.box_bytes, (size_t)(base + lane)), nv, D.stride, lo, hi);
-      a = process_box<V, CAPV, CAPR, SH>(D, pid, p, lo, hi, K, A.leaf_volume, st);
+      a = process_box<V, CAPV, CAPR, SH>(D, pid, p, lo, hi, K, A.leaf_volume, st, wide);
     }
-    const int nch = a.kind == ACT_SPLIT ? a.m : 0;
+    const int nch = a.kind == ACT_SPLIT ? a.m * a.m2 : 0;
     int incl = nch;
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(FULL, incl, o);
@@ -643,7 +667,7 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
     const int coff = incl - nch;
     const unsigned leafmask = __ballot_sync(FULL, a.kind == ACT_LEAF);
     __syncwarp();  // every popped box has been read: its slot may be reused
-    if (nch) {
+    if (nch && a.sv2 < 0) {
       bool mx = (p.maxmask >> a.sv) & 1;
       for (int j = 0; j < a.m; ++j) {
         V plo, phi;
@@ -651,6 +675,25 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
         write_box<V, V>(box_at(stack, A.box_bytes, (size_t)(base + coff + j)), pid, lo, hi, nv,
                         D.stride, a.sv, plo, phi);
       }
+    } else if (nch) {
+      // product split: children in lexicographic order of (earlier symbol's
+      // piece, later symbol's piece), best on top of the stack
+      const int s1 = a.sv < a.sv2 ? a.sv : a.sv2, s2 = a.sv < a.sv2 ? a.sv2 : a.sv;
+      const int m1 = s1 == a.sv ? a.m : a.m2, m2 = s1 == a.sv ? a.m2 : a.m;
+      const bool mx1 = (p.maxmask >> s1) & 1, mx2 = (p.maxmask >> s2) & 1;
+      const V lo1 = lo[s1], hi1 = hi[s1], lo2 = lo[s2], hi2 = hi[s2];
+      for (int j = 0; j < nch; ++j) {
+        const int t = nch - 1 - j;  // worst first
+        V plo, phi;
+        mk_piece(lo1, hi1, m1, t / m2, mx1, &plo, &phi);
+        lo[s1] = plo;
+        hi[s1] = phi;
+        mk_piece(lo2, hi2, m2, t % m2, mx2, &plo, &phi);
+        write_box<V, V>(box_at(stack, A.box_bytes, (size_t)(base + coff + j)), pid, lo, hi, nv,
+                        D.stride, s2, plo, phi);
+      }
+      lo[s1] = lo1;
+      hi[s1] = hi1;
     }
     if (a.kind == ACT_LEAF) {
       const int loff = __popc(leafmask & ((1u << lane) - 1u));

@@ -14,4 +14,4 @@ for d in (4096,):
             eng.solve_packed(sets[n], {"max_seconds": 600.0, "max_rounds": -d})
             ms.append(eng.last_stats["device_ms"])
         st = eng.last_stats
-        print('dive', d, n, 'ms', ' '.join('%.2f' % x for x in ms), 'boxes', st['boxes'], 'steps', st['steps'], flush=True)
+        print('dive', d, n, 'ms', ' '.join('%.2f' % x for x in ms), 'boxes', st['boxes'], 'steps', st['steps'], 'rounds', st['rounds'], 'launches', st['launches'], 'leaves', st['leaves'], 'points', st['points'], flush=True)
