@@ -57,9 +57,45 @@ def main(argv) -> None:
             s["z3_model"] = {k: int(x) for k, x in v.model.items()}
         print(f"{name} site {i} line {s['line']}:{s['col']} {s['site']}: reference "
               f"{s['verdict']} ({s['reason']}), z3 {v.status} in {s['z3_s']}s", flush=True)
+    doc["findings_pinned"] = pinned_findings(name, doc)
     with open(path, "w") as fh:
         json.dump(doc, fh, separators=(",", ":"))
         fh.write("\n")
+
+
+def pinned_findings(name, doc):
+    """The reference's own analyze() (front end, Detectors, merge_findings,
+    engine/report.py:109-140) with every timed-out query answered by its z3
+    verdict instead: the findings the reference reports when its solver is
+    given the time it needs.  Stored as ``findings_pinned``."""
+    from refbridge import to_ref
+    from minikernel.solver import interface as SI
+    from minikernel.solver.query import Verdict
+    from minikernel.sym import expr as E
+
+    from paper_2603_24595_b200 import ir
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from refpath import analyze_workload
+
+    pins = {}
+    for s in doc["sites"]:
+        if s.get("reason") == "solver timeout" and s.get("z3_verdict") == "unsat":
+            key = tuple(E.render(to_ref(ir.from_json(a), E)) for a in s["query"])
+            pins[key] = Verdict.unsat()
+    orig = SI.Solver.check
+
+    def check(self, assertions, bounds=None):
+        got = pins.get(tuple(E.render(a) for a in assertions))
+        if got is not None and not bounds:
+            return got
+        return orig(self, assertions, bounds)
+
+    SI.Solver.check = check
+    try:
+        return analyze_workload(name)["findings"]
+    finally:
+        SI.Solver.check = orig
 
 
 if __name__ == "__main__":
