@@ -116,6 +116,7 @@ class CompiledQuery:
     problems: List[Problem]
     defs: Dict[str, Node]          # eliminated symbols -> expr over free symbols
     free_default: Dict[str, int]   # symbols absent from every atom
+    compile_s: float = 0.0         # host time spent compiling this query
 
     def assemble(self, results: Sequence[Tuple[str, Optional[List[int]]]]):
         """Combine per-problem device results into the reference verdict.

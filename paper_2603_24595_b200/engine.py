@@ -42,8 +42,11 @@ class BatchStats:
 
 def _compile_one(item) -> Tuple[Optional[CompiledQuery], Optional[str]]:
     assertions, origin_of = item
+    t0 = time.perf_counter()
     try:
-        return compile_query(assertions, origin_of), None
+        cq = compile_query(assertions, origin_of)
+        cq.compile_s = time.perf_counter() - t0
+        return cq, None
     except CompileError as exc:
         return None, str(exc)
 

@@ -22,7 +22,9 @@ for name in sys.argv[1:]:
         res = chk.decide(comp, packed, offs)
         t3 = time.perf_counter()
         st = chk.engine.last_stats
-    print(name, "compile %.1f ms, pack %.1f ms, decide %.1f ms (device %.1f ms, call %.1f ms)" % (
-        1e3 * (t1 - t0), 1e3 * (t2 - t1), 1e3 * (t3 - t2), st["device_ms"], 1e3 * st["seconds"]),
-        flush=True)
+    per = sorted((c.compile_s for c, _ in comp if c is not None), reverse=True)
+    print(name, "compile %.1f ms (sum %.1f ms, max %.2f ms, n %d, workers %d), pack %.1f ms, "
+          "decide %.1f ms (device %.1f ms, call %.1f ms)" % (
+              1e3 * (t1 - t0), 1e3 * sum(per), 1e3 * per[0], len(per), chk.compile_workers,
+              1e3 * (t2 - t1), 1e3 * (t3 - t2), st["device_ms"], 1e3 * st["seconds"]), flush=True)
 chk.close()
