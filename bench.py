@@ -308,13 +308,20 @@ def _heavy_line(chk, args, int_peak, sm_mhz, sms):
                          "ncu_issue_active_pct": cal.get("k_search_issue_active_pct")}}
 
 
-def _race_sweep_line(chk, args, peaks, src):
-    """K2 (sort-based race sweep, include/mk_b200.h mk_race_sweep) on config
-    1's output store (rms_norm, Llama-2-7B hidden 4096: out[blockIdx.x *
-    hidden + idx]) replayed at a full concrete launch: every (thread, loop
-    iteration) access of the launch is generated, radix-sorted by byte
-    offset in HBM and scanned for conflicts.  HBM roofline: algorithmic bytes
-    = 4 x tuple bytes per access / device time."""
+def _race_sweep_line(chk, args, peaks, src, int_peak):
+    """K2 (race sweep, include/mk_b200.h mk_race_sweep) on config 1's output
+    store (rms_norm, Llama-2-7B hidden 4096: out[blockIdx.x * hidden + idx])
+    replayed at a full concrete launch: every (thread, loop iteration) access
+    of the launch is evaluated and checked for conflicts.
+
+    The sweep that runs is the fused ordered pass (the store is coalesced, so
+    its keys arrive in order and the stable sort is the identity): one
+    NVRTC-specialised kernel, no tuples in HBM, integer-issue bound; its
+    roofline is thread instructions per instance (ncu, profiles/
+    ncu_k2_summary.json) x instances / kernel time over 148 SMs x 128 lanes x
+    clock.  ``sort_path`` runs the same tuples through the HBM radix-sort path
+    (MK_RACE_FORCE_SORT): algorithmic bytes = 4 x tuple bytes per access
+     / device time, against the HBM peak."""
     from paper_2603_24595_b200 import race
 
     doc, queries = _load_workload("rms_norm")
@@ -324,22 +331,54 @@ def _race_sweep_line(chk, args, peaks, src):
     progs = [race.race_program(a, o, launch) for s, (a, o) in zip(doc["sites"], queries)
              if s["site"] == "store_site" and s["line"] == 20]
     prog = max(progs, key=lambda p: p.instances)
-    for _ in range(2):
-        chk.engine.race_sweep(prog)
-    runs = [chk.engine.race_sweep(prog) for _ in range(3)]
+
+    def timed(env):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            for _ in range(2):
+                chk.engine.race_sweep(prog)
+            return [chk.engine.race_sweep(prog) for _ in range(3)]
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+
+    runs = timed({})
     ms = sum(r["gen_ms"] + r["sort_ms"] + r["scan_ms"] for r in runs) / len(runs)
     r = runs[-1]
+    cal = _calibration("k2")
+    per_inst = cal.get("thread_inst_per_instance")
+    kms = sum(x["gen_ms"] for x in runs) / len(runs)
+    achieved = prog.instances * per_inst / (kms / 1e3) / 1e9 if per_inst and kms > 0 else None
+    sruns = timed({"MK_RACE_FORCE_SORT": "1"})
+    sms_ = sum(x["gen_ms"] + x["sort_ms"] + x["scan_ms"] for x in sruns) / len(sruns)
+    sr = sruns[-1]
     hbm_peak = peaks.get("hbm_gbs", 6650.0) if isinstance(peaks, dict) else 6650.0
-    achieved = r["hbm_bytes"] / (ms / 1e3) / 1e9
+    s_ach = sr["hbm_bytes"] / (sms_ / 1e3) / 1e9
     return {"workload": f"rms_norm output store (BASELINE configs[0]) at num_tokens={T}: "
                         f"{T} blocks x 1023 threads x 4 iterations",
             "accesses": r["tuples"], "instances": prog.instances, "has_race": bool(r["has_race"]),
-            "ms": ms, "gen_ms": r["gen_ms"], "sort_ms": r["sort_ms"], "scan_ms": r["scan_ms"],
-            "sort_key_bits": r["sort_bits"],
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None,
-                         "algorithmic_bytes": r["hbm_bytes"],
-                         "peak_source": f"peaks file: {src}"}}
+            "path": "fused ordered pass" if r["fused"] else ("in-order scan" if r["sorted"] else "radix sort"),
+            "ms": ms, "instances_per_s": prog.instances / (ms / 1e3),
+            "gen_ms": r["gen_ms"], "sort_ms": r["sort_ms"], "scan_ms": r["scan_ms"],
+            "roofline": {"bound": "int32-issue",
+                         "achieved": achieved, "peak": int_peak / 1e9, "unit": "Gop/s",
+                         "frac": achieved * 1e9 / int_peak if achieved else None,
+                         "traffic": r["hbm_bytes"],
+                         "kernel": "mk_race_fused_jit (NVRTC, sm_100a)",
+                         "ops": f"SASS thread instructions per instance: {per_inst} "
+                                "(ncu, profiles/ncu_k2_summary.json)"},
+            "sort_path": {"ms": sms_, "gen_ms": sr["gen_ms"], "sort_ms": sr["sort_ms"],
+                          "scan_ms": sr["scan_ms"], "sort_key_bits": sr["sort_bits"],
+                          "same_result": (sr["tuples"], sr["conflicts"], sr["has_race"]) ==
+                                         (r["tuples"], r["conflicts"], r["has_race"]),
+                          "roofline": {"bound": "hbm", "achieved": s_ach, "peak": hbm_peak,
+                                       "unit": "GB/s", "frac": s_ach / hbm_peak, "traffic": None,
+                                       "algorithmic_bytes": sr["hbm_bytes"],
+                                       "peak_source": f"peaks file: {src}"}}}
 
 
 def run_b200(args):
@@ -470,7 +509,7 @@ def run_b200(args):
         achieved = insns / (search_ms / 1e3) if search_ms > 0 else 0.0
         ops = "bytecode instructions executed (no ncu calibration committed)"
 
-    k2 = _race_sweep_line(chk, args, peaks, src) if rank == 0 and args.race_tokens > 0 else None
+    k2 = _race_sweep_line(chk, args, peaks, src, int_peak) if rank == 0 and args.race_tokens > 0 else None
     analyze = _analyze_line(chk, args, doc) if rank == 0 and world == 1 and args.analyze else None
     heavy = (_heavy_line(chk, args, int_peak, sm_mhz, sms)
              if rank == 0 and world == 1 and args.heavy and args.heavy != args.workload else None)

@@ -226,6 +226,8 @@ typedef struct mk_race_result {
   uint64_t hbm_bytes;   /* algorithmic HBM bytes moved by the three phases */
   int32_t jit;          /* 1: generator specialised at run time (NVRTC), 0: interpreted */
   int32_t sorted;       /* 1: the keys arrived in order and the sort was skipped */
+  int32_t fused;        /* 1: decided by the fused ordered pass (no tuples in HBM) */
+  int32_t reserved;
 } mk_race_result;
 
 int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out);

@@ -66,72 +66,85 @@ inline std::string lit(int64_t v) {
   return o.str();
 }
 
-// CUDA source of the race generator for one program (host copy of the
+// CUDA source of the race generators for one program (host copy of the
 // problem).  Key type, sentinel, offset origin and block radix are baked in.
+// Two kernels share one generated access function:
+//   mk_race_gen_jit    dense (key, index) tuples for the sort path;
+//   mk_race_fused_jit  the ordered fast path: every warp walks a contiguous
+//                      instance range (lane l takes base + l + 32 j), compares
+//                      each access with the previous one in instance order in
+//                      registers (ballot + shuffles), and leaves only a
+//                      per-warp summary (first / last access) for the chunk
+//                      boundary pass.  Nothing per instance touches HBM.
+// rbits[r] (optional) is 32 when register r provably stays inside int32 on
+// the whole instance box (interval evaluation of the root box, inclusion
+// isotonic): such registers are 32-bit locals and an operation whose
+// operands and result are all 32-bit runs on the 32-bit pipe; everything
+// else is exact int64 (the narrow class).
 inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
                                    const mk_i128* consts, int n_outer, int off_reg, int shared,
                                    const int id_var[6], const int64_t* lo, const int64_t* hi,
-                                   bool key64) {
+                                   bool key64, const int* rbits = nullptr, int64_t off_lo = 0,
+                                   unsigned long long nblocks = 1) {
   const int nv = p.nvars, nc = p.nconst, nr = p.nregs;
   std::ostringstream s;
   const char* KT = key64 ? "unsigned long long" : "unsigned int";
-  s << "typedef long long i64;\n"
+  auto b32 = [&](int r) { return rbits && rbits[r] == 32; };
+  auto ty = [&](int r) { return b32(r) ? "int" : "i64"; };
+  s << "typedef long long i64;\ntypedef unsigned long long u64;\n"
        "__device__ __forceinline__ i64 mk_emod(i64 a, i64 b) { i64 m = b < 0 ? -b : b; i64 r = a % m;"
+       " return r < 0 ? r + m : r; }\n"
+       "__device__ __forceinline__ int mk_emod32(int a, int b) { int m = b < 0 ? -b : b; int r = a % m;"
        " return r < 0 ? r + m : r; }\n"
        "__device__ __forceinline__ i64 mk_shl(i64 a, i64 k) { return k >= 62 ? 0 :"
        " (i64)((unsigned long long)a << k); }\n"
        "__device__ __forceinline__ i64 mk_shr(i64 a, i64 k) { return a >> (k > 63 ? 63 : k); }\n";
-  s << "extern \"C\" __global__ void __launch_bounds__(256) mk_race_gen_jit(unsigned long long vol, "
-    << KT << " sentinel, " << KT
-    << "* keys, unsigned int* vals, unsigned long long* count, unsigned long long* evaluated,"
-       " i64 off_lo, unsigned long long nblocks) {\n";
   for (int i = 0; i < nv; ++i) {
-    s << "  const i64 lo" << i << " = " << lit(lo[i]) << ", sp" << i << " = " << lit(hi[i] - lo[i] + 1)
-      << ";\n";
+    s << "#define lo" << i << " " << lit(lo[i]) << "\n#define sp" << i << " " << lit(hi[i] - lo[i] + 1)
+      << "\n";
   }
-  s << "  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;\n"
-       "  unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;\n";
-  // odometer digits of idx and of the stride over the leading vars
-  for (int i = 0; i < n_outer; ++i) s << "  i64 d" << i << ", t" << i << ";\n";
-  s << "  { unsigned long long a = idx, b = stride;\n";
-  for (int i = n_outer - 1; i >= 0; --i) {
-    s << "    d" << i << " = (i64)(a % (unsigned long long)sp" << i << "); a /= (unsigned long long)sp" << i
-      << "; t" << i << " = (i64)(b % (unsigned long long)sp" << i << "); b /= (unsigned long long)sp"
-      << i << ";\n";
-  }
-  s << "  }\n  unsigned long long done = 0, models = 0;\n"
-       "  for (; idx < vol; idx += stride) {\n";
-  for (int i = 0; i < n_outer; ++i) s << "    const i64 x" << i << " = lo" << i << " + d" << i << ";\n";
-  s << "    " << KT << " key = sentinel;\n";
-  // existential (trailing) vars: first model wins
+  // the access function: leading values in, (hit, key) out
+  s << "__device__ __forceinline__ bool mk_acc(";
+  for (int i = 0; i < n_outer; ++i) s << (i ? ", " : "") << "const " << ty(i) << " x" << i;
+  s << (n_outer ? ", " : "") << "u64& done, " << KT << "& key) {\n";
   unsigned long long inner = 1;
   for (int i = n_outer; i < nv; ++i) inner *= (unsigned long long)(hi[i] - lo[i] + 1);
-  s << "    for (unsigned long long j = 0; j < " << inner << "ULL; ++j) {\n";
+  // with no existential vars every instance is one evaluation: the callers
+  // count them per warp instead of per instance
+  const bool count_inner = inner > 1;
+  s << "  for (unsigned long long j = 0; j < " << inner << "ULL; ++j) {\n";
   if (nv > n_outer) {
-    s << "      unsigned long long jj = j;\n";
+    s << "    unsigned long long jj = j;\n";
     for (int i = nv - 1; i >= n_outer; --i)
-      s << "      const i64 x" << i << " = lo" << i << " + (i64)(jj % (unsigned long long)sp" << i
-        << "); jj /= (unsigned long long)sp" << i << ";\n";
+      s << "    const " << ty(i) << " x" << i << " = (" << ty(i) << ")(lo" << i
+        << " + (i64)(jj % (unsigned long long)sp" << i << ")); jj /= (unsigned long long)sp" << i << ";\n";
   }
-  s << "      ++done;\n      bool hit = false;\n      i64 off = 0;\n      do {\n";
-  for (int r = 0; r < nr; ++r) s << "        i64 v" << r << " = 0; bool e" << r << " = false;\n";
-  for (int i = 0; i < nv; ++i) s << "        v" << i << " = x" << i << ";\n";
-  for (int i = 0; i < nc; ++i) s << "        v" << (nv + i) << " = " << lit((int64_t)consts[i].lo) << ";\n";
+  s << (count_inner ? "    ++done;\n" : "") << "    bool hit = false;\n    i64 off = 0;\n    do {\n";
+  for (int r = nv + nc; r < nr; ++r) s << "      " << ty(r) << " v" << r << " = 0; bool e" << r << " = false;\n";
+  for (int i = 0; i < nv; ++i) s << "      const " << ty(i) << " v" << i << " = x" << i << "; const bool e" << i << " = false;\n";
+  for (int i = 0; i < nc; ++i)
+    s << "      const " << ty(nv + i) << " v" << (nv + i) << " = " << lit((int64_t)consts[i].lo)
+      << "; const bool e" << (nv + i) << " = false;\n";
   for (int k = 0; k < p.ninsn; ++k) {
     const mk_insn in = insns[k];
     const int a = in.a, b = in.b, c = in.c, d = in.dst;
     if (in.op == MK_OP_ATOM) {
-      s << "        if (e" << a << " || !v" << a << ") break;\n";
+      s << "      if (e" << a << " || !v" << a << ") break;\n";
       continue;
     }
-    s << "        { const i64 A = v" << a << ", B = v" << b << "; const bool EA = e" << a << ", EB = e"
-      << b << "; i64 R = 0; bool E = false; (void)A; (void)B; (void)EA; (void)EB;\n          ";
+    // 32-bit arithmetic only when operands and result are all int32-bounded
+    // (then the mathematical result is the int32 result); shifts stay int64
+    const bool arith32 = b32(a) && b32(b) && b32(d) && in.op != MK_OP_SHL && in.op != MK_OP_SHR;
+    const char* OT = arith32 ? "int" : "i64";
+    s << "      { const " << OT << " A = (" << OT << ")v" << a << ", B = (" << OT << ")v" << b
+      << "; const bool EA = e" << a << ", EB = e" << b << "; " << OT
+      << " R = 0; bool E = false; (void)A; (void)B; (void)EA; (void)EB;\n        ";
     switch (in.op) {
       case MK_OP_AND: s << "if (EA) E = true; else if (!A) R = 0; else { R = B ? 1 : 0; E = EB; }"; break;
       case MK_OP_OR: s << "if (EA) E = true; else if (A) R = 1; else { R = B ? 1 : 0; E = EB; }"; break;
       case MK_OP_NOT: s << "E = EA; R = A ? 0 : 1;"; break;
       case MK_OP_ITE:
-        s << "const i64 C = v" << c << "; const bool EC = e" << c
+        s << "const " << OT << " C = (" << OT << ")v" << c << "; const bool EC = e" << c
           << "; if (EA) E = true; else if (A) { R = B; E = EB; } else { R = C; E = EC; }";
         break;
       default: {
@@ -144,7 +157,9 @@ inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
           case MK_OP_SHR: s << "R = mk_shr(A, B);"; break;
           case MK_OP_DIV: s << "if (B == 0) E = true; else R = A / B;"; break;
           case MK_OP_MOD: s << "if (B == 0) E = true; else R = A % B;"; break;
-          case MK_OP_EMOD: s << "if (B == 0) E = true; else R = mk_emod(A, B);"; break;
+          case MK_OP_EMOD:
+            s << "if (B == 0) E = true; else R = " << (arith32 ? "mk_emod32" : "mk_emod") << "(A, B);";
+            break;
           case MK_OP_EQ: s << "R = A == B;"; break;
           case MK_OP_NE: s << "R = A != B;"; break;
           case MK_OP_LT: s << "R = A < B;"; break;
@@ -156,89 +171,238 @@ inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
         s << " }";
       }
     }
-    s << "\n          v" << d << " = R; e" << d << " = E; }\n";
+    s << "\n        v" << d << " = (" << ty(d) << ")R; e" << d << " = E; }\n";
   }
-  s << "        hit = true; off = v" << off_reg << ";\n      } while (0);\n";
-  s << "      if (hit) {\n        unsigned long long bk = 0;\n";
+  s << "      hit = true; off = (i64)v" << off_reg << ";\n    } while (0);\n";
+  s << "    if (hit) {\n      u64 bk = 0;\n";
   if (shared) {
     for (int ax = 2; ax >= 0; --ax) {
       const int v = id_var[ax];
       if (v < 0) continue;
-      s << "        bk = bk * (unsigned long long)sp" << v << " + (unsigned long long)(x" << v << " - lo" << v
-        << ");\n";
+      s << "      bk = bk * (u64)sp" << v << " + (u64)((i64)x" << v << " - lo" << v << ");\n";
     }
   }
-  s << "        key = (" << KT << ")((unsigned long long)(off - off_lo) * nblocks + bk);\n"
-       "        ++models;\n        break;\n      }\n    }\n"
-       "    keys[idx] = key;\n    vals[idx] = (unsigned int)idx;\n";
-  // odometer step
-  s << "    { i64 carry = 0, dd;\n";
-  for (int i = n_outer - 1; i >= 0; --i) {
-    s << "      dd = d" << i << " + t" << i << " + carry; carry = dd >= sp" << i << " ? 1 : 0; d" << i
-      << " = dd - (carry ? sp" << i << " : 0);\n";
+  s << "      key = (" << KT << ")((u64)(off - (" << lit(off_lo) << ")) * " << nblocks
+    << "ull + bk);\n      (void)done;\n      return true;\n    }\n"
+       "  }\n  (void)done;\n  return false;\n}\n";
+  // the identity of an instance as one integer (< 2^31: mixed radix of its
+  // thread-identity digits; shared memory: thread ids only, the key holds the
+  // block)
+  s << "__device__ __forceinline__ unsigned mk_idk(";
+  for (int i = 0; i < n_outer; ++i) s << (i ? ", " : "") << "const int d" << i;
+  s << ") {\n  unsigned k = 0;\n";
+  for (int ax = shared ? 3 : 0; ax < 6; ++ax) {
+    const int v = id_var[ax];
+    if (v < 0) continue;
+    s << "  k = k * (unsigned)sp" << v << " + (unsigned)d" << v << ";\n";
   }
-  s << "    }\n  }\n"
+  s << "  return k;\n}\n";
+  s << "__device__ __noinline__ unsigned mk_idk_of(unsigned long long a) {\n";
+  for (int i = n_outer - 1; i >= 0; --i)
+    s << "  const int d" << i << " = (int)(a % (unsigned long long)sp" << i << "); a /= (unsigned long long)sp" << i
+      << ";\n";
+  s << "  return mk_idk(";
+  for (int i = 0; i < n_outer; ++i) s << (i ? ", " : "") << "d" << i;
+  s << ");\n}\n";
+  // leading digits are int32 (the instance box holds < 2^31 instances)
+  auto call_args = [&]() {
+    std::ostringstream a;
+    for (int i = 0; i < n_outer; ++i) a << "(" << ty(i) << ")(lo" << i << " + d" << i << "), ";
+    return a.str();
+  };
+  auto id_args = [&]() {
+    std::ostringstream a;
+    for (int i = 0; i < n_outer; ++i) a << (i ? ", " : "") << "d" << i;
+    return a.str();
+  };
+  // mixed-radix odometer over the leading digits; the step's digits are
+  // literals (32 for the fused pass), or computed from the grid stride
+  auto odometer_init = [&](const char* start, const char* step, unsigned long long cstep) {
+    std::ostringstream o;
+    for (int i = 0; i < n_outer; ++i) o << "  int d" << i << ", t" << i << ";\n";
+    o << "  { unsigned long long a = " << start << ", b = " << step << "; (void)b;\n";
+    unsigned long long c = cstep;
+    for (int i = n_outer - 1; i >= 0; --i) {
+      const unsigned long long sp = (unsigned long long)(hi[i] - lo[i] + 1);
+      o << "    d" << i << " = (int)(a % (unsigned long long)sp" << i << "); a /= (unsigned long long)sp" << i << "; ";
+      if (cstep) {
+        o << "t" << i << " = " << (c % sp) << ";\n";
+        c /= sp;
+      } else {
+        o << "t" << i << " = (int)(b % (unsigned long long)sp" << i << "); b /= (unsigned long long)sp" << i << ";\n";
+      }
+    }
+    o << "  }\n";
+    return o.str();
+  };
+  auto odometer_step = [&]() {
+    std::ostringstream o;
+    o << "    { int c = 0;\n";
+    for (int i = n_outer - 1; i >= 0; --i) {
+      o << "      d" << i << " += t" << i << " + c; c = d" << i << " >= (int)sp" << i << "; if (c) d" << i
+        << " -= (int)sp" << i << ";\n";
+    }
+    o << "      (void)c;\n    }\n";
+    return o.str();
+  };
+  // dense generator (sort path)
+  s << "extern \"C\" __global__ void __launch_bounds__(256) mk_race_gen_jit(unsigned long long vol, "
+    << KT << " sentinel, " << KT
+    << "* keys, unsigned int* vals, unsigned long long* count, unsigned long long* evaluated,"
+       " i64 off_lo, unsigned long long nblocks) {\n"
+       "  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;\n"
+       "  unsigned long long idx = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;\n"
+    << odometer_init("idx", "stride", 0)
+    << "  unsigned long long done = 0, models = 0;\n"
+       "  for (; idx < vol; idx += stride) {\n"
+       "    " << KT << " key = sentinel;\n"
+       << (count_inner ? "" : "    ++done;\n") <<
+       "    if (mk_acc(" << call_args() << "done, key)) ++models; else key = sentinel;\n"
+       "    keys[idx] = key;\n    vals[idx] = (unsigned int)idx;\n"
+    << odometer_step()
+    << "  }\n"
        "  for (int o = 16; o > 0; o >>= 1) { done += __shfl_down_sync(0xffffffffu, done, o);"
        " models += __shfl_down_sync(0xffffffffu, models, o); }\n"
        "  if ((threadIdx.x & 31) == 0) { if (done) atomicAdd(evaluated, done);"
        " if (models) atomicAdd(count, models); }\n}\n";
+  // fused ordered scan (fast path).  rec: MK_RACE_REC u64 per warp = have,
+  // first key, first identity, first index, last key, last identity, last
+  // index, best conflict (idx_b << 32 | idx_a), its key, pad.
+  // ctr: [0] accesses [1] conflicts [2] min (idx_b << 32 | idx_a) [3]
+  // evaluations [4] out-of-order flag.  Lane l holds instance b0 + l, so
+  // instance indices need no shuffle; the hot loop moves only keys (ballot +
+  // two shuffles), identities are computed only on the rare equal-key steps.
+  s << "extern \"C\" __global__ void __launch_bounds__(256) mk_race_fused_jit(unsigned long long vol, "
+       "unsigned long long chunk, i64 off_lo_unused, unsigned long long nblocks_unused, u64* rec, u64* ctr) {\n"
+       "  const unsigned lane = threadIdx.x & 31;\n"
+       "  const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;\n"
+       "  const unsigned long long base = warp * chunk;\n"
+       "  unsigned long long end = base + chunk; if (end > vol) end = vol;\n"
+       "  const unsigned uend = (unsigned)(end < base ? base : end);\n"
+       "  const unsigned lt = (1u << lane) - 1u;\n"
+    << odometer_init("(base + lane)", "32ull", 32)
+    << "  u64 done = 0, conf = 0, best = ~0ull, bkey = 0;\n"
+       "  unsigned models = 0;\n"
+       "  bool have = false, down = false;\n"
+       "  " << KT << " ck = 0, fk = 0;\n"
+       "  unsigned cx = 0, fx = 0;\n"
+       "  for (unsigned b0 = (unsigned)base; b0 < uend; b0 += 32) {\n"
+       "    const unsigned idx = b0 + lane;\n"
+       "    " << KT << " key = 0;\n"
+       "    bool valid = false;\n"
+       "    if (idx < uend) valid = mk_acc(" << call_args() << "done, key);\n"
+       "    const unsigned mask = __ballot_sync(0xffffffffu, valid);\n"
+       "    if (mask) {\n"
+       "      const unsigned lower = mask & lt;\n"
+       "      const int src = lower ? 31 - __clz(lower) : 0;\n"
+       "      " << KT << " pk = __shfl_sync(0xffffffffu, key, src);\n"
+       "      if (!lower) pk = ck;\n"
+       "      const bool ph = lower ? true : have;\n"
+       "      models += valid ? 1u : 0u;\n"
+       "      if (valid && ph && key < pk) down = true;\n"
+       "      const bool eq = valid && ph && key == pk;\n"
+       "      if (__any_sync(0xffffffffu, eq)) {\n"
+       "        const unsigned idk = valid ? mk_idk(" << id_args() << ") : 0u;\n"
+       "        unsigned pi = __shfl_sync(0xffffffffu, idk, src);\n"
+       "        const unsigned px = lower ? b0 + (unsigned)src : cx;\n"
+       "        if (eq && !lower) pi = mk_idk_of(cx);\n"
+       "        if (eq && idk != pi) { ++conf; const u64 c = ((u64)idx << 32) | px;"
+       " if (c < best) { best = c; bkey = (u64)key; } }\n"
+       "      }\n"
+       "      if (!have) { const int fl = __ffs(mask) - 1; fk = __shfl_sync(0xffffffffu, key, fl);"
+       " fx = b0 + (unsigned)fl; }\n"
+       "      const int hl = 31 - __clz(mask);\n"
+       "      ck = __shfl_sync(0xffffffffu, key, hl); cx = b0 + (unsigned)hl;\n"
+       "      have = true;\n"
+       "    }\n"
+    << odometer_step()
+    << "  }\n"
+    << (count_inner ? "" : "  done = (lane == 0 && uend > (unsigned)base) ? (u64)(uend - (unsigned)base) : 0ull;\n")
+    << "  u64 m64 = models;\n"
+       "  for (int o = 16; o > 0; o >>= 1) {\n"
+       "    done += __shfl_down_sync(0xffffffffu, done, o);\n"
+       "    m64 += __shfl_down_sync(0xffffffffu, m64, o);\n"
+       "    conf += __shfl_down_sync(0xffffffffu, conf, o);\n"
+       "    const u64 b2 = __shfl_down_sync(0xffffffffu, best, o), k2 = __shfl_down_sync(0xffffffffu, bkey, o);\n"
+       "    if (b2 < best) { best = b2; bkey = k2; }\n"
+       "  }\n"
+       "  const bool anydown = __any_sync(0xffffffffu, down);\n"
+       "  if (lane == 0) {\n"
+       "    u64* r = rec + warp * 10;\n"
+       "    r[0] = have ? 1ull : 0ull; r[1] = (u64)fk; r[2] = have ? mk_idk_of(fx) : 0u; r[3] = fx;\n"
+       "    r[4] = (u64)ck; r[5] = have ? mk_idk_of(cx) : 0u; r[6] = cx;\n"
+       "    r[7] = best; r[8] = bkey;\n"
+       "    if (m64) atomicAdd(ctr + 0, m64);\n"
+       "    if (conf) atomicAdd(ctr + 1, conf);\n"
+       "    if (best != ~0ull) atomicMin(ctr + 2, best);\n"
+       "    if (done) atomicAdd(ctr + 3, done);\n"
+       "    if (anydown) atomicOr(ctr + 4, 1ull);\n"
+       "  }\n}\n";
   return s.str();
 }
 
 struct Cache {
   std::map<std::string, cudaKernel_t> kernels;
+  std::map<std::string, cudaLibrary_t> libs;
   std::string last_error;
 };
 
 // compile (or fetch) the kernel for `src`; nullptr on failure
-inline cudaKernel_t get_kernel(Cache& cache, const std::string& src, int device) {
-  auto it = cache.kernels.find(src);
+inline cudaKernel_t get_kernel(Cache& cache, const std::string& src, int device,
+                               const char* name = "mk_race_gen_jit") {
+  const std::string ckey = std::string(name) + "\n" + src;
+  auto it = cache.kernels.find(ckey);
   if (it != cache.kernels.end()) return it->second;
-  Nvrtc& N = nvrtc();
-  if (!N.load()) {
-    cache.last_error = "nvrtc unavailable";
-    return nullptr;
-  }
-  int major = 0, minor = 0;
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
-  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
-  const std::string arch = "--gpu-architecture=sm_" + std::to_string(major * 10 + minor) +
-                           (major >= 9 ? "a" : "");
-  nvrtcProgram prog;
-  if (N.create(&prog, src.c_str(), "mk_race_gen_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
-    cache.last_error = "nvrtcCreateProgram failed";
-    return nullptr;
-  }
-  const char* opts[] = {arch.c_str(), "--std=c++17", "-default-device"};
-  nvrtcResult rc = N.compile(prog, 3, opts);
-  if (rc != NVRTC_SUCCESS) {
+  auto lt = cache.libs.find(src);
+  cudaLibrary_t lib = nullptr;
+  if (lt != cache.libs.end()) lib = lt->second;
+  if (!lib) {
+    Nvrtc& N = nvrtc();
+    if (!N.load()) {
+      cache.last_error = "nvrtc unavailable";
+      return nullptr;
+    }
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    const std::string arch = "--gpu-architecture=sm_" + std::to_string(major * 10 + minor) +
+                             (major >= 9 ? "a" : "");
+    nvrtcProgram prog;
+    if (N.create(&prog, src.c_str(), "mk_race_gen_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+      cache.last_error = "nvrtcCreateProgram failed";
+      return nullptr;
+    }
+    const char* opts[] = {arch.c_str(), "--std=c++17", "-default-device"};
+    nvrtcResult rc = N.compile(prog, 3, opts);
+    if (rc != NVRTC_SUCCESS) {
+      size_t n = 0;
+      N.log_size(prog, &n);
+      std::string log(n, '\0');
+      if (n) N.log(prog, &log[0]);
+      cache.last_error = "nvrtc: " + log;
+      N.destroy(&prog);
+      return nullptr;
+    }
     size_t n = 0;
-    N.log_size(prog, &n);
-    std::string log(n, '\0');
-    if (n) N.log(prog, &log[0]);
-    cache.last_error = "nvrtc: " + log;
+    N.cubin_size(prog, &n);
+    std::string bin(n, '\0');
+    N.cubin(prog, &bin[0]);
     N.destroy(&prog);
-    return nullptr;
-  }
-  size_t n = 0;
-  N.cubin_size(prog, &n);
-  std::string bin(n, '\0');
-  N.cubin(prog, &bin[0]);
-  N.destroy(&prog);
-  cudaLibrary_t lib;
-  if (cudaLibraryLoadData(&lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) !=
-      cudaSuccess) {
-    cache.last_error = "cudaLibraryLoadData failed";
-    cudaGetLastError();
-    return nullptr;
+    if (cudaLibraryLoadData(&lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) !=
+        cudaSuccess) {
+      cache.last_error = "cudaLibraryLoadData failed";
+      cudaGetLastError();
+      return nullptr;
+    }
+    cache.libs[src] = lib;
   }
   cudaKernel_t k;
-  if (cudaLibraryGetKernel(&k, lib, "mk_race_gen_jit") != cudaSuccess) {
+  if (cudaLibraryGetKernel(&k, lib, name) != cudaSuccess) {
     cache.last_error = "cudaLibraryGetKernel failed";
     cudaGetLastError();
     return nullptr;
   }
-  cache.kernels[src] = k;
+  cache.kernels[ckey] = k;
   return k;
 }
 

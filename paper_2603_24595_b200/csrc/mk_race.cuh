@@ -176,6 +176,69 @@ __global__ void __launch_bounds__(RACE_THREADS) k_race_scan(RaceDev R, const K* 
   if (unsorted && __any_sync(FULL, down) && (threadIdx.x & 31) == 0) atomicOr(unsorted, 1ull);
 }
 
+// Chunk boundaries of the fused ordered pass (mk_jit.cuh mk_race_fused_jit):
+// every warp left its first and last access in instance order; one CTA
+// pairs each non-empty chunk's first access with the previous non-empty
+// chunk's last one (exclusive max-scan of "last non-empty chunk"), adds the
+// boundary conflicts and out-of-order flag, then resolves the key of the
+// globally first conflict.  ctr: [1] conflicts [2] min (idx_b << 32 | idx_a)
+// [4] out-of-order flag [5] key of the first conflict.
+constexpr int MK_RACE_REC = 10;
+
+struct MaxInt {
+  __device__ int operator()(int a, int b) const { return a > b ? a : b; }
+};
+
+__global__ void __launch_bounds__(1024) k_race_bound(const unsigned long long* rec, int W,
+                                                     unsigned long long* ctr) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  const int per = (W + 1023) / 1024;
+  const int b = threadIdx.x * per;
+  const int e = min(W, b + per);
+  int last = -1;
+  for (int w = b; w < e; ++w)
+    if (rec[(size_t)w * MK_RACE_REC]) last = w;
+  int prev = -1;
+  Scan(tmp).ExclusiveScan(last, prev, -1, MaxInt());
+  const int prev0 = prev;
+  unsigned long long conf = 0, best = ~0ull;
+  bool down = false;
+  for (int w = b; w < e; ++w) {
+    const unsigned long long* r = rec + (size_t)w * MK_RACE_REC;
+    if (!r[0]) continue;
+    if (prev >= 0) {
+      const unsigned long long* q = rec + (size_t)prev * MK_RACE_REC;
+      if (r[1] < q[4]) {
+        down = true;
+      } else if (r[1] == q[4] && r[2] != q[5]) {
+        ++conf;
+        const unsigned long long c = (r[3] << 32) | q[6];
+        if (c < best) best = c;
+      }
+    }
+    prev = w;
+  }
+  if (conf) atomicAdd(ctr + 1, conf);
+  if (best != ~0ull) atomicMin(ctr + 2, best);
+  if (down) atomicOr(ctr + 4, 1ull);
+  __threadfence();
+  __syncthreads();
+  const unsigned long long g = *(volatile unsigned long long*)(ctr + 2);
+  if (g == ~0ull) return;
+  prev = prev0;
+  for (int w = b; w < e; ++w) {
+    const unsigned long long* r = rec + (size_t)w * MK_RACE_REC;
+    if (!r[0]) continue;
+    if (r[7] == g) ctr[5] = r[8];
+    if (prev >= 0) {
+      const unsigned long long* q = rec + (size_t)prev * MK_RACE_REC;
+      if (r[1] == q[4] && r[2] != q[5] && ((r[3] << 32) | q[6]) == g) ctr[5] = r[1];
+    }
+    prev = w;
+  }
+}
+
 template <typename K>
 struct NotSentinel {
   K sentinel;
@@ -227,14 +290,112 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   const K sentinel = (K)(bits >= (int)(8 * sizeof(K)) ? ~(K)0 : (((K)1 << bits) - 1));
   // specialised generator (NVRTC) when available, else the interpreter
   cudaKernel_t jk = nullptr;
+  std::string src;
   if (!getenv("MK_NO_JIT")) {
     const mk_problem_set& set = prog->set;
-    const std::string src = mkjit::race_gen_source(
+    // register widths: interval evaluation of the instance box on the host
+    // (the device's own interval semantics, mk_core.cuh); a register whose
+    // range stays inside int32 gets a 32-bit local
+    const mk_problem& hp = set.probs[0];
+    std::vector<int> rbits(hp.nregs, 64);
+    {
+      const MkProb HP = mk_prob_view(set.probs, 0, set.insns, set.consts, set.atom_regs,
+                                     set.atom_masks, set.rows, set.row_terms);
+      std::vector<MkIvT<i128>> Rg(MK_MAXR);
+      for (auto& r : Rg) {
+        r.lo = 1;
+        r.hi = 0;
+        r.fl = 0;
+      }
+      std::vector<i128> vl(hp.nvars), vh(hp.nvars);
+      for (int i = 0; i < hp.nvars; ++i) {
+        vl[i] = (i128)hlo[i];
+        vh[i] = (i128)hhi[i];
+      }
+      int64_t cnt = 0;
+      const MkBoxVerdict bv = mk_eval_box<i128>(HP, vl.data(), vh.data(), Rg.data(), &cnt);
+      if (!bv.any_false) {
+        for (int r = 0; r < hp.nregs; ++r) {
+          const MkIvT<i128>& g = Rg[r];
+          if ((g.fl & MK_FL_OK) && g.lo <= g.hi && g.lo >= (i128)INT32_MIN && g.hi <= (i128)INT32_MAX)
+            rbits[r] = 32;
+        }
+      }
+    }
+    src = mkjit::race_gen_source(
         set.probs[0], set.insns + set.probs[0].insn_off, set.consts + set.probs[0].const_off,
-        R.n_outer, prog->off_reg, prog->shared, prog->id_var, hlo, hhi, sizeof(K) == 8);
+        R.n_outer, prog->off_reg, prog->shared, prog->id_var, hlo, hhi, sizeof(K) == 8,
+        getenv("MK_JIT_WIDE") ? nullptr : rbits.data(), R.off_lo, R.nblocks);
+    if (const char* dump = getenv("MK_JIT_DUMP")) {
+      FILE* f = fopen(dump, "w");
+      if (f) {
+        fputs(src.c_str(), f);
+        fclose(f);
+      }
+    }
     jk = mkjit::get_kernel(ctx->jit, src, ctx->device);
   }
   out->jit = jk != nullptr;
+  // fast path: the fused ordered pass (no per-instance HBM traffic).  When
+  // the accesses arrive in non-decreasing key order in instance order (a
+  // coalesced store), the stable sort is the identity and the adjacent-pair
+  // scan of the sorted tuples is exactly what the pass computes in registers;
+  // otherwise its result is discarded and the sort path below runs.
+  if (jk && !getenv("MK_RACE_NO_FAST") && !getenv("MK_RACE_FORCE_SORT")) {
+    cudaKernel_t fk = mkjit::get_kernel(ctx->jit, src, ctx->device, "mk_race_fused_jit");
+    if (fk) {
+      const int fgrid = ctx->sms * 8;
+      const unsigned long long warps = (unsigned long long)fgrid * (RACE_THREADS / 32);
+      unsigned long long chunk = (vol + warps - 1) / warps;
+      chunk = (chunk + 31) / 32 * 32;
+      if (chunk < 32) chunk = 32;
+      const size_t rbytes = sizeof(unsigned long long) * MK_RACE_REC * warps;
+      int rc0 = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, rbytes);
+      if (rc0) return rc0;
+      unsigned long long* rec = static_cast<unsigned long long*>(ctx->d_work);
+      unsigned long long init[6] = {0ull, 0ull, ~0ull, 0ull, 0ull, 0ull};
+      CK(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, s));
+      CK(cudaEventRecord(ctx->ev[0], s));
+      unsigned long long a_vol = vol, a_chunk = chunk, a_nb = R.nblocks;
+      long long a_off = R.off_lo;
+      unsigned long long* a_rec = rec;
+      unsigned long long* a_ctr = ctr;
+      void* fargs[] = {&a_vol, &a_chunk, &a_off, &a_nb, &a_rec, &a_ctr};
+      CK(cudaLaunchKernel((const void*)fk, dim3(fgrid), dim3(RACE_THREADS), fargs, 0, s));
+      CK(cudaEventRecord(ctx->ev[1], s));
+      k_race_bound<<<1, 1024, 0, s>>>(rec, (int)warps, ctr);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(ctx->ev[2], s));
+      unsigned long long h[6];
+      CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
+      CK(cudaEventRecord(ctx->ev[3], s));
+      CK(cudaStreamSynchronize(s));
+      if (!h[4]) {
+        out->fused = 1;
+        out->sorted = 1;
+        out->tuples = h[0];
+        out->instances = h[3];
+        out->conflicts = h[1];
+        out->has_race = h[1] > 0;
+        out->sort_bits = bits;
+        if (out->has_race) {
+          out->idx_b = h[2] >> 32;
+          out->idx_a = h[2] & 0xffffffffull;
+          out->offset = (int64_t)(h[5] / R.nblocks) + R.off_lo;
+        }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+        out->gen_ms = ms;
+        cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]);
+        out->scan_ms = ms;
+        out->sort_ms = 0.0;
+        out->hbm_bytes = 2ull * rbytes;   // per-warp records: written once, read once
+        return MK_OK;
+      }
+      // out of order: reset the counters for the sort path
+      CK(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    }
+  }
   CK(cudaEventRecord(ctx->ev[0], s));
   if (jk) {
     unsigned long long a_vol = vol, a_nb = R.nblocks;
@@ -255,27 +416,44 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   }
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[1], s));
-  // order-preserving compaction of the accesses (sentinels out), then one
-  // scan that also detects order: keys that already arrive non-decreasing
-  // (a coalesced access pattern: offsets grow with the thread index) need
-  // no sort, since equal keys are then already adjacent in instance order,
-  // exactly as the stable sort would leave them
-  {
+  // order-preserving compaction of the accesses (sentinels out; skipped when
+  // every instance is an access), then one scan that also detects order:
+  // keys that already arrive non-decreasing (a coalesced access pattern:
+  // offsets grow with the thread index) need no sort, since equal keys are
+  // then already adjacent in instance order, exactly as the stable sort would
+  // leave them.  MK_RACE_FORCE_SORT sorts regardless (measurement).
+  unsigned long long h[6];
+  CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  K* kc = k0;
+  K* ko = k1;
+  uint32_t* vc = v0;
+  uint32_t* vo = v1;
+  if (h[0] == vol) {
+    CK(cudaMemcpyAsync(ctr + 5, &vol, sizeof(vol), cudaMemcpyHostToDevice, s));
+  } else {
     NotSentinel<K> pred{sentinel};
     auto flags = thrust::make_transform_iterator((const K*)k0, pred);
     size_t tb = cub_bytes;
     CK(cub::DeviceSelect::If(wb + o_cub, tb, k0, k1, ctr + 5, (int)vol, pred, s));
     tb = cub_bytes;
     CK(cub::DeviceSelect::Flagged(wb + o_cub, tb, v0, flags, v1, ctr + 5, (int)vol, s));
+    kc = k1;
+    ko = k0;
+    vc = v1;
+    vo = v0;
   }
-  k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, k1, v1, ctr + 5, ctr + 1, ctr + 2, ctr + 4);
-  CK(cudaGetLastError());
-  unsigned long long h[6];
+  const bool force = getenv("MK_RACE_FORCE_SORT") != nullptr;
+  if (!force) {
+    k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, kc, vc, ctr + 5, ctr + 1, ctr + 2, ctr + 4);
+    CK(cudaGetLastError());
+  }
   CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  if (force) h[4] = 1;
   const unsigned long long n = h[5];
-  cub::DoubleBuffer<K> kb(k1, k0);
-  cub::DoubleBuffer<uint32_t> vb(v1, v0);
+  cub::DoubleBuffer<K> kb(kc, ko);
+  cub::DoubleBuffer<uint32_t> vb(vc, vo);
   out->sorted = h[4] == 0;
   CK(cudaEventRecord(ctx->ev[2], s));
   if (h[4]) {

@@ -92,13 +92,14 @@ class RaceResult(ctypes.Structure):
                 ("idx_b", ctypes.c_uint64), ("offset", ctypes.c_int64),
                 ("gen_ms", ctypes.c_double), ("sort_ms", ctypes.c_double),
                 ("scan_ms", ctypes.c_double), ("hbm_bytes", ctypes.c_uint64),
-                ("jit", ctypes.c_int32), ("sorted", ctypes.c_int32)]
+                ("jit", ctypes.c_int32), ("sorted", ctypes.c_int32),
+                ("fused", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
-assert ctypes.sizeof(RaceProg) == 144 and ctypes.sizeof(RaceResult) == 96
+assert ctypes.sizeof(RaceProg) == 144 and ctypes.sizeof(RaceResult) == 104
 
 
 def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:

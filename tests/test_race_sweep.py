@@ -155,25 +155,34 @@ def test_device_sweep_full_launch_rms_norm():
 
 @pytest.mark.gpu
 def test_device_sweep_paths_agree():
-    """The NVRTC-specialised generator and the interpreted one give the same
-    tuples, conflicts and first pair; both the in-order (no sort) and the
-    radix-sort paths are exercised."""
+    """The fused ordered pass (NVRTC-specialised, no tuples in HBM), the
+    specialised sort path and the interpreted sort path give the same tuples,
+    conflicts and first pair; the fused pass decides the in-order cases and
+    hands the out-of-order ones to the radix sort."""
     from paper_2603_24595_b200.native import Engine
 
     eng = Engine(0)
     keys = ("tuples", "conflicts", "has_race", "idx_a", "idx_b", "offset", "sorted")
-    seen_sorted = set()
+    seen_sorted, seen_fused_race = set(), False
     for name, i, launch, expect, prog in _cases():
-        os.environ.pop("MK_NO_JIT", None)
-        a = eng.race_sweep(prog)
-        os.environ["MK_NO_JIT"] = "1"
-        try:
-            b = eng.race_sweep(prog)
-        finally:
-            os.environ.pop("MK_NO_JIT", None)
-        assert b["jit"] == 0
-        assert [a[k] for k in keys] == [b[k] for k in keys], (name, i)
-        if a["tuples"] > 1:
-            seen_sorted.add(bool(a["sorted"]))
+        runs = []
+        for env in ({}, {"MK_RACE_NO_FAST": "1"}, {"MK_NO_JIT": "1"}):
+            for k in ("MK_NO_JIT", "MK_RACE_NO_FAST"):
+                os.environ.pop(k, None)
+            os.environ.update(env)
+            try:
+                runs.append(eng.race_sweep(prog))
+            finally:
+                for k in env:
+                    os.environ.pop(k, None)
+        fast, slow, interp = runs
+        assert interp["jit"] == 0 and interp["fused"] == 0 and slow["fused"] == 0
+        assert [fast[k] for k in keys] == [slow[k] for k in keys] == [interp[k] for k in keys], \
+            (name, i, fast, slow)
+        assert fast["fused"] == (1 if fast["sorted"] else 0)
+        if fast["tuples"] > 1:
+            seen_sorted.add(bool(fast["sorted"]))
+        seen_fused_race |= bool(fast["fused"] and fast["has_race"])
     assert seen_sorted == {True, False}
+    assert seen_fused_race
     eng.close()
