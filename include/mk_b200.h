@@ -232,6 +232,64 @@ typedef struct mk_race_result {
 
 int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out);
 
+/* ---------------------------------------------------------------------
+ * Access sweep (K2, oracle semantics): read-write and write-write races
+ * across instructions, with barrier epochs, over one concrete launch.
+ *
+ * The reference's symbolic checker only pairs a store with its own twin
+ * (engine/detectors.py:204-232).  Its specification's concrete oracle
+ * (absent from the reference) pairs ACCESSES: same region,
+ * overlapping bytes, different threads, at least one write, same barrier
+ * epoch for shared memory (any epoch for global).  This entry point is that
+ * rule, data-parallel, behind a non-parity flag of the host API: problem i
+ * of `set` is access i's path program over one thread's private symbols
+ * (atoms = path, register off_reg = byte offset); every instance of every
+ * access emits one tuple per granule it covers,
+ *   key = ((kbase + block * span + (offset - off_lo) / granule + j) << 1) | is_read,
+ *   val = (thread identity << 32) | dense tuple slot,
+ * the tuples are radix-sorted in HBM (writes first inside a granule) and a
+ * segmented scan finds, per granule, a write and an access by another
+ * thread.  Identity = the launch-wide thread number (shared: within the
+ * block, the key holds the block).  The host lays out kbase / span / off_lo
+ * so keys of different regions (and shared epochs) never collide.
+ */
+typedef struct mk_access_prog {
+  int32_t off_reg;       /* register holding the byte offset */
+  int32_t n_exist;       /* trailing existential vars (see mk_race_prog) */
+  int32_t id_var[6];     /* blockIdx.x,y,z, threadIdx.x,y,z var indices or -1 */
+  int64_t id_fixed[6];   /* their values when id_var == -1 */
+  int32_t write;         /* 1 store, 0 load */
+  int32_t shared;        /* 1: key includes the block (shared memory) */
+  int32_t granule;       /* bytes per tuple; offsets must be multiples */
+  int32_t tuples;        /* tuples per instance = access width / granule */
+  uint64_t kbase;        /* key origin of this access's region (and epoch) */
+  uint64_t span;         /* granules per block (shared) */
+  int64_t off_lo;        /* region origin, a multiple of granule */
+} mk_access_prog;
+
+typedef struct mk_access_input {
+  mk_problem_set set;    /* one narrow problem per access */
+  const mk_access_prog* progs;
+  int64_t grid[3];       /* gridDim.x,y,z of the launch */
+  int64_t block[3];      /* blockDim.x,y,z */
+  int32_t key_bits;      /* every sort key (granule << 1 | is_read) < 2^key_bits */
+  int32_t pad;
+} mk_access_input;
+
+typedef struct mk_access_result {
+  uint64_t instances;    /* instances enumerated over all accesses */
+  uint64_t tuples;       /* granule tuples of executed accesses */
+  uint64_t racy;         /* granules with a race */
+  int32_t has_race;
+  int32_t misaligned;    /* an offset was not a multiple of its granule:
+                            rerun with granule 1 (result otherwise void) */
+  uint64_t slot_a;       /* dense tuple slot of the first race's write */
+  uint64_t slot_b;       /* ... and of its partner (another thread) */
+  double gen_ms, sort_ms, scan_ms;
+} mk_access_result;
+
+int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access_result* out);
+
 #ifdef __cplusplus
 }
 #endif

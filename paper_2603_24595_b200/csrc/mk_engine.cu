@@ -1544,3 +1544,4 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
 }
 
 #include "mk_race.cuh"
+#include "mk_access.cuh"

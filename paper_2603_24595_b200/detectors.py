@@ -66,6 +66,10 @@ class GpuDetectors:
     _cache: Dict[Tuple[str, ...], QueryResult] = field(default_factory=dict)
     _screen_cache: Dict[Tuple[str, ...], str] = field(default_factory=dict)
     screen_fallbacks: int = 0
+    # non-parity: record every executed access for the oracle race replay
+    # (paper_2603_24595_b200.replay); off by default
+    record_accesses: bool = False
+    accesses: List[object] = field(default_factory=list)
 
     def __post_init__(self) -> None:
         if self.options is None:
@@ -168,6 +172,8 @@ class GpuDetectors:
         E = self._E
         if not self.enabled or not addr.known:
             return
+        if self.record_accesses:
+            self._record(state, addr, nbytes, line, col, text)
         key = ("OutOfBounds", line, col)
         if self._memo.get(key):
             return
@@ -206,9 +212,26 @@ class GpuDetectors:
 
     # -- DataRace (engine/detectors.py:204-273) -------------------------------------
 
+    def _record(self, state, addr, nbytes, line, col, text) -> None:
+        """An executed access (engine/executor.py:428-472) with its path
+        condition and barrier epoch (engine/state.py:142); the store that
+        follows turns it into a write (store_site)."""
+        from .replay import AccessRecord
+
+        region = addr.provenance
+        self.accesses.append(AccessRecord(
+            kind="read", line=line, col=col, text=text, region=region.rid,
+            shared=region.kind == "shared", width=int(nbytes),
+            offset=ir.from_ref(addr.offset_bytes), path=[ir.from_ref(a) for a in state.path],
+            epoch=int(getattr(state, "barrier_epoch", 0))))
+        self._last_access = (id(state), line, col, addr.offset_bytes)
+
     def store_site(self, state, region, addr, nbytes: int, line: int, col: int,
                    text: str) -> None:
         E = self._E
+        if self.record_accesses and self.enabled and self.accesses and \
+                getattr(self, "_last_access", None) == (id(state), line, col, addr.offset_bytes):
+            self.accesses[-1].kind = "write"
         if not self.enabled or state.thread is None:
             return
         key = ("DataRace", line, col)
@@ -284,18 +307,25 @@ class GpuDetectors:
         return got
 
 
-def install(device: int = 0, checker: Optional[SiteChecker] = None, screening: bool = False):
+def install(device: int = 0, checker: Optional[SiteChecker] = None, screening: bool = False,
+            recorders: Optional[list] = None):
     """Swap the checking stage of the reference executor for the B200 engine
     (engine/executor.py:33 resolves ``Detectors`` at construction time); with
     ``screening`` the executor's branch screening (engine/executor.py:489-492)
-    also runs on the engine.  Returns what ``uninstall`` needs to restore."""
+    also runs on the engine.  With ``recorders`` (a list) every constructed
+    detector also records the executed accesses for the oracle race replay
+    (paper_2603_24595_b200.replay) and is appended to it.  Returns what
+    ``uninstall`` needs to restore."""
     import minikernel.engine.executor as X
 
     prev = (X.Detectors, X.Executor._screen)
 
     class _Bound(GpuDetectors):
         def __init__(self, solver, table, kernel, options=None):
-            super().__init__(solver, table, kernel, options, device=device, checker=checker)
+            super().__init__(solver, table, kernel, options, device=device, checker=checker,
+                             record_accesses=recorders is not None)
+            if recorders is not None:
+                recorders.append(self)
 
     _Bound.__name__ = "GpuDetectors"
     X.Detectors = _Bound

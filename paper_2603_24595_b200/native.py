@@ -99,6 +99,32 @@ class RaceResult(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class AccessProg(ctypes.Structure):
+    _fields_ = [("off_reg", ctypes.c_int32), ("n_exist", ctypes.c_int32),
+                ("id_var", ctypes.c_int32 * 6), ("id_fixed", ctypes.c_int64 * 6),
+                ("write", ctypes.c_int32), ("shared", ctypes.c_int32),
+                ("granule", ctypes.c_int32), ("tuples", ctypes.c_int32),
+                ("kbase", ctypes.c_uint64), ("span", ctypes.c_uint64), ("off_lo", ctypes.c_int64)]
+
+
+class AccessInput(ctypes.Structure):
+    _fields_ = [("set", ProblemSet), ("progs", ctypes.c_void_p),
+                ("grid", ctypes.c_int64 * 3), ("block", ctypes.c_int64 * 3),
+                ("key_bits", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class AccessResult(ctypes.Structure):
+    _fields_ = [("instances", ctypes.c_uint64), ("tuples", ctypes.c_uint64),
+                ("racy", ctypes.c_uint64), ("has_race", ctypes.c_int32),
+                ("misaligned", ctypes.c_int32), ("slot_a", ctypes.c_uint64),
+                ("slot_b", ctypes.c_uint64), ("gen_ms", ctypes.c_double),
+                ("sort_ms", ctypes.c_double), ("scan_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+assert ctypes.sizeof(AccessProg) == 120 and ctypes.sizeof(AccessResult) == 72
 assert ctypes.sizeof(RaceProg) == 144 and ctypes.sizeof(RaceResult) == 104
 
 
@@ -119,6 +145,8 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
     lib.mk_set_free.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     lib.mk_race_sweep.argtypes = [ctypes.c_void_p, ctypes.POINTER(RaceProg),
                                   ctypes.POINTER(RaceResult)]
+    lib.mk_access_sweep.argtypes = [ctypes.c_void_p, ctypes.POINTER(AccessInput),
+                                    ctypes.POINTER(AccessResult)]
     return lib
 
 
@@ -309,6 +337,33 @@ class Engine:
         if res["has_race"]:
             res["pair"] = (prog.decode(res["idx_a"]), prog.decode(res["idx_b"]))
         return res
+
+    def access_sweep(self, problems, progs, grid, block, key_bits) -> dict:
+        """Oracle-semantics race sweep of several accesses at one launch
+        (paper_2603_24595_b200.replay -> mk_access_sweep).  ``progs`` is a
+        list of dicts with the mk_access_prog fields."""
+        packed = PackedSet(problems)
+        arr = (AccessProg * len(progs))()
+        for a, d in zip(arr, progs):
+            for k, v in d.items():
+                if k in ("id_var", "id_fixed"):
+                    for i, x in enumerate(v):
+                        getattr(a, k)[i] = x
+                else:
+                    setattr(a, k, v)
+        inp = AccessInput()
+        inp.set = packed.struct
+        inp.progs = ctypes.cast(arr, ctypes.c_void_p)
+        for i in range(3):
+            inp.grid[i] = int(grid[i])
+            inp.block[i] = int(block[i])
+        inp.key_bits = int(key_bits)
+        out = AccessResult()
+        rc = self.lib.mk_access_sweep(self.ctx, ctypes.byref(inp), ctypes.byref(out))
+        if rc != 0:
+            msg = self.lib.mk_last_error(self.ctx)
+            raise RuntimeError(f"mk_access_sweep failed ({rc}): {msg.decode() if msg else ''}")
+        return out.as_dict()
 
     # -- device-resident sets ------------------------------------------------------
 

@@ -211,6 +211,19 @@ def race_program(assertions: Sequence[ir.Node], origin_of: Callable[[str], str],
     (``launch`` must give a value to every non-private symbol; a finding's
     witness does)."""
     path, off, shared = split_race_query(assertions)
+    return path_program(path, off, shared, origin_of, launch, max_instances)
+
+
+def path_program(path: Sequence[ir.Node], off: ir.Node, shared: bool,
+                 origin_of: Callable[[str], str], launch: Mapping[str, int],
+                 max_instances: int = MAX_INSTANCES,
+                 id_extents: Optional[Mapping[str, int]] = None) -> RaceProgram:
+    """One thread's access program (path atoms, byte offset) at a concrete
+    launch.  With ``id_extents`` (thread-id name -> launch extent) every id
+    of extent > 1 is an enumerated coordinate even when the path and offset
+    never mention it (the concrete oracle runs every thread of the launch,
+    SPEC.md:586-600); without it only the mentioned ids are, as the
+    reference's symbolic twin query has them (engine/detectors.py:234-273)."""
     names: Dict[str, str] = {}
     for a in path:
         ir.symbols_of(a, names)
@@ -281,7 +294,16 @@ def race_program(assertions: Sequence[ir.Node], origin_of: Callable[[str], str],
         free |= set(ir.symbols_of(a))
     free |= set(ir.symbols_of(offset))
     free |= {n for n in ID_NAMES if n in widths and n not in fixed}
+    extra: Dict[str, Tuple[int, int]] = {}
+    if id_extents:
+        for n in ID_NAMES:
+            if n not in widths and n not in fixed and id_extents.get(n, 1) > 1:
+                extra[n] = (0, int(id_extents[n]) - 1)
+        free |= set(extra)
     for n in free:
+        if n in extra:
+            bounds[n] = extra[n]
+            continue
         b = ps.bounds.get(n)
         if b is None:
             b = ir.bounds(widths[n]) if n in widths else (None, None)

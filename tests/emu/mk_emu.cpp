@@ -277,3 +277,89 @@ extern "C" int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_resu
   out->hbm_bytes = 4ull * 12ull * out->tuples;
   return MK_OK;
 }
+
+// -- access sweep (K2, oracle semantics), serial restatement of csrc/mk_access.cuh --
+
+extern "C" int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access_result* out) {
+  std::memset(out, 0, sizeof(*out));
+  const mk_problem_set& set = in->set;
+  long long grid[3], block[3];
+  for (int k = 0; k < 3; ++k) {
+    grid[k] = in->grid[k] > 0 ? in->grid[k] : 1;
+    block[k] = in->block[k] > 0 ? in->block[k] : 1;
+  }
+  std::vector<std::pair<unsigned long long, unsigned long long>> tuples;  // (key, val), dense order
+  unsigned long long slot = 0;
+  std::vector<MkCvT<int64_t>> R(MK_MAXR);
+  for (int pi = 0; pi < set.nprob; ++pi) {
+    const mk_problem& p = set.probs[pi];
+    const mk_access_prog& A = in->progs[pi];
+    if (!(p.flags & MK_PF_NARROW)) {
+      ctx->err = "access sweep needs narrow problems";
+      return MK_EINVAL;
+    }
+    MkProb P = mk_prob_view(set.probs, pi, set.insns, set.consts, set.atom_regs, set.atom_masks,
+                            set.rows, set.row_terms);
+    const int nv = p.nvars, n_outer = nv - A.n_exist;
+    std::vector<int64_t> lo(nv), hi(nv);
+    unsigned long long vol = 1, inner = 1;
+    for (int i = 0; i < nv; ++i) {
+      lo[i] = (int64_t)set.var_lo[p.var_off + i].lo;
+      hi[i] = (int64_t)set.var_hi[p.var_off + i].lo;
+      (i < n_outer ? vol : inner) *= (unsigned long long)(hi[i] - lo[i] + 1);
+    }
+    int64_t x[MK_MAXV];
+    for (unsigned long long idx = 0; idx < vol; ++idx, slot += (unsigned long long)A.tuples) {
+      bool hit = false;
+      int64_t off = 0;
+      for (unsigned long long j = 0; j < inner && !hit; ++j) {
+        mk_decode(lo.data(), hi.data(), nv, 0ull, idx * inner + j, x);
+        bool ovf = false;
+        int64_t cnt = 0;
+        out->instances++;
+        if (mk_eval_point(P, x, R.data(), &ovf, &cnt)) {
+          hit = true;
+          off = R[A.off_reg].v;
+        }
+      }
+      if (!hit) continue;
+      long long id[6];
+      for (int k = 0; k < 6; ++k) id[k] = A.id_var[k] >= 0 ? (long long)x[A.id_var[k]] : A.id_fixed[k];
+      const unsigned long long blk = ((unsigned long long)id[2] * grid[1] + id[1]) * grid[0] + id[0];
+      const unsigned long long thr = ((unsigned long long)id[5] * block[1] + id[4]) * block[0] + id[3];
+      const unsigned long long nthr = (unsigned long long)(block[0] * block[1] * block[2]);
+      const unsigned long long idk = A.shared ? thr : blk * nthr + thr;
+      const long long rel = (long long)off - A.off_lo;
+      if (rel < 0 || rel % A.granule) out->misaligned = 1;
+      const unsigned long long k0 =
+          A.kbase + (A.shared ? blk * A.span : 0ull) + (unsigned long long)(rel / A.granule);
+      for (int j = 0; j < A.tuples; ++j)
+        tuples.push_back({((k0 + j) << 1) | (A.write ? 0ull : 1ull), (idk << 32) | (slot + j)});
+    }
+  }
+  out->tuples = tuples.size();
+  if (out->misaligned) return MK_OK;
+  std::stable_sort(tuples.begin(), tuples.end(),
+                   [](const std::pair<unsigned long long, unsigned long long>& a,
+                      const std::pair<unsigned long long, unsigned long long>& b) {
+                     return a.first < b.first;
+                   });
+  const size_t n = tuples.size();
+  for (size_t i = 0; i < n; ++i) {
+    const unsigned long long k = tuples[i].first;
+    if (i > 0 && (tuples[i - 1].first >> 1) == (k >> 1)) continue;
+    if (k & 1ull) continue;
+    for (size_t j = i + 1; j < n && (tuples[j].first >> 1) == (k >> 1); ++j) {
+      if ((tuples[j].second >> 32) != (tuples[i].second >> 32)) {
+        if (!out->has_race) {
+          out->slot_a = tuples[i].second & 0xffffffffull;
+          out->slot_b = tuples[j].second & 0xffffffffull;
+        }
+        out->has_race = 1;
+        out->racy++;
+        break;
+      }
+    }
+  }
+  return MK_OK;
+}
