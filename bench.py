@@ -381,6 +381,87 @@ def _race_sweep_line(chk, args, peaks, src, int_peak):
                                        "peak_source": f"peaks file: {src}"}}}
 
 
+def _access_line(chk, args, peaks, src):
+    """K2 with the specification's oracle rule (paper_2603_24595_b200.replay,
+    mk_access_sweep): every load and store the reference front end executes
+    on fused_add_rms_norm (Fig. 2, hidden 7168; in-place residual update,
+    shared reduction with a barrier) replayed at num_tokens = --access-tokens:
+    granule tuples of all accesses to written regions, radix-sorted in HBM,
+    segmented read-write / write-write scan.  HBM roofline: algorithmic bytes
+    = 4 x 16 B per tuple (8 B key + 8 B value; one write at
+    generation, one read + one write for a single-pass-equivalent sort, one
+    read in the scan) / device time."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from refpath import add_reference, analyze_workload
+
+    if not add_reference():
+        return {"unavailable": "reference front end not installed under baseline/_ref"}
+    from paper_2603_24595_b200 import replay
+    from paper_2603_24595_b200.detectors import install, uninstall
+
+    name = "fused_add_rms_norm"
+    recs = []
+    prev = install(checker=chk, recorders=recs)
+    try:
+        analyze_workload(name)
+    finally:
+        uninstall(prev)
+    records = [a for d in recs for a in d.accesses]
+    origin_of = recs[0].table.origin_of
+    T = args.access_tokens
+    launch = replay.launch_model(chk, records, origin_of, {"BS": 1, "SL": T})
+    for _ in range(2):
+        replay.replay_races(chk.engine, records, origin_of, launch)
+    runs = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        r = replay.replay_races(chk.engine, records, origin_of, launch)
+        runs.append((time.perf_counter() - t0, r))
+    res = runs[-1][1]
+    # device phases of the last call (the result carries no timings: take them
+    # from one direct sweep of the same layout)
+    accs, progs, key_bits, _ = replay.build(records, origin_of, launch)
+    grid = [launch[d] for d in replay.DIMS[:3]]
+    block = [launch[d] for d in replay.DIMS[3:]]
+    probs = [a.program.problem for a in accs]
+    dev = [chk.engine.access_sweep(probs, progs, grid, block, key_bits, nkeys=1 << (key_bits - 1))
+           for _ in range(3)]
+    old = os.environ.get("MK_ACCESS_NO_FAST")
+    os.environ["MK_ACCESS_NO_FAST"] = "1"
+    try:
+        srt = [chk.engine.access_sweep(probs, progs, grid, block, key_bits) for _ in range(3)]
+    finally:
+        if old is None:
+            os.environ.pop("MK_ACCESS_NO_FAST", None)
+    sort_ms = sum(d["gen_ms"] + d["sort_ms"] + d["scan_ms"] for d in srt) / len(srt)
+    ms = sum(d["gen_ms"] + d["sort_ms"] + d["scan_ms"] for d in dev) / len(dev)
+    hbm_peak = peaks.get("hbm_gbs", 6650.0) if isinstance(peaks, dict) else 6650.0
+    algo = 4 * 16 * res.tuples
+    s_ach = algo / (sort_ms / 1e3) / 1e9
+    # owner-table pass: one 4 B claim (write phase) or probe (read phase) per
+    # tuple, plus the table fill
+    own = 4 * res.tuples + 4 * (1 << (key_bits - 1))
+    ach = own / (ms / 1e3) / 1e9
+    return {"workload": f"{name} (Fig. 2, hidden 7168) at num_tokens={T}, launch "
+                        f"<<<{grid[0]}; {block[0]}>>>: every recorded access of a written region",
+            "accesses": res.accesses, "instances": res.instances, "tuples": res.tuples,
+            "has_race": res.has_race, "racy_granules": res.racy, "key_bits": key_bits,
+            "device_ms": ms, "gen_ms": dev[-1]["gen_ms"], "sort_ms": dev[-1]["sort_ms"],
+            "scan_ms": dev[-1]["scan_ms"], "wall_ms": 1e3 * min(t for t, _ in runs),
+            "tuples_per_s": res.tuples / (ms / 1e3),
+            "path": "owner table (race-free, no sort)" if dev[-1]["fast"] else "radix sort",
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": ach / hbm_peak, "traffic": None, "algorithmic_bytes": own,
+                         "peak_source": f"peaks file: {src}"},
+            "sort_path": {"ms": sort_ms, "gen_ms": srt[-1]["gen_ms"], "sort_ms": srt[-1]["sort_ms"],
+                          "scan_ms": srt[-1]["scan_ms"],
+                          "same_result": (srt[-1]["has_race"], srt[-1]["tuples"]) ==
+                                         (dev[-1]["has_race"], dev[-1]["tuples"]),
+                          "roofline": {"bound": "hbm", "achieved": s_ach, "peak": hbm_peak,
+                                       "unit": "GB/s", "frac": s_ach / hbm_peak, "traffic": None,
+                                       "algorithmic_bytes": algo}}}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -511,6 +592,8 @@ def run_b200(args):
 
     k2 = _race_sweep_line(chk, args, peaks, src, int_peak) if rank == 0 and args.race_tokens > 0 else None
     analyze = _analyze_line(chk, args, doc) if rank == 0 and world == 1 and args.analyze else None
+    access = (_access_line(chk, args, peaks, src)
+              if rank == 0 and world == 1 and args.access_tokens > 0 else None)
     heavy = (_heavy_line(chk, args, int_peak, sm_mhz, sms)
              if rank == 0 and world == 1 and args.heavy and args.heavy != args.workload else None)
 
@@ -568,6 +651,7 @@ def run_b200(args):
                                         f"(clock sampled; peaks file: {src})"},
             "cpu_baseline": cpu,
             "k2_race_sweep": k2,
+            "k2_access_replay": access,
             "time_to_verdict": analyze,
             "k1_heavy": heavy,
             "clocks": clk,
@@ -593,6 +677,8 @@ def main():
                     help="skip the end-to-end analyze() time-to-verdict line")
     ap.add_argument("--heavy", default="paged_attention_v1",
                     help="workload of the k1_heavy line ('' to skip)")
+    ap.add_argument("--access-tokens", type=int, default=16384,
+                    help="num_tokens of the oracle-rule access replay line (0: skip)")
     ap.add_argument("--race-tokens", type=int, default=262144,
                     help="num_tokens of the K2 race-sweep line (0: skip)")
     args = ap.parse_args()

@@ -274,6 +274,8 @@ typedef struct mk_access_input {
   int64_t block[3];      /* blockDim.x,y,z */
   int32_t key_bits;      /* every sort key (granule << 1 | is_read) < 2^key_bits */
   int32_t pad;
+  uint64_t nkeys;        /* granule keys in use (all < nkeys): sizes the
+                            owner table of the race-free fast path (0: none) */
 } mk_access_input;
 
 typedef struct mk_access_result {
@@ -286,6 +288,8 @@ typedef struct mk_access_result {
   uint64_t slot_a;       /* dense tuple slot of the first race's write */
   uint64_t slot_b;       /* ... and of its partner (another thread) */
   double gen_ms, sort_ms, scan_ms;
+  int32_t fast;          /* 1: decided by the owner-table pass (no sort) */
+  int32_t jit;           /* 1: generator specialised at run time (NVRTC) */
 } mk_access_result;
 
 int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access_result* out);

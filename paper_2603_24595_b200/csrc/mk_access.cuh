@@ -47,16 +47,25 @@ struct AccLaunch {
 
 constexpr int ACC_THREADS = 256;
 
+// MODE 0: dense (key, val) tuples for the sort path.  MODE 1 / 2: the
+// owner-table fast path -- writes claim their granules (atomicCAS of the
+// writer's identity; a second writer identity is a race), then reads check
+// them (a granule owned by another identity is a race).  No tuple reaches
+// HBM; a launch without races is decided exactly, one with races goes to the
+// sort path for the canonical first pair and the racy-granule count.
+constexpr unsigned ACC_EMPTY = 0xffffffffu;
+
+template <int MODE>
 __global__ void __launch_bounds__(ACC_THREADS) k_acc_gen(
     const AccDev* __restrict__ progs, int nprog, unsigned long long total, AccLaunch L,
     const mk_problem* probs, const mk_insn* insns, const mk_i128* consts, const int32_t* ar,
     const uint64_t* am, const mk_row* rows, const mk_row_term* terms, const mk_i128* vlo,
     const mk_i128* vhi, unsigned long long* keys, unsigned long long* vals,
-    unsigned long long* ctr) {
+    unsigned* owner, unsigned long long* ctr) {
   extern __shared__ int64_t sh[];
   int64_t lo[SMALL_V], hi[SMALL_V], x[SMALL_V];
   unsigned long long done = 0, emitted = 0;
-  bool misaligned = false;
+  bool misaligned = false, race = false;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   for (unsigned long long g = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
        g += stride) {
@@ -67,6 +76,8 @@ __global__ void __launch_bounds__(ACC_THREADS) k_acc_gen(
       if (progs[m].start <= g) a = m; else b = m - 1;
     }
     const AccDev& A = progs[a];
+    if (MODE == 1 && !A.write) continue;
+    if (MODE == 2 && A.write) continue;
     const unsigned long long local = g - A.start;
     const MkProb P = mk_prob_view(probs, A.prob, insns, consts, ar, am, rows, terms);
     const int nv = P.p->nvars;
@@ -74,7 +85,15 @@ __global__ void __launch_bounds__(ACC_THREADS) k_acc_gen(
       lo[i] = (int64_t)vlo[P.p->var_off + i].lo;
       hi[i] = (int64_t)vhi[P.p->var_off + i].lo;
     }
-    mk_decode(lo, hi, A.n_outer, 0ull, local, x);
+    {
+      // instance boxes hold < 2^31 instances: 32-bit mixed-radix decode
+      unsigned r = (unsigned)local;
+      for (int i = A.n_outer - 1; i >= 0; --i) {
+        const unsigned sp = (unsigned)(hi[i] - lo[i] + 1);
+        x[i] = lo[i] + (int64_t)(r % sp);
+        r /= sp;
+      }
+    }
     bool hit = false;
     int64_t off = 0;
     for (unsigned long long j = 0; j < A.inner && !hit; ++j) {
@@ -92,6 +111,7 @@ __global__ void __launch_bounds__(ACC_THREADS) k_acc_gen(
     }
     const unsigned long long slot0 = A.slot + local * (unsigned long long)A.tuples;
     if (!hit) {
+      if (MODE) continue;
       for (int j = 0; j < A.tuples; ++j) {
         keys[slot0 + j] = ~0ull;
         vals[slot0 + j] = 0ull;
@@ -110,9 +130,22 @@ __global__ void __launch_bounds__(ACC_THREADS) k_acc_gen(
     if (rel < 0 || rel % A.granule) misaligned = true;
     const unsigned long long k0 =
         A.kbase + (A.shared ? blk * A.span : 0ull) + (unsigned long long)(rel / A.granule);
-    for (int j = 0; j < A.tuples; ++j) {
-      keys[slot0 + j] = ((k0 + (unsigned long long)j) << 1) | (A.write ? 0ull : 1ull);
-      vals[slot0 + j] = (idk << 32) | (slot0 + (unsigned long long)j);
+    if (MODE == 0) {
+      for (int j = 0; j < A.tuples; ++j) {
+        keys[slot0 + j] = ((k0 + (unsigned long long)j) << 1) | (A.write ? 0ull : 1ull);
+        vals[slot0 + j] = (idk << 32) | (slot0 + (unsigned long long)j);
+      }
+    } else if (!misaligned) {
+      for (int j = 0; j < A.tuples; ++j) {
+        unsigned* o = owner + (k0 + (unsigned long long)j);
+        if (MODE == 1) {
+          const unsigned old = atomicCAS(o, ACC_EMPTY, (unsigned)idk);
+          if (old != ACC_EMPTY && old != (unsigned)idk) race = true;
+        } else {
+          const unsigned w = *o;
+          if (w != ACC_EMPTY && w != (unsigned)idk) race = true;
+        }
+      }
     }
     emitted += (unsigned long long)A.tuples;
   }
@@ -121,10 +154,12 @@ __global__ void __launch_bounds__(ACC_THREADS) k_acc_gen(
     emitted += __shfl_down_sync(FULL, emitted, o);
   }
   const bool mis = __any_sync(FULL, misaligned);
+  const bool rc = __any_sync(FULL, race);
   if ((threadIdx.x & 31) == 0) {
     if (done) atomicAdd(ctr + 0, done);
     if (emitted) atomicAdd(ctr + 1, emitted);
     if (mis) atomicOr(ctr + 2, 1ull);
+    if (rc) atomicOr(ctr + 6, 1ull);
   }
 }
 
@@ -281,24 +316,108 @@ extern "C" int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access
     L.block[k] = in->block[k] > 0 ? in->block[k] : 1;
   }
   const size_t shm = sizeof(int64_t) * (size_t)maxr * ACC_THREADS;
-  if (shm > 48 * 1024)
-    CK(cudaFuncSetAttribute(k_acc_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  if (shm > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_acc_gen<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    CK(cudaFuncSetAttribute(k_acc_gen<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    CK(cudaFuncSetAttribute(k_acc_gen<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+  }
   const int grid = ctx->sms * 8;
+  const mk_problem* d_probs = reinterpret_cast<const mk_problem*>(base + ds->o_probs);
+  const mk_insn* d_insn = reinterpret_cast<const mk_insn*>(base + ds->o_insn);
+  const mk_i128* d_const = reinterpret_cast<const mk_i128*>(base + ds->o_const);
+  const int32_t* d_ar = reinterpret_cast<const int32_t*>(base + ds->o_ar);
+  const uint64_t* d_am = reinterpret_cast<const uint64_t*>(base + ds->o_am);
+  const mk_row* d_rows = reinterpret_cast<const mk_row*>(base + ds->o_rows);
+  const mk_row_term* d_terms = reinterpret_cast<const mk_row_term*>(base + ds->o_terms);
+  const mk_i128* d_vlo = reinterpret_cast<const mk_i128*>(base + ds->o_vlo);
+  const mk_i128* d_vhi = reinterpret_cast<const mk_i128*>(base + ds->o_vhi);
+  unsigned long long h[8];
+  // specialised generator (NVRTC): straight-line access functions with
+  // int32-typed registers; the interpreted k_acc_gen<MODE> otherwise
+  cudaKernel_t jk = nullptr;
+  if (!getenv("MK_NO_JIT") && total) {
+    std::vector<mkjit::AccGenInfo> info(np);
+    for (int i = 0; i < np; ++i) {
+      const mk_problem& p = set.probs[i];
+      mkjit::AccGenInfo& I = info[i];
+      I.n_outer = dev[i].n_outer;
+      I.start = dev[i].start;
+      I.slot = dev[i].slot;
+      I.vol = dev[i].vol;
+      I.lo.resize(p.nvars);
+      I.hi.resize(p.nvars);
+      for (int v = 0; v < p.nvars; ++v) {
+        I.lo[v] = (int64_t)set.var_lo[p.var_off + v].lo;
+        I.hi[v] = (int64_t)set.var_hi[p.var_off + v].lo;
+      }
+      if (!getenv("MK_JIT_WIDE")) I.rbits = register_bits(set, i, I.lo.data(), I.hi.data());
+    }
+    const std::string src = mkjit::access_gen_source(set, in->progs, info, L.grid, L.block, total);
+    if (const char* dump = getenv("MK_JIT_DUMP_ACCESS")) {
+      FILE* f = fopen(dump, "w");
+      if (f) {
+        fputs(src.c_str(), f);
+        fclose(f);
+      }
+    }
+    jk = mkjit::get_kernel(ctx->jit, src, ctx->device, "mk_access_jit");
+  }
+  out->jit = jk != nullptr;
+  auto gen = [&](int mode, unsigned long long* keys, unsigned long long* vals,
+                 unsigned* owner) -> cudaError_t {
+    if (jk) {
+      int a_mode = mode;
+      unsigned long long* a_keys = keys;
+      unsigned long long* a_vals = vals;
+      unsigned* a_owner = owner;
+      unsigned long long* a_ctr = ctr;
+      void* args[] = {&a_mode, &a_keys, &a_vals, &a_owner, &a_ctr};
+      return cudaLaunchKernel((const void*)jk, dim3(grid), dim3(ACC_THREADS), args, 0, s);
+    }
+    if (mode == 0)
+      k_acc_gen<0><<<grid, ACC_THREADS, shm, s>>>(d_dev, np, total, L, d_probs, d_insn, d_const, d_ar,
+                                                  d_am, d_rows, d_terms, d_vlo, d_vhi, keys, vals,
+                                                  owner, ctr);
+    else if (mode == 1)
+      k_acc_gen<1><<<grid, ACC_THREADS, shm, s>>>(d_dev, np, total, L, d_probs, d_insn, d_const, d_ar,
+                                                  d_am, d_rows, d_terms, d_vlo, d_vhi, keys, vals,
+                                                  owner, ctr);
+    else
+      k_acc_gen<2><<<grid, ACC_THREADS, shm, s>>>(d_dev, np, total, L, d_probs, d_insn, d_const, d_ar,
+                                                  d_am, d_rows, d_terms, d_vlo, d_vhi, keys, vals,
+                                                  owner, ctr);
+    return cudaGetLastError();
+  };
+  // fast path: the owner table (one u32 per granule key) when it fits
+  if (total && in->nkeys > 0 && in->nkeys <= (1ull << 30) && !getenv("MK_ACCESS_NO_FAST")) {
+    void* otab = nullptr;
+    CK(cudaMallocAsync(&otab, sizeof(unsigned) * in->nkeys, s));
+    unsigned* owner = static_cast<unsigned*>(otab);
+    CK(cudaMemsetAsync(owner, 0xff, sizeof(unsigned) * in->nkeys, s));
+    CK(cudaEventRecord(ctx->ev[0], s));
+    CK(gen(1, nullptr, nullptr, owner));
+    CK(gen(2, nullptr, nullptr, owner));
+    CK(cudaEventRecord(ctx->ev[1], s));
+    CK(cudaFreeAsync(otab, s));
+    CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h[2] || !h[6]) {
+      // misaligned (host reruns at granule 1) or race-free: decided
+      out->instances = h[0];
+      out->tuples = h[1];
+      out->misaligned = h[2] ? 1 : 0;
+      out->fast = 1;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+      out->gen_ms = ms;
+      return MK_OK;
+    }
+    CK(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  }
   CK(cudaEventRecord(ctx->ev[0], s));
-  if (total)
-    k_acc_gen<<<grid, ACC_THREADS, shm, s>>>(
-        d_dev, np, total, L, reinterpret_cast<const mk_problem*>(base + ds->o_probs),
-        reinterpret_cast<const mk_insn*>(base + ds->o_insn),
-        reinterpret_cast<const mk_i128*>(base + ds->o_const),
-        reinterpret_cast<const int32_t*>(base + ds->o_ar),
-        reinterpret_cast<const uint64_t*>(base + ds->o_am),
-        reinterpret_cast<const mk_row*>(base + ds->o_rows),
-        reinterpret_cast<const mk_row_term*>(base + ds->o_terms),
-        reinterpret_cast<const mk_i128*>(base + ds->o_vlo),
-        reinterpret_cast<const mk_i128*>(base + ds->o_vhi), k0, v0, ctr);
+  if (total) CK(gen(0, k0, v0, nullptr));
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[1], s));
-  unsigned long long h[8];
   CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   out->instances = h[0];

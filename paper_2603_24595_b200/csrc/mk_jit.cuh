@@ -15,7 +15,9 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <functional>
 #include <map>
+#include <vector>
 #include <sstream>
 #include <string>
 
@@ -64,6 +66,69 @@ inline std::string lit(int64_t v) {
   std::ostringstream o;
   o << v << "LL";
   return o.str();
+}
+
+// Straight-line evaluation of one path program's bytecode (registers as
+// locals v<r> with error flags e<r>; an atom that is false or in error
+// breaks out of the enclosing do { } while (0)).  Vars are x<i>.
+inline void emit_path(std::ostringstream& s, const mk_problem& p, const mk_insn* insns,
+                      const mk_i128* consts, const int* rbits) {
+  const int nv = p.nvars, nc = p.nconst, nr = p.nregs;
+  auto b32 = [&](int r) { return rbits && rbits[r] == 32; };
+  auto ty = [&](int r) { return b32(r) ? "int" : "i64"; };
+  for (int r = nv + nc; r < nr; ++r) s << "      " << ty(r) << " v" << r << " = 0; bool e" << r << " = false;\n";
+  for (int i = 0; i < nv; ++i) s << "      const " << ty(i) << " v" << i << " = x" << i << "; const bool e" << i << " = false;\n";
+  for (int i = 0; i < nc; ++i)
+    s << "      const " << ty(nv + i) << " v" << (nv + i) << " = " << lit((int64_t)consts[i].lo)
+      << "; const bool e" << (nv + i) << " = false;\n";
+  for (int k = 0; k < p.ninsn; ++k) {
+    const mk_insn in = insns[k];
+    const int a = in.a, b = in.b, c = in.c, d = in.dst;
+    if (in.op == MK_OP_ATOM) {
+      s << "      if (e" << a << " || !v" << a << ") break;\n";
+      continue;
+    }
+    // 32-bit arithmetic only when operands and result are all int32-bounded
+    // (then the mathematical result is the int32 result); shifts stay int64
+    const bool arith32 = b32(a) && b32(b) && b32(d) && in.op != MK_OP_SHL && in.op != MK_OP_SHR;
+    const char* OT = arith32 ? "int" : "i64";
+    s << "      { const " << OT << " A = (" << OT << ")v" << a << ", B = (" << OT << ")v" << b
+      << "; const bool EA = e" << a << ", EB = e" << b << "; " << OT
+      << " R = 0; bool E = false; (void)A; (void)B; (void)EA; (void)EB;\n        ";
+    switch (in.op) {
+      case MK_OP_AND: s << "if (EA) E = true; else if (!A) R = 0; else { R = B ? 1 : 0; E = EB; }"; break;
+      case MK_OP_OR: s << "if (EA) E = true; else if (A) R = 1; else { R = B ? 1 : 0; E = EB; }"; break;
+      case MK_OP_NOT: s << "E = EA; R = A ? 0 : 1;"; break;
+      case MK_OP_ITE:
+        s << "const " << OT << " C = (" << OT << ")v" << c << "; const bool EC = e" << c
+          << "; if (EA) E = true; else if (A) { R = B; E = EB; } else { R = C; E = EC; }";
+        break;
+      default: {
+        s << "E = EA || EB; if (!E) { ";
+        switch (in.op) {
+          case MK_OP_ADD: s << "R = A + B;"; break;
+          case MK_OP_SUB: s << "R = A - B;"; break;
+          case MK_OP_MUL: s << "R = A * B;"; break;
+          case MK_OP_SHL: s << "R = mk_shl(A, B);"; break;
+          case MK_OP_SHR: s << "R = mk_shr(A, B);"; break;
+          case MK_OP_DIV: s << "if (B == 0) E = true; else R = A / B;"; break;
+          case MK_OP_MOD: s << "if (B == 0) E = true; else R = A % B;"; break;
+          case MK_OP_EMOD:
+            s << "if (B == 0) E = true; else R = " << (arith32 ? "mk_emod32" : "mk_emod") << "(A, B);";
+            break;
+          case MK_OP_EQ: s << "R = A == B;"; break;
+          case MK_OP_NE: s << "R = A != B;"; break;
+          case MK_OP_LT: s << "R = A < B;"; break;
+          case MK_OP_LE: s << "R = A <= B;"; break;
+          case MK_OP_GT: s << "R = A > B;"; break;
+          case MK_OP_GE: s << "R = A >= B;"; break;
+          default: s << "E = true;"; break;
+        }
+        s << " }";
+      }
+    }
+    s << "\n        v" << d << " = (" << ty(d) << ")R; e" << d << " = E; }\n";
+  }
 }
 
 // CUDA source of the race generators for one program (host copy of the
@@ -120,59 +185,7 @@ inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
         << " + (i64)(jj % (unsigned long long)sp" << i << ")); jj /= (unsigned long long)sp" << i << ";\n";
   }
   s << (count_inner ? "    ++done;\n" : "") << "    bool hit = false;\n    i64 off = 0;\n    do {\n";
-  for (int r = nv + nc; r < nr; ++r) s << "      " << ty(r) << " v" << r << " = 0; bool e" << r << " = false;\n";
-  for (int i = 0; i < nv; ++i) s << "      const " << ty(i) << " v" << i << " = x" << i << "; const bool e" << i << " = false;\n";
-  for (int i = 0; i < nc; ++i)
-    s << "      const " << ty(nv + i) << " v" << (nv + i) << " = " << lit((int64_t)consts[i].lo)
-      << "; const bool e" << (nv + i) << " = false;\n";
-  for (int k = 0; k < p.ninsn; ++k) {
-    const mk_insn in = insns[k];
-    const int a = in.a, b = in.b, c = in.c, d = in.dst;
-    if (in.op == MK_OP_ATOM) {
-      s << "      if (e" << a << " || !v" << a << ") break;\n";
-      continue;
-    }
-    // 32-bit arithmetic only when operands and result are all int32-bounded
-    // (then the mathematical result is the int32 result); shifts stay int64
-    const bool arith32 = b32(a) && b32(b) && b32(d) && in.op != MK_OP_SHL && in.op != MK_OP_SHR;
-    const char* OT = arith32 ? "int" : "i64";
-    s << "      { const " << OT << " A = (" << OT << ")v" << a << ", B = (" << OT << ")v" << b
-      << "; const bool EA = e" << a << ", EB = e" << b << "; " << OT
-      << " R = 0; bool E = false; (void)A; (void)B; (void)EA; (void)EB;\n        ";
-    switch (in.op) {
-      case MK_OP_AND: s << "if (EA) E = true; else if (!A) R = 0; else { R = B ? 1 : 0; E = EB; }"; break;
-      case MK_OP_OR: s << "if (EA) E = true; else if (A) R = 1; else { R = B ? 1 : 0; E = EB; }"; break;
-      case MK_OP_NOT: s << "E = EA; R = A ? 0 : 1;"; break;
-      case MK_OP_ITE:
-        s << "const " << OT << " C = (" << OT << ")v" << c << "; const bool EC = e" << c
-          << "; if (EA) E = true; else if (A) { R = B; E = EB; } else { R = C; E = EC; }";
-        break;
-      default: {
-        s << "E = EA || EB; if (!E) { ";
-        switch (in.op) {
-          case MK_OP_ADD: s << "R = A + B;"; break;
-          case MK_OP_SUB: s << "R = A - B;"; break;
-          case MK_OP_MUL: s << "R = A * B;"; break;
-          case MK_OP_SHL: s << "R = mk_shl(A, B);"; break;
-          case MK_OP_SHR: s << "R = mk_shr(A, B);"; break;
-          case MK_OP_DIV: s << "if (B == 0) E = true; else R = A / B;"; break;
-          case MK_OP_MOD: s << "if (B == 0) E = true; else R = A % B;"; break;
-          case MK_OP_EMOD:
-            s << "if (B == 0) E = true; else R = " << (arith32 ? "mk_emod32" : "mk_emod") << "(A, B);";
-            break;
-          case MK_OP_EQ: s << "R = A == B;"; break;
-          case MK_OP_NE: s << "R = A != B;"; break;
-          case MK_OP_LT: s << "R = A < B;"; break;
-          case MK_OP_LE: s << "R = A <= B;"; break;
-          case MK_OP_GT: s << "R = A > B;"; break;
-          case MK_OP_GE: s << "R = A >= B;"; break;
-          default: s << "E = true;"; break;
-        }
-        s << " }";
-      }
-    }
-    s << "\n        v" << d << " = (" << ty(d) << ")R; e" << d << " = E; }\n";
-  }
+  emit_path(s, p, insns, consts, rbits);
   s << "      hit = true; off = (i64)v" << off_reg << ";\n    } while (0);\n";
   s << "    if (hit) {\n      u64 bk = 0;\n";
   if (shared) {
@@ -338,6 +351,126 @@ inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
        "    if (done) atomicAdd(ctr + 3, done);\n"
        "    if (anydown) atomicOr(ctr + 4, 1ull);\n"
        "  }\n}\n";
+  return s.str();
+}
+
+// CUDA source of the multi-access generator (mk_access.cuh): one straight-
+// line access function per access program and one kernel that dispatches a
+// global instance index to its program with a balanced if-tree over the
+// literal instance starts.  mode 0: dense (key, val) tuples; 1 / 2: the
+// owner-table write / read passes (semantics of k_acc_gen).
+struct AccGenInfo {
+  int n_outer = 0;
+  unsigned long long start = 0, slot = 0, vol = 0;
+  std::vector<int64_t> lo, hi;
+  std::vector<int> rbits;
+};
+
+inline std::string access_gen_source(const mk_problem_set& set, const mk_access_prog* progs,
+                                     const std::vector<AccGenInfo>& info, const long long grid[3],
+                                     const long long block[3], unsigned long long total) {
+  const int np = set.nprob;
+  std::ostringstream s;
+  s << "typedef long long i64;\ntypedef unsigned long long u64;\n"
+       "__device__ __forceinline__ i64 mk_emod(i64 a, i64 b) { i64 m = b < 0 ? -b : b; i64 r = a % m;"
+       " return r < 0 ? r + m : r; }\n"
+       "__device__ __forceinline__ int mk_emod32(int a, int b) { int m = b < 0 ? -b : b; int r = a % m;"
+       " return r < 0 ? r + m : r; }\n"
+       "__device__ __forceinline__ i64 mk_shl(i64 a, i64 k) { return k >= 62 ? 0 :"
+       " (i64)((unsigned long long)a << k); }\n"
+       "__device__ __forceinline__ i64 mk_shr(i64 a, i64 k) { return a >> (k > 63 ? 63 : k); }\n";
+  const unsigned long long nthr = (unsigned long long)(block[0] * block[1] * block[2]);
+  for (int pi = 0; pi < np; ++pi) {
+    const mk_problem& p = set.probs[pi];
+    const mk_access_prog& A = progs[pi];
+    const AccGenInfo& I = info[pi];
+    const int nv = p.nvars, n_outer = I.n_outer;
+    const int* rb = I.rbits.empty() ? nullptr : I.rbits.data();
+    auto ty = [&](int r) { return rb && rb[r] == 32 ? "int" : "i64"; };
+    s << "__device__ __forceinline__ bool acc_" << pi
+      << "(unsigned local, u64& k0, unsigned& idk, bool& mis, u64& done) {\n"
+         "  unsigned r = local; (void)r;\n";
+    for (int i = n_outer - 1; i >= 0; --i) {
+      const unsigned long long sp = (unsigned long long)(I.hi[i] - I.lo[i] + 1);
+      s << "  const " << ty(i) << " x" << i << " = (" << ty(i) << ")(" << lit(I.lo[i]) << " + (i64)(r % "
+        << sp << "u)); r /= " << sp << "u;\n";
+    }
+    unsigned long long inner = 1;
+    for (int i = n_outer; i < nv; ++i) inner *= (unsigned long long)(I.hi[i] - I.lo[i] + 1);
+    s << "  for (unsigned long long j = 0; j < " << inner << "ULL; ++j) {\n";
+    if (nv > n_outer) {
+      s << "    unsigned long long jj = j;\n";
+      for (int i = nv - 1; i >= n_outer; --i) {
+        const unsigned long long sp = (unsigned long long)(I.hi[i] - I.lo[i] + 1);
+        s << "    const " << ty(i) << " x" << i << " = (" << ty(i) << ")(" << lit(I.lo[i])
+          << " + (i64)(jj % " << sp << "ull)); jj /= " << sp << "ull;\n";
+      }
+    }
+    s << "    ++done;\n    bool hit = false;\n    i64 off = 0;\n    do {\n";
+    emit_path(s, p, set.insns + p.insn_off, set.consts + p.const_off, rb);
+    s << "      hit = true; off = (i64)v" << A.off_reg << ";\n    } while (0);\n";
+    s << "    if (hit) {\n";
+    for (int k = 0; k < 6; ++k) {
+      s << "      const u64 id" << k << " = (u64)";
+      if (A.id_var[k] >= 0) s << "(i64)x" << A.id_var[k];
+      else s << lit(A.id_fixed[k]);
+      s << ";\n";
+    }
+    s << "      const u64 blk = (id2 * " << grid[1] << "ull + id1) * " << grid[0] << "ull + id0;\n"
+      << "      const u64 thr = (id5 * " << block[1] << "ull + id4) * " << block[0] << "ull + id3;\n"
+      << "      idk = (unsigned)(" << (A.shared ? "thr" : "blk * " + std::to_string(nthr) + "ull + thr") << ");\n"
+      << "      const i64 rel = off - (" << lit(A.off_lo) << ");\n"
+      << "      if (rel < 0 || rel % " << A.granule << " != 0) mis = true;\n"
+      << "      k0 = " << A.kbase << "ull + " << (A.shared ? "blk * " + std::to_string(A.span) + "ull" : "0ull")
+      << " + (u64)(rel / " << A.granule << ");\n"
+      << "      (void)blk; (void)thr;\n      return true;\n    }\n  }\n  return false;\n}\n";
+  }
+  // dispatch tree
+  std::function<void(int, int, int)> tree = [&](int a, int b, int ind) {
+    const std::string pad(ind, ' ');
+    if (a == b) {
+      const mk_access_prog& A = progs[a];
+      const AccGenInfo& I = info[a];
+      s << pad << "if ((mode == 1 && !" << A.write << ") || (mode == 2 && " << A.write << ")) continue;\n"
+        << pad << "{ const unsigned l = (unsigned)(g - " << I.start << "ull);\n"
+        << pad << "  hit = acc_" << a << "(l, k0, idk, mis, done); T = " << A.tuples << "; W = "
+        << A.write << "; slot0 = " << I.slot << "ull + (u64)l * " << A.tuples << "ull; }\n";
+      return;
+    }
+    const int m = (a + b) / 2;
+    s << pad << "if (g < " << info[m + 1].start << "ull) {\n";
+    tree(a, m, ind + 2);
+    s << pad << "} else {\n";
+    tree(m + 1, b, ind + 2);
+    s << pad << "}\n";
+  };
+  s << "extern \"C\" __global__ void __launch_bounds__(256) mk_access_jit(int mode, u64* keys, u64* vals,"
+       " unsigned* owner, u64* ctr) {\n"
+       "  u64 done = 0, emitted = 0;\n  bool mis = false, race = false;\n"
+       "  const u64 stride = (u64)gridDim.x * blockDim.x;\n"
+       "  for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g < " << total << "ull; g += stride) {\n"
+       "    u64 k0 = 0, slot0 = 0; unsigned idk = 0; bool hit = false; int T = 1, W = 0;\n";
+  tree(0, np - 1, 4);
+  s << "    if (!hit) {\n"
+       "      if (mode == 0) for (int j = 0; j < T; ++j) { keys[slot0 + j] = ~0ull; vals[slot0 + j] = 0ull; }\n"
+       "      continue;\n    }\n"
+       "    if (mode == 0) {\n"
+       "      for (int j = 0; j < T; ++j) { keys[slot0 + j] = ((k0 + (u64)j) << 1) | (W ? 0ull : 1ull);"
+       " vals[slot0 + j] = ((u64)idk << 32) | (slot0 + (u64)j); }\n"
+       "    } else if (!mis) {\n"
+       "      for (int j = 0; j < T; ++j) {\n"
+       "        unsigned* o = owner + (k0 + (u64)j);\n"
+       "        if (mode == 1) { const unsigned old = atomicCAS(o, 0xffffffffu, idk);"
+       " if (old != 0xffffffffu && old != idk) race = true; }\n"
+       "        else { const unsigned w = *o; if (w != 0xffffffffu && w != idk) race = true; }\n"
+       "      }\n    }\n"
+       "    emitted += (u64)T;\n  }\n"
+       "  for (int o = 16; o > 0; o >>= 1) { done += __shfl_down_sync(0xffffffffu, done, o);"
+       " emitted += __shfl_down_sync(0xffffffffu, emitted, o); }\n"
+       "  const bool am = __any_sync(0xffffffffu, mis), ar = __any_sync(0xffffffffu, race);\n"
+       "  if ((threadIdx.x & 31) == 0) { if (done) atomicAdd(ctr + 0, done);"
+       " if (emitted) atomicAdd(ctr + 1, emitted); if (am) atomicOr(ctr + 2, 1ull);"
+       " if (ar) atomicOr(ctr + 6, 1ull); }\n}\n";
   return s.str();
 }
 

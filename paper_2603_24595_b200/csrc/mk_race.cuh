@@ -248,6 +248,38 @@ struct NotSentinel {
 }  // namespace
 
 
+// Register widths of problem `pid` for the specialised generators: interval
+// evaluation of its instance box on the host (the device's own interval
+// semantics, mk_core.cuh); a register whose range stays inside int32 is 32.
+static std::vector<int> register_bits(const mk_problem_set& set, int pid, const int64_t* lo,
+                                      const int64_t* hi) {
+  const mk_problem& hp = set.probs[pid];
+  std::vector<int> rbits(hp.nregs, 64);
+  const MkProb HP = mk_prob_view(set.probs, pid, set.insns, set.consts, set.atom_regs,
+                                 set.atom_masks, set.rows, set.row_terms);
+  std::vector<MkIvT<i128>> Rg(MK_MAXR);
+  for (auto& r : Rg) {
+    r.lo = 1;
+    r.hi = 0;
+    r.fl = 0;
+  }
+  std::vector<i128> vl(hp.nvars), vh(hp.nvars);
+  for (int i = 0; i < hp.nvars; ++i) {
+    vl[i] = (i128)lo[i];
+    vh[i] = (i128)hi[i];
+  }
+  int64_t cnt = 0;
+  const MkBoxVerdict bv = mk_eval_box<i128>(HP, vl.data(), vh.data(), Rg.data(), &cnt);
+  if (!bv.any_false) {
+    for (int r = 0; r < hp.nregs; ++r) {
+      const MkIvT<i128>& g = Rg[r];
+      if ((g.fl & MK_FL_OK) && g.lo <= g.hi && g.lo >= (i128)INT32_MIN && g.hi <= (i128)INT32_MAX)
+        rbits[r] = 32;
+    }
+  }
+  return rbits;
+}
+
 template <typename K>
 static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int bits, int nregs,
                     mk_race_result* out, char* base, unsigned long long* ctr,
@@ -293,35 +325,7 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   std::string src;
   if (!getenv("MK_NO_JIT")) {
     const mk_problem_set& set = prog->set;
-    // register widths: interval evaluation of the instance box on the host
-    // (the device's own interval semantics, mk_core.cuh); a register whose
-    // range stays inside int32 gets a 32-bit local
-    const mk_problem& hp = set.probs[0];
-    std::vector<int> rbits(hp.nregs, 64);
-    {
-      const MkProb HP = mk_prob_view(set.probs, 0, set.insns, set.consts, set.atom_regs,
-                                     set.atom_masks, set.rows, set.row_terms);
-      std::vector<MkIvT<i128>> Rg(MK_MAXR);
-      for (auto& r : Rg) {
-        r.lo = 1;
-        r.hi = 0;
-        r.fl = 0;
-      }
-      std::vector<i128> vl(hp.nvars), vh(hp.nvars);
-      for (int i = 0; i < hp.nvars; ++i) {
-        vl[i] = (i128)hlo[i];
-        vh[i] = (i128)hhi[i];
-      }
-      int64_t cnt = 0;
-      const MkBoxVerdict bv = mk_eval_box<i128>(HP, vl.data(), vh.data(), Rg.data(), &cnt);
-      if (!bv.any_false) {
-        for (int r = 0; r < hp.nregs; ++r) {
-          const MkIvT<i128>& g = Rg[r];
-          if ((g.fl & MK_FL_OK) && g.lo <= g.hi && g.lo >= (i128)INT32_MIN && g.hi <= (i128)INT32_MAX)
-            rbits[r] = 32;
-        }
-      }
-    }
+    const std::vector<int> rbits = register_bits(set, 0, hlo, hhi);
     src = mkjit::race_gen_source(
         set.probs[0], set.insns + set.probs[0].insn_off, set.consts + set.probs[0].const_off,
         R.n_outer, prog->off_reg, prog->shared, prog->id_var, hlo, hhi, sizeof(K) == 8,

@@ -110,7 +110,8 @@ class AccessProg(ctypes.Structure):
 class AccessInput(ctypes.Structure):
     _fields_ = [("set", ProblemSet), ("progs", ctypes.c_void_p),
                 ("grid", ctypes.c_int64 * 3), ("block", ctypes.c_int64 * 3),
-                ("key_bits", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("key_bits", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("nkeys", ctypes.c_uint64)]
 
 
 class AccessResult(ctypes.Structure):
@@ -118,13 +119,14 @@ class AccessResult(ctypes.Structure):
                 ("racy", ctypes.c_uint64), ("has_race", ctypes.c_int32),
                 ("misaligned", ctypes.c_int32), ("slot_a", ctypes.c_uint64),
                 ("slot_b", ctypes.c_uint64), ("gen_ms", ctypes.c_double),
-                ("sort_ms", ctypes.c_double), ("scan_ms", ctypes.c_double)]
+                ("sort_ms", ctypes.c_double), ("scan_ms", ctypes.c_double),
+                ("fast", ctypes.c_int32), ("jit", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
-assert ctypes.sizeof(AccessProg) == 120 and ctypes.sizeof(AccessResult) == 72
+assert ctypes.sizeof(AccessProg) == 120 and ctypes.sizeof(AccessResult) == 80
 assert ctypes.sizeof(RaceProg) == 144 and ctypes.sizeof(RaceResult) == 104
 
 
@@ -338,7 +340,7 @@ class Engine:
             res["pair"] = (prog.decode(res["idx_a"]), prog.decode(res["idx_b"]))
         return res
 
-    def access_sweep(self, problems, progs, grid, block, key_bits) -> dict:
+    def access_sweep(self, problems, progs, grid, block, key_bits, nkeys=0) -> dict:
         """Oracle-semantics race sweep of several accesses at one launch
         (paper_2603_24595_b200.replay -> mk_access_sweep).  ``progs`` is a
         list of dicts with the mk_access_prog fields."""
@@ -358,6 +360,7 @@ class Engine:
             inp.grid[i] = int(grid[i])
             inp.block[i] = int(block[i])
         inp.key_bits = int(key_bits)
+        inp.nkeys = int(nkeys)
         out = AccessResult()
         rc = self.lib.mk_access_sweep(self.ctx, ctypes.byref(inp), ctypes.byref(out))
         if rc != 0:

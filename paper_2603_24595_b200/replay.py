@@ -78,6 +78,7 @@ class ReplayResult:
     accesses: int                  # records swept
     skipped: List[Tuple[AccessRecord, str]] = field(default_factory=list)
     first: Optional[Dict] = None   # the first race: both accesses, threads, byte
+    fast: bool = False             # decided by the owner-table pass (race-free)
 
 
 def _threads(launch: Mapping[str, int]) -> Tuple[List[int], List[int]]:
@@ -95,7 +96,12 @@ def build(records: Sequence[AccessRecord], origin_of: Callable[[str], str],
     ext = dict(zip(ID_NAMES, grid + block))
     accs: List[Access] = []
     skipped: List[Tuple[AccessRecord, str]] = []
+    # every race has a write: a region no access writes (kernel inputs,
+    # weights) cannot race, so its reads are never swept
+    written = {r.region for r in records if r.kind == "write"}
     for r in records:
+        if r.region not in written:
+            continue
         try:
             prog = path_program(r.path, r.offset, r.shared, origin_of, launch, id_extents=ext)
         except NotSweepable as exc:
@@ -202,7 +208,8 @@ def replay_races(engine, records: Sequence[AccessRecord], origin_of: Callable[[s
         if not accs:
             return ReplayResult(False, 0, 0, 0, 0, skipped)
         grid, block = _threads(launch)
-        res = engine.access_sweep([a.program.problem for a in accs], progs, grid, block, key_bits)
+        res = engine.access_sweep([a.program.problem for a in accs], progs, grid, block, key_bits,
+                                  nkeys=1 << (key_bits - 1))
         if not res["misaligned"]:
             break
         # an offset not on its region's granule: byte granules everywhere
@@ -210,9 +217,32 @@ def replay_races(engine, records: Sequence[AccessRecord], origin_of: Callable[[s
     else:  # pragma: no cover - granule 1 is always aligned
         raise RuntimeError("access sweep misaligned at granule 1")
     out = ReplayResult(bool(res["has_race"]), int(res["racy"]), int(res["instances"]),
-                       int(res["tuples"]), len(accs), skipped)
+                       int(res["tuples"]), len(accs), skipped, fast=bool(res.get("fast", 0)))
     if out.has_race:
         a, la, ja = _locate(accs, int(res["slot_a"]))
         b, lb, jb = _locate(accs, int(res["slot_b"]))
         out.first = {"write": describe(a, la, ja), "other": describe(b, lb, jb)}
     return out
+
+
+def launch_model(checker, records: Sequence[AccessRecord], origin_of: Callable[[str], str],
+                 pins: Mapping[str, int]) -> Dict[str, int]:
+    """A concrete launch for a replay: the canonical model (decided by the
+    engine, ``checker``: engine.SiteChecker) of the launch-level atoms of the
+    first recorded path -- the context's initial constraints and wrapper
+    facts (engine/executor.py:152-200) -- with ``pins`` (e.g. BS, SL) fixed."""
+    from .race import THREAD_PRIVATE
+
+    path = records[0].path
+    widths: Dict[str, str] = {}
+    for a in path:
+        ir.symbols_of(a, widths)
+    atoms = [a for a in path
+             if all(origin_of(n) not in THREAD_PRIVATE for n in ir.symbols_of(a))]
+    for k, v in pins.items():
+        w = widths.get(k, "i64")
+        atoms.append(("p", "eq", ("s", k, w), ("c", int(v), w)))
+    r = checker.check(atoms, origin_of)
+    if r.status != "sat":
+        raise NotSweepable(f"no launch with {dict(pins)}: {r.status}")
+    return dict(r.witness)

@@ -41,27 +41,15 @@ def _recorded(name):
 
 
 def _launch(accesses, origin_of, pins):
-    """A concrete launch: the canonical model of the first path's
-    launch-level atoms with ``pins`` fixed (decided by the emulated engine)."""
-    from paper_2603_24595_b200 import ir
+    """A concrete launch (replay.launch_model, decided by the emulated engine)."""
+    from paper_2603_24595_b200 import replay
     from paper_2603_24595_b200.engine import SiteChecker
-    from paper_2603_24595_b200.race import THREAD_PRIVATE
 
-    path = accesses[0].path
-    widths = {}
-    for a in path:
-        ir.symbols_of(a, widths)
-    atoms = [a for a in path
-             if all(origin_of(n) not in THREAD_PRIVATE for n in ir.symbols_of(a))]
-    for k, v in pins.items():
-        atoms.append(("p", "eq", ("s", k, widths.get(k, "i64")), ("c", v, widths.get(k, "i64"))))
     chk = SiteChecker(lib_path=EMU, compile_workers=0)
     try:
-        r = chk.check(atoms, origin_of)
+        return replay.launch_model(chk, accesses, origin_of, pins)
     finally:
         chk.close()
-    assert r.status == "sat", r
-    return dict(r.witness)
 
 
 CASES = [
@@ -211,3 +199,37 @@ def test_device_replay_equals_emulation_at_scale():
         emu.close()
     assert (a.has_race, a.racy, a.instances, a.tuples) == (b.has_race, b.racy, b.instances, b.tuples)
     assert a.first == b.first
+    assert a.fast and not a.has_race             # race-free: the owner-table pass decides
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not HAVE_REF, reason="reference front end not available")
+@pytest.mark.parametrize("name,pins,expect", CASES)
+def test_device_fast_and_sort_paths_agree(name, pins, expect):
+    """The owner-table pass and the radix-sort path reach the same verdict;
+    a racy launch always ends on the sort path (canonical first pair)."""
+    from paper_2603_24595_b200 import replay
+    from paper_2603_24595_b200.native import Engine
+
+    accesses, origin_of = _recorded(name)
+    launch = _launch(accesses, origin_of, pins)
+    eng = Engine(0)
+    try:
+        a = replay.replay_races(eng, accesses, origin_of, launch)
+        os.environ["MK_ACCESS_NO_FAST"] = "1"
+        try:
+            b = replay.replay_races(eng, accesses, origin_of, launch)
+        finally:
+            os.environ.pop("MK_ACCESS_NO_FAST", None)
+        os.environ["MK_NO_JIT"] = "1"       # the interpreted generator, both paths
+        try:
+            c = replay.replay_races(eng, accesses, origin_of, launch)
+        finally:
+            os.environ.pop("MK_NO_JIT", None)
+    finally:
+        eng.close()
+    assert (a.has_race, a.instances, a.tuples) == (b.has_race, b.instances, b.tuples) == \
+        (c.has_race, c.instances, c.tuples)
+    assert a.fast == (not a.has_race) and not b.fast
+    if a.has_race:
+        assert (a.racy, a.first) == (b.racy, b.first) == (c.racy, c.first)
