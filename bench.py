@@ -381,14 +381,17 @@ def _race_sweep_line(chk, args, peaks, src, int_peak):
                                        "peak_source": f"peaks file: {src}"}}}
 
 
-def _access_line(chk, args, peaks, src):
+def _access_line(chk, args, peaks, src, int_peak):
     """K2 with the specification's oracle rule (paper_2603_24595_b200.replay,
     mk_access_sweep): every load and store the reference front end executes
     on fused_add_rms_norm (Fig. 2, hidden 7168; in-place residual update,
     shared reduction with a barrier) replayed at num_tokens = --access-tokens:
     granule tuples of all accesses to written regions, radix-sorted in HBM,
-    segmented read-write / write-write scan.  HBM roofline: algorithmic bytes
-    = 4 x 16 B per tuple (8 B key + 8 B value; one write at
+    segmented read-write / write-write scan.  The path that runs on a
+    race-free launch is the owner-table pass (integer-issue roofline, ncu
+    calibration profiles/ncu_access_summary.json); ``sort_path`` times the
+    radix-sort path on the same accesses, HBM roofline: algorithmic bytes =
+    4 x 16 B per tuple (8 B key + 8 B value; one write at
     generation, one read + one write for a single-pass-equivalent sort, one
     read in the scan) / device time."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -438,10 +441,11 @@ def _access_line(chk, args, peaks, src):
     hbm_peak = peaks.get("hbm_gbs", 6650.0) if isinstance(peaks, dict) else 6650.0
     algo = 4 * 16 * res.tuples
     s_ach = algo / (sort_ms / 1e3) / 1e9
-    # owner-table pass: one 4 B claim (write phase) or probe (read phase) per
-    # tuple, plus the table fill
-    own = 4 * res.tuples + 4 * (1 << (key_bits - 1))
-    ach = own / (ms / 1e3) / 1e9
+    # owner-table pass: integer-issue bound (no tuples in HBM); thread
+    # instructions per instance from the committed ncu launch list
+    cal = _calibration("access")
+    per_inst = cal.get("thread_inst_per_instance")
+    ach = res.instances * per_inst / (ms / 1e3) / 1e9 if per_inst and ms > 0 else None
     return {"workload": f"{name} (Fig. 2, hidden 7168) at num_tokens={T}, launch "
                         f"<<<{grid[0]}; {block[0]}>>>: every recorded access of a written region",
             "accesses": res.accesses, "instances": res.instances, "tuples": res.tuples,
@@ -450,9 +454,12 @@ def _access_line(chk, args, peaks, src):
             "scan_ms": dev[-1]["scan_ms"], "wall_ms": 1e3 * min(t for t, _ in runs),
             "tuples_per_s": res.tuples / (ms / 1e3),
             "path": "owner table (race-free, no sort)" if dev[-1]["fast"] else "radix sort",
-            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": ach / hbm_peak, "traffic": None, "algorithmic_bytes": own,
-                         "peak_source": f"peaks file: {src}"},
+            "roofline": {"bound": "int32-issue", "achieved": ach, "peak": int_peak / 1e9,
+                         "unit": "Gop/s", "frac": ach * 1e9 / int_peak if ach else None,
+                         "traffic": cal.get("dram_bytes"),
+                         "kernel": "mk_access_jit (NVRTC, sm_100a), owner-table write + read passes",
+                         "ops": f"SASS thread instructions per instance: {per_inst} "
+                                "(ncu, profiles/ncu_access_summary.json)"},
             "sort_path": {"ms": sort_ms, "gen_ms": srt[-1]["gen_ms"], "sort_ms": srt[-1]["sort_ms"],
                           "scan_ms": srt[-1]["scan_ms"],
                           "same_result": (srt[-1]["has_race"], srt[-1]["tuples"]) ==
@@ -592,7 +599,7 @@ def run_b200(args):
 
     k2 = _race_sweep_line(chk, args, peaks, src, int_peak) if rank == 0 and args.race_tokens > 0 else None
     analyze = _analyze_line(chk, args, doc) if rank == 0 and world == 1 and args.analyze else None
-    access = (_access_line(chk, args, peaks, src)
+    access = (_access_line(chk, args, peaks, src, int_peak)
               if rank == 0 and world == 1 and args.access_tokens > 0 else None)
     heavy = (_heavy_line(chk, args, int_peak, sm_mhz, sms)
              if rank == 0 and world == 1 and args.heavy and args.heavy != args.workload else None)

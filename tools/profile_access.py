@@ -16,6 +16,7 @@ from paper_2603_24595_b200.detectors import install, uninstall  # noqa: E402
 from paper_2603_24595_b200.engine import SiteChecker  # noqa: E402
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+FAST = len(sys.argv) > 2 and sys.argv[2] == "fast"   # owner-table path
 assert add_reference()
 torch.cuda.set_device(0)
 chk = SiteChecker(device=0, compile_workers=0)
@@ -32,11 +33,12 @@ accs, progs, key_bits, _ = replay.build(records, origin_of, launch)
 grid = [launch[d] for d in replay.DIMS[:3]]
 block = [launch[d] for d in replay.DIMS[3:]]
 probs = [a.program.problem for a in accs]
+nkeys = (1 << (key_bits - 1)) if FAST else 0
 for _ in range(2):
-    chk.engine.access_sweep(probs, progs, grid, block, key_bits)
+    chk.engine.access_sweep(probs, progs, grid, block, key_bits, nkeys)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-r = chk.engine.access_sweep(probs, progs, grid, block, key_bits)
+r = chk.engine.access_sweep(probs, progs, grid, block, key_bits, nkeys)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
 print(json.dumps(r))

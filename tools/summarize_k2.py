@@ -8,6 +8,7 @@ import json
 import sys
 
 launches, step, out = sys.argv[1], sys.argv[2], sys.argv[3]
+kernel = sys.argv[4] if len(sys.argv) > 4 else "mk_race_fused_jit"
 st = json.loads(open(step).read().strip().splitlines()[-1])
 rows = list(csv.reader(open(launches)))
 hdr = None
@@ -22,12 +23,15 @@ for r in rows:
         v = float(d["Metric Value"].replace(",", ""))
         per.setdefault(k, {}).setdefault(d["Metric Name"], 0.0)
         per[k][d["Metric Name"]] += v
-res = {"source": "tools/profile_k2.py (rms_norm output store, num_tokens 262144)",
+res = {"source": "tools/profile_k2.py (rms_norm output store, num_tokens 262144)"
+       if kernel == "mk_race_fused_jit" else
+       "tools/profile_access.py (fused_add_rms_norm accesses, num_tokens 16384)",
        "instances": st["instances"], "accesses": st["tuples"], "kernels": per}
-f = per.get("mk_race_fused_jit")
+f = per.get(kernel)
 if f and f.get("smsp__thread_inst_executed.sum"):
     res["thread_inst_per_instance"] = f["smsp__thread_inst_executed.sum"] / st["instances"]
     res["warp_inst_per_instance"] = f.get("smsp__inst_executed.sum", 0.0) / st["instances"]
-    res["fused_us"] = f.get("gpu__time_duration.sum", 0.0) / 1e3
+    res["kernel_us"] = f.get("gpu__time_duration.sum", 0.0) / 1e3
+    res["dram_bytes"] = f.get("dram__bytes_read.sum", 0.0) + f.get("dram__bytes_write.sum", 0.0)
 json.dump(res, open(out, "w"), indent=1)
 print(json.dumps(res, indent=1))
