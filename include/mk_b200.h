@@ -159,6 +159,8 @@ typedef struct mk_stats {
   double device_ms;     /* CUDA-event time of the whole call on the engine stream */
   int64_t launches;     /* kernels launched by the call */
   int64_t steps;        /* warp search steps (boxes / steps = lanes busy per step) */
+  int64_t strategy;     /* 0 as the limits chose, 1 decided by the probe (roots straight
+                           to the persistent search), 2 probe then pre-split + search */
 } mk_stats;
 
 typedef struct mk_ctx mk_ctx;

@@ -276,7 +276,7 @@ __device__ __forceinline__ MkProb view(const DevSet& D, int pid) {
                       D.terms);
 }
 
-__global__ void k_roots(DevSet D, int nprob, void* stack) {
+__global__ void k_roots(DevSet D, int nprob, void* stack, int keep_incumbents) {
   int pid = blockIdx.x * blockDim.x + threadIdx.x;
   if (pid >= nprob) return;
   const mk_problem p = D.probs[pid];
@@ -289,6 +289,8 @@ __global__ void k_roots(DevSet D, int nprob, void* stack) {
     hi[i] = D.var_hi[p.var_off + i];
   }
   D.inc[pid].lock = 0;
+  D.inc[pid].err = 0;
+  if (keep_incumbents) return;  // a model of a previous attempt stays a valid bound
   D.inc[pid].version = 0;
   D.inc[pid].has = 0;
   D.inc[pid].err = 0;
@@ -1030,7 +1032,8 @@ struct ClassRun {
 };
 
 static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* status,
-                   mk_i128* point, mk_stats* stats, std::chrono::steady_clock::time_point t0) {
+                   mk_i128* point, mk_stats* stats, std::chrono::steady_clock::time_point t0,
+                   bool keep_incumbents = false, bool* budget_out = nullptr) {
   mk_stats local_stats;
   std::memset(&local_stats, 0, sizeof(local_stats));
   const int nprob = ds->nprob;
@@ -1150,11 +1153,12 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     cls[c].ms = 0.0;
   }
   // pre-split until every unit of the larger persistent grid has a task
-  const long long presplit_target =
+  long long presplit_target =
       lim && lim->chunk < 0 ? 0
                             : (long long)(ctx->units[1] > ctx->units[0] ? ctx->units[1] : ctx->units[0]);
+  if (const char* e = getenv("MK_PRESPLIT_TARGET")) presplit_target = atoll(e);
 
-  k_roots<<<(nprob + 127) / 128, 128, 0, s>>>(D, nprob, stack);
+  k_roots<<<(nprob + 127) / 128, 128, 0, s>>>(D, nprob, stack, keep_incumbents ? 1 : 0);
   ++launches;
   CK(cudaGetLastError());
   long long top = nprob;
@@ -1471,6 +1475,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     if (inc[i].err || pend[i]) status[i] = MK_UNKNOWN;
     else status[i] = inc[i].has ? MK_SAT : MK_UNSAT;
   }
+  if (budget_out) *budget_out = budget_hit;
   local_stats.rounds = rounds + search_launches;
   local_stats.boxes = (int64_t)dst.boxes;
   local_stats.leaves = (int64_t)dst.leaves;
@@ -1490,6 +1495,64 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   local_stats.launches = launches;
   local_stats.steps = (int64_t)dst.steps;
   if (stats) *stats = local_stats;
+  return MK_OK;
+}
+
+// Search strategy: the pre-split (breadth rounds until every persistent unit
+// has a task) pays off on long searches -- one deep unsat core spread over
+// the whole grid -- but costs host round trips and explores subtrees an
+// early model would prune on short ones.  Unless the caller chose (chunk !=
+// 0), a short probe runs first with the roots handed straight to the
+// persistent search; if it decides every problem inside its budget that is
+// the answer (exact either way: the strategy changes the order, not the
+// optimum), otherwise the full strategy runs from scratch.
+static int run_adaptive(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* status,
+                        mk_i128* point, mk_stats* stats, std::chrono::steady_clock::time_point t0) {
+  if ((lim && lim->chunk != 0) || getenv("MK_NO_PROBE"))
+    return run_set(ctx, ds, lim, status, point, stats, t0);
+  // a probe step must check its deadline often: small leaves (a warp
+  // enumerates at most 32 leaves per step)
+  double probe_s = 0.001;
+  if (const char* e = getenv("MK_PROBE_MS")) probe_s = atof(e) / 1e3;
+  long long probe_leaf = 512;
+  if (const char* e = getenv("MK_PROBE_LEAF")) probe_leaf = atoll(e);
+  mk_limits probe;
+  std::memset(&probe, 0, sizeof(probe));
+  if (lim) probe = *lim;
+  const double max_s = lim && lim->max_seconds > 0 ? lim->max_seconds : 30.0;
+  probe.chunk = -1;
+  probe.max_seconds = probe_s < max_s ? probe_s : max_s;
+  if (!(lim && lim->leaf_volume > 0)) probe.leaf_volume = probe_leaf;
+  mk_stats s1, s2;
+  bool hit = false;
+  int rc = run_set(ctx, ds, &probe, status, point, &s1, t0, false, &hit);
+  bool undecided = false;
+  for (int i = 0; i < ds->nprob; ++i) undecided |= status[i] == MK_UNKNOWN;
+  if (rc || (!hit && !undecided) || probe.max_seconds >= max_s) {
+    s1.strategy = 1;
+    if (stats) *stats = s1;
+    return rc;
+  }
+  // a fresh full run: its search order (first-fail splits before any model)
+  // is the one the long searches are tuned for
+  rc = run_set(ctx, ds, lim, status, point, &s2, t0, false, nullptr);
+  if (rc) return rc;
+  if (stats) {
+    s2.rounds += s1.rounds;
+    s2.boxes += s1.boxes;
+    s2.leaves += s1.leaves;
+    s2.points += s1.points;
+    s2.covered += s1.covered;
+    s2.bb_ms += s1.bb_ms;
+    s2.leaf_ms += s1.leaf_ms;
+    s2.insns_bb += s1.insns_bb;
+    s2.insns_leaf += s1.insns_leaf;
+    s2.device_ms += s1.device_ms;
+    s2.launches += s1.launches;
+    s2.steps += s1.steps;
+    s2.strategy = 2;
+    *stats = s2;
+  }
   return MK_OK;
 }
 
@@ -1525,7 +1588,7 @@ extern "C" int mk_set_eval(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32
     if (stats) std::memset(stats, 0, sizeof(*stats));
     return MK_OK;
   }
-  return run_set(ctx, ds, lim, status, point, stats, t0);
+  return run_adaptive(ctx, ds, lim, status, point, stats, t0);
 }
 
 extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_limits* lim,
@@ -1540,7 +1603,7 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   // one-shot: the context's scratch set is reused across calls
   int rc = upload_set(ctx, set, &ctx->scratch);
   if (rc) return rc;
-  return run_set(ctx, &ctx->scratch, lim, status, point, stats, t0);
+  return run_adaptive(ctx, &ctx->scratch, lim, status, point, stats, t0);
 }
 
 #include "mk_race.cuh"

@@ -73,7 +73,7 @@ class Stats(ctypes.Structure):
                 ("bb_ms", ctypes.c_double), ("leaf_ms", ctypes.c_double),
                 ("insns_bb", ctypes.c_int64), ("insns_leaf", ctypes.c_int64),
                 ("device_ms", ctypes.c_double), ("launches", ctypes.c_int64),
-                ("steps", ctypes.c_int64)]
+                ("steps", ctypes.c_int64), ("strategy", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
