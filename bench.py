@@ -48,6 +48,8 @@ CONFIG_NAMES = {
     "racy": "race probe (shared + global stores)",
     "paged_attention_v1": "vLLM paged_attention_v1, Mistral-7B (32/8 heads, head 128, block 16), "
                           "symbolic seq_len and block-table contents",
+    "paged_attention_v2": "vLLM paged_attention_v2 (512-token partitions), Mistral-7B (32/8 heads, "
+                          "head 128, block 16), symbolic seq_len and block-table contents",
     "moe_align_mixtral": "fused-MoE moe_align_block_size, Mixtral-8x7B (8 experts, top-2)",
     "topk_softmax": "fused-MoE topk_softmax, Mixtral-8x7B (8 experts, top-2)",
 }
