@@ -585,6 +585,17 @@ def _form_key(terms: Dict[object, int]) -> Tuple[Tuple, int]:
     return key, f
 
 
+def _replace_node(e: Node, old: Node, new: Node) -> Node:
+    """Every occurrence of the subtree ``old`` in ``e`` replaced by ``new``."""
+    if e == old:
+        return new
+    kids = ir.children(e)
+    if not kids:
+        return e
+    repl = tuple(_replace_node(c, old, new) for c in kids)
+    return e if repl == kids else ir.rebuild(e, repl)
+
+
 # -- presolve ----------------------------------------------------------------------------
 
 class _Presolve:
@@ -786,6 +797,9 @@ class _Presolve:
         # 5. lattice substitution for emod(.., c) == r
         if self._try_lattice(lin):
             return True
+        # 5b. quotient variables for divisions by positive constants
+        if self._try_quotient(lin):
+            return True
         # 6. gcd aggregation of wide terms
         if self._try_aggregate(lin):
             return True
@@ -881,6 +895,55 @@ class _Presolve:
             del self.atoms[idx]
             self._eliminate(v, expr)
             return True
+        return False
+
+    def _try_quotient(self, lin: _Lin) -> bool:
+        """Quotient variable for a division by a positive constant whose
+        dividend is linear and non-negative on the whole box (so truncation
+        is the floor): q = e / d  <=>  d*q <= e <= d*q + d - 1, the rows the
+        reference's own rewrite_divs introduces (solver/linear.py:130-306).
+        Every occurrence of the quotient becomes q, so atoms that compared
+        through it become linear rows the device's contraction (FBBT) can
+        use.  q is a function of e's symbols; placed after every symbol in
+        the witness order it changes neither the model set over the query's
+        symbols nor its lexicographic optimum, and it is not a witness
+        symbol.  Division by a positive constant cannot raise."""
+        if self.kcount > 64:
+            return False
+        ivl = _Ivl(self.bounds)
+        seen: Set[Node] = set()
+        for a in self.atoms:
+            if a[0] != "p":
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None:
+                continue
+            for k in lf[0]:
+                if isinstance(k, str) or k in seen:
+                    continue
+                seen.add(k)
+                if k[0] != "b" or k[1] != "div" or k[3][0] != "c" or not isinstance(k[3][1], int) \
+                        or k[3][1] < 2:
+                    continue
+                d, e = k[3][1], k[2]
+                ef = lin.lin(e)
+                if not ef[0] or any(not isinstance(t, str) for t in ef[0]):
+                    continue
+                lo, hi = ivl(e)
+                if lo is None or hi is None or lo < 0:
+                    continue
+                qname = f"{min(ef[0], key=_term_sort_key)}#q{self.kcount}"
+                self.kcount += 1
+                self.widths[qname] = "i64"
+                self.pos[qname] = max(self.pos.values()) + 1.0
+                self.maximize[qname] = False
+                self.bounds[qname] = (lo // d, hi // d)
+                q = ("s", qname, "i64")
+                self.atoms = [_replace_node(x, k, q) for x in self.atoms]
+                dq = ("b", "mul", ("c", d, "i64"), q, "i64")
+                self.atoms.append(("p", "le", dq, e))
+                self.atoms.append(("p", "le", e, ("b", "add", dq, ("c", d - 1, "i64"), "i64")))
+                return True
         return False
 
     def _try_aggregate(self, lin: _Lin) -> bool:
