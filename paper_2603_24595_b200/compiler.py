@@ -791,6 +791,10 @@ class _Presolve:
             return True
         if changed:
             return True
+        # 3b. mixed-radix split with a symbolic radix (before elimination
+        # rewrites the digit equality into bounds)
+        if self._try_radix(lin):
+            return True
         # 4. unit-coefficient equality elimination (order preserving)
         if self._try_eliminate(lin):
             return True
@@ -944,6 +948,89 @@ class _Presolve:
                 self.atoms.append(("p", "le", dq, e))
                 self.atoms.append(("p", "le", e, ("b", "add", dq, ("c", d - 1, "i64"), "i64")))
                 return True
+        return False
+
+    def _nonneg(self, x: str) -> bool:
+        lo = self.bounds.get(x, (None, None))[0]
+        return lo is not None and lo >= 0
+
+    def _below(self, lin: _Lin, u: str, pname: str) -> bool:
+        """Some atom states u <= P - k with k >= 1."""
+        for a in self.atoms:
+            if a[0] != "p" or a[1] != "le":
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is not None and lf[0] == {u: 1, pname: -1} and lf[1] >= 1:
+                return True
+        return False
+
+    def _try_radix(self, lin: _Lin) -> bool:
+        """``c*P*X1 - c*P*X2 + R = 0`` with P a symbol >= 1 and R provably
+        inside (-|c|*P, |c|*P): then P*(X1 - X2) is a multiple of P strictly
+        inside (-P, P), so X1 = X2 and R = 0 (exact for integers).  R may hold
+        one digit pair c_s*(u - w) with 0 <= u, w <= P - 1 (atoms), |c_s| <=
+        |c|, plus terms of constant range K < |c_s| (or K < |c|*P_lo without
+        a pair).  This is the injectivity of a mixed-radix index with a
+        launch-dependent radix (``((seq * heads + head) * gridDim.z +
+        blockIdx.z) * 128 + tid``), which a race twin query's offset
+        equality hinges on; interval search cannot see it."""
+        for idx, a in enumerate(self.atoms):
+            if a[0] != "p" or a[1] != "eq":
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None:
+                continue
+            terms, c0 = lf
+            muls = [(k, v) for k, v in terms.items()
+                    if not isinstance(k, str) and k[0] == "b" and k[1] == "mul"]
+            if len(muls) != 2:
+                continue
+            (t1, c1), (t2, c2) = muls
+            if c1 != -c2:
+                continue
+            common = [f for f in (t1[2], t1[3]) if f[0] == "s" and f in (t2[2], t2[3])]
+            if len(common) != 1:
+                continue
+            P = common[0]
+            pname = P[1]
+            plo = self.bounds.get(pname, (None, None))[0]
+            if plo is None or plo < 1:
+                continue
+            x1 = t1[2] if t1[3] == P else t1[3]
+            x2 = t2[2] if t2[3] == P else t2[3]
+            rest = {k: v for k, v in terms.items() if k not in (t1, t2)}
+            if any(not isinstance(k, str) for k in rest):
+                continue
+            # one digit pair below the radix
+            pair = None
+            for u, cu in rest.items():
+                for w, cw in rest.items():
+                    if u < w and cu == -cw and pair is None \
+                            and all(self._nonneg(x) for x in (u, w)) \
+                            and self._below(lin, u, pname) and self._below(lin, w, pname):
+                        pair = (u, w, abs(cu))
+            others = {k: v for k, v in rest.items() if pair is None or k not in pair[:2]}
+            lo = hi = c0
+            ok = True
+            for k, v in others.items():
+                b = self.bounds.get(k, (None, None))
+                if b[0] is None or b[1] is None:
+                    ok = False
+                    break
+                lo += min(v * b[0], v * b[1])
+                hi += max(v * b[0], v * b[1])
+            if not ok:
+                continue
+            K = max(abs(lo), abs(hi))
+            if pair is not None:
+                if not (pair[2] <= abs(c1) and K < pair[2]):
+                    continue
+            elif not K < abs(c1) * plo:
+                continue
+            del self.atoms[idx]
+            self.atoms.append(("p", "eq", x1, x2))
+            self.atoms.append(("p", "eq", lin_to_ir((rest, c0), self.widths), ("c", 0, "i64")))
+            return True
         return False
 
     def _try_aggregate(self, lin: _Lin) -> bool:
