@@ -214,6 +214,11 @@ typedef struct mk_race_prog {
                            instance of the leading vars is one access iff
                            SOME value of them satisfies the path */
   int32_t pad;
+  uint64_t begin, end;  /* instance range [begin, end) of this call (a shard of
+                           the launch across GPUs); end == 0: every instance.
+                           A range is decided by the fused ordered pass only:
+                           `sorted` = 0 in the result when its keys are not in
+                           order (the caller then sweeps the whole launch) */
 } mk_race_prog;
 
 typedef struct mk_race_result {
@@ -229,7 +234,14 @@ typedef struct mk_race_result {
   int32_t jit;          /* 1: generator specialised at run time (NVRTC), 0: interpreted */
   int32_t sorted;       /* 1: the keys arrived in order and the sort was skipped */
   int32_t fused;        /* 1: decided by the fused ordered pass (no tuples in HBM) */
-  int32_t reserved;
+  int32_t have;         /* range calls: the range holds at least one access */
+  /* range calls: first and last access of the range in instance order (key,
+     thread identity, instance index), for the exact combination of shards:
+     adjacent shards conflict when last.key == next first.key with distinct
+     identities (the boundary pair) */
+  uint64_t first_key, first_id, first_idx, last_key, last_id, last_idx;
+  int64_t off_lo;       /* key -> byte offset: key / nblocks + off_lo */
+  uint64_t nblocks;
 } mk_race_result;
 
 int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out);

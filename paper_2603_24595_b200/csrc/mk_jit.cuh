@@ -286,11 +286,12 @@ inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
   // instance indices need no shuffle; the hot loop moves only keys (ballot +
   // two shuffles), identities are computed only on the rare equal-key steps.
   s << "extern \"C\" __global__ void __launch_bounds__(256) mk_race_fused_jit(unsigned long long vol, "
-       "unsigned long long chunk, i64 off_lo_unused, unsigned long long nblocks_unused, u64* rec, u64* ctr) {\n"
+       "unsigned long long chunk, unsigned long long start, unsigned long long nblocks_unused, u64* rec,"
+       " u64* ctr) {\n"
        "  const unsigned lane = threadIdx.x & 31;\n"
        "  const unsigned long long warp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;\n"
-       "  const unsigned long long base = warp * chunk;\n"
-       "  unsigned long long end = base + chunk; if (end > vol) end = vol;\n"
+       "  const unsigned long long base = start + warp * chunk;\n"
+       "  unsigned long long end = base + chunk; if (end > start + vol) end = start + vol;\n"
        "  const unsigned uend = (unsigned)(end < base ? base : end);\n"
        "  const unsigned lt = (1u << lane) - 1u;\n"
     << odometer_init("(base + lane)", "32ull", 32)

@@ -202,6 +202,33 @@ __global__ void __launch_bounds__(1024) k_race_bound(const unsigned long long* r
   int prev = -1;
   Scan(tmp).ExclusiveScan(last, prev, -1, MaxInt());
   const int prev0 = prev;
+  // the range's first and last access (shard combination across GPUs)
+  __shared__ int s_first, s_last;
+  if (threadIdx.x == 0) {
+    s_first = 0x7fffffff;
+    s_last = -1;
+  }
+  __syncthreads();
+  if (last >= 0) {
+    atomicMax(&s_last, last);
+    for (int w = b; w < e; ++w)
+      if (rec[(size_t)w * MK_RACE_REC]) {
+        atomicMin(&s_first, w);
+        break;
+      }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_last >= 0) {
+    const unsigned long long* f = rec + (size_t)s_first * MK_RACE_REC;
+    const unsigned long long* l = rec + (size_t)s_last * MK_RACE_REC;
+    ctr[6] = f[1];
+    ctr[7] = f[2];
+    ctr[8] = f[3];
+    ctr[9] = l[4];
+    ctr[10] = l[5];
+    ctr[11] = l[6];
+    ctr[12] = 1;
+  }
   unsigned long long conf = 0, best = ~0ull;
   bool down = false;
   for (int w = b; w < e; ++w) {
@@ -345,35 +372,58 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   // coalesced store), the stable sort is the identity and the adjacent-pair
   // scan of the sorted tuples is exactly what the pass computes in registers;
   // otherwise its result is discarded and the sort path below runs.
-  if (jk && !getenv("MK_RACE_NO_FAST") && !getenv("MK_RACE_FORCE_SORT")) {
+  const bool ranged = prog->end > 0;
+  const unsigned long long r_begin = ranged ? prog->begin : 0ull;
+  const unsigned long long r_count = ranged ? (prog->end > prog->begin ? prog->end - prog->begin : 0ull)
+                                            : vol;
+  out->off_lo = R.off_lo;
+  out->nblocks = R.nblocks;
+  if (ranged && !jk) {
+    // a shard is decided by the fused pass only; without it the caller
+    // sweeps the whole launch
+    out->sorted = 0;
+    return MK_OK;
+  }
+  if (jk && (ranged || (!getenv("MK_RACE_NO_FAST") && !getenv("MK_RACE_FORCE_SORT")))) {
     cudaKernel_t fk = mkjit::get_kernel(ctx->jit, src, ctx->device, "mk_race_fused_jit");
     if (fk) {
       const int fgrid = ctx->sms * 8;
       const unsigned long long warps = (unsigned long long)fgrid * (RACE_THREADS / 32);
-      unsigned long long chunk = (vol + warps - 1) / warps;
+      unsigned long long chunk = (r_count + warps - 1) / warps;
       chunk = (chunk + 31) / 32 * 32;
       if (chunk < 32) chunk = 32;
       const size_t rbytes = sizeof(unsigned long long) * MK_RACE_REC * warps;
       int rc0 = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, rbytes);
       if (rc0) return rc0;
       unsigned long long* rec = static_cast<unsigned long long*>(ctx->d_work);
-      unsigned long long init[6] = {0ull, 0ull, ~0ull, 0ull, 0ull, 0ull};
+      unsigned long long init[13] = {0ull, 0ull, ~0ull, 0ull, 0ull, 0ull, 0ull,
+                                     0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
       CK(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, s));
       CK(cudaEventRecord(ctx->ev[0], s));
-      unsigned long long a_vol = vol, a_chunk = chunk, a_nb = R.nblocks;
-      long long a_off = R.off_lo;
+      unsigned long long a_vol = r_count, a_chunk = chunk, a_nb = R.nblocks, a_start = r_begin;
       unsigned long long* a_rec = rec;
       unsigned long long* a_ctr = ctr;
-      void* fargs[] = {&a_vol, &a_chunk, &a_off, &a_nb, &a_rec, &a_ctr};
+      void* fargs[] = {&a_vol, &a_chunk, &a_start, &a_nb, &a_rec, &a_ctr};
       CK(cudaLaunchKernel((const void*)fk, dim3(fgrid), dim3(RACE_THREADS), fargs, 0, s));
       CK(cudaEventRecord(ctx->ev[1], s));
       k_race_bound<<<1, 1024, 0, s>>>(rec, (int)warps, ctr);
       CK(cudaGetLastError());
       CK(cudaEventRecord(ctx->ev[2], s));
-      unsigned long long h[6];
+      unsigned long long h[13];
       CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
       CK(cudaEventRecord(ctx->ev[3], s));
       CK(cudaStreamSynchronize(s));
+      out->have = h[12] ? 1 : 0;
+      out->first_key = h[6];
+      out->first_id = h[7];
+      out->first_idx = h[8];
+      out->last_key = h[9];
+      out->last_id = h[10];
+      out->last_idx = h[11];
+      if (ranged && h[4]) {
+        out->sorted = 0;   // out of order: the caller sweeps the whole launch
+        return MK_OK;
+      }
       if (!h[4]) {
         out->fused = 1;
         out->sorted = 1;
@@ -399,6 +449,10 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
       // out of order: reset the counters for the sort path
       CK(cudaMemcpyAsync(ctr, init, sizeof(init), cudaMemcpyHostToDevice, s));
     }
+  }
+  if (ranged) {
+    out->sorted = 0;   // no specialised fused pass: the caller sweeps the whole launch
+    return MK_OK;
   }
   CK(cudaEventRecord(ctx->ev[0], s));
   if (jk) {

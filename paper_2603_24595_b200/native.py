@@ -82,7 +82,7 @@ class Stats(ctypes.Structure):
 class RaceProg(ctypes.Structure):
     _fields_ = [("set", ProblemSet), ("off_reg", ctypes.c_int32), ("shared", ctypes.c_int32),
                 ("id_var", ctypes.c_int32 * 6), ("n_exist", ctypes.c_int32),
-                ("pad", ctypes.c_int32)]
+                ("pad", ctypes.c_int32), ("begin", ctypes.c_uint64), ("end", ctypes.c_uint64)]
 
 
 class RaceResult(ctypes.Structure):
@@ -93,7 +93,11 @@ class RaceResult(ctypes.Structure):
                 ("gen_ms", ctypes.c_double), ("sort_ms", ctypes.c_double),
                 ("scan_ms", ctypes.c_double), ("hbm_bytes", ctypes.c_uint64),
                 ("jit", ctypes.c_int32), ("sorted", ctypes.c_int32),
-                ("fused", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("fused", ctypes.c_int32), ("have", ctypes.c_int32),
+                ("first_key", ctypes.c_uint64), ("first_id", ctypes.c_uint64),
+                ("first_idx", ctypes.c_uint64), ("last_key", ctypes.c_uint64),
+                ("last_id", ctypes.c_uint64), ("last_idx", ctypes.c_uint64),
+                ("off_lo", ctypes.c_int64), ("nblocks", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -127,7 +131,7 @@ class AccessResult(ctypes.Structure):
 
 
 assert ctypes.sizeof(AccessProg) == 120 and ctypes.sizeof(AccessResult) == 80
-assert ctypes.sizeof(RaceProg) == 144 and ctypes.sizeof(RaceResult) == 104
+assert ctypes.sizeof(RaceProg) == 160 and ctypes.sizeof(RaceResult) == 168
 
 
 def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
@@ -319,11 +323,14 @@ class Engine:
 
     # -- race sweep (K2) -----------------------------------------------------------
 
-    def race_sweep(self, prog) -> dict:
+    def race_sweep(self, prog, begin: int = 0, end: int = 0) -> dict:
         """Concrete race replay of one store at one launch
-        (paper_2603_24595_b200.race.RaceProgram -> mk_race_sweep)."""
+        (paper_2603_24595_b200.race.RaceProgram -> mk_race_sweep); with
+        ``end`` > 0 only instances [begin, end) (a shard of the launch)."""
         packed = PackedSet([prog.problem])
         rp = RaceProg()
+        rp.begin = int(begin)
+        rp.end = int(end)
         rp.set = packed.struct
         rp.off_reg = prog.off_reg
         rp.shared = 1 if prog.shared else 0

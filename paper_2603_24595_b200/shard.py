@@ -211,3 +211,75 @@ def check_slabbed(checker: SiteChecker, queries: Sequence[Query], group=None,
         status, witness = cq.assemble(results[off:off + len(cq.problems)])
         out.append(QueryResult(status, witness))
     return out
+
+
+# -- K2 race sweep across GPUs ------------------------------------------------------------
+
+def shard_range(total: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous instance range of one rank (instance order = key order for
+    the fused pass, so shards meet at one boundary pair each)."""
+    return total * rank // world, total * (rank + 1) // world
+
+
+def combine_race_shards(parts: Sequence[dict]) -> Optional[dict]:
+    """Exact combination of ranged sweeps in rank order: conflicts inside
+    each shard plus one boundary pair per pair of adjacent non-empty shards
+    (the last access of one and the first of the next: equal key, distinct
+    identity); the first conflict is the least (idx_b << 32 | idx_a).  None
+    when a shard or a boundary is out of key order (the fused pass does not
+    apply: the launch is swept whole)."""
+    if any(not p["sorted"] for p in parts):
+        return None
+    out = {"instances": sum(p["instances"] for p in parts),
+           "tuples": sum(p["tuples"] for p in parts),
+           "conflicts": sum(p["conflicts"] for p in parts), "sorted": 1, "fused": 1}
+    cands = [((p["idx_b"] << 32) | p["idx_a"], p["offset"]) for p in parts if p["has_race"]]
+    prev = None
+    for p in parts:
+        if not p["have"]:
+            continue
+        if prev is not None:
+            if p["first_key"] < prev["last_key"]:
+                return None
+            if p["first_key"] == prev["last_key"] and p["first_id"] != prev["last_id"]:
+                out["conflicts"] += 1
+                cands.append(((p["first_idx"] << 32) | prev["last_idx"],
+                              p["first_key"] // p["nblocks"] + p["off_lo"]))
+        prev = p
+    out["has_race"] = int(out["conflicts"] > 0)
+    if cands:
+        c, off = min(cands)
+        out["idx_b"], out["idx_a"], out["offset"] = c >> 32, c & 0xffffffff, off
+    else:
+        out["idx_a"] = out["idx_b"] = out["offset"] = 0
+    return out
+
+
+def race_sweep_sharded(engine, prog, group=None) -> dict:
+    """K2 over every rank: rank r sweeps its contiguous
+    instance range with the fused ordered pass; one all_gather_object of the
+    per-shard summaries (a few hundred bytes) and the exact combination give
+    every rank the result the single-GPU sweep returns.  If any shard's keys
+    (or a shard boundary) are out of order, rank 0 sweeps the whole launch
+    (radix-sort path) and broadcasts its result."""
+    rank, world = _world(group)
+    keys = ("instances", "tuples", "conflicts", "has_race", "idx_a", "idx_b", "offset", "sorted")
+    if world == 1:
+        return engine.race_sweep(prog)
+    dist = _dist()
+    b, e = shard_range(prog.instances, rank, world)
+    mine = engine.race_sweep(prog, b, e) if e > b else \
+        {"sorted": 1, "have": 0, "instances": 0, "tuples": 0, "conflicts": 0, "has_race": 0}
+    mine = {k: v for k, v in mine.items() if k != "pair"}
+    parts: List[dict] = [None] * world  # type: ignore[list-item]
+    dist.all_gather_object(parts, mine, group=group)
+    got = combine_race_shards(parts)
+    if got is None:
+        box = [engine.race_sweep(prog) if rank == 0 else None]
+        if box[0] is not None:
+            box[0] = {k: box[0][k] for k in keys}
+        dist.broadcast_object_list(box, src=0, group=group)
+        got = box[0]
+    if got["has_race"]:
+        got["pair"] = (prog.decode(got["idx_a"]), prog.decode(got["idx_b"]))
+    return got

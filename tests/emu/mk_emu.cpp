@@ -208,8 +208,105 @@ extern "C" int mk_set_free(mk_ctx* ctx, mk_dset* d) {
 #include <algorithm>
 #include <utility>
 
+// ranged call (a shard of the launch): the fused ordered pass's semantics --
+// accesses in instance order, keys must be non-decreasing, adjacent equal keys
+// with distinct identities conflict; first / last access reported for the
+// combination of shards.  Keys and identities as the device computes them.
+static int race_range(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out) {
+  const mk_problem_set& set = prog->set;
+  const mk_problem& p = set.probs[0];
+  MkProb P = mk_prob_view(set.probs, 0, set.insns, set.consts, set.atom_regs, set.atom_masks,
+                          set.rows, set.row_terms);
+  const int nv = p.nvars, n_outer = nv - prog->n_exist;
+  std::vector<int64_t> lo(nv), hi(nv);
+  unsigned long long inner = 1;
+  for (int i = 0; i < nv; ++i) {
+    lo[i] = (int64_t)set.var_lo[p.var_off + i].lo;
+    hi[i] = (int64_t)set.var_hi[p.var_off + i].lo;
+    if (i >= n_outer) inner *= (unsigned long long)(hi[i] - lo[i] + 1);
+  }
+  // key origin: the root box's offset interval (mk_race_sweep's k_race_root)
+  std::vector<MkIvT<int64_t>> Rg(MK_MAXR);
+  int64_t cnt0 = 0;
+  mk_eval_box<int64_t>(P, lo.data(), hi.data(), Rg.data(), &cnt0);
+  const int64_t off_lo = Rg[prog->off_reg].lo;
+  unsigned long long nblocks = 1;
+  for (int a = 0; a < 3; ++a)
+    if (prog->shared && prog->id_var[a] >= 0)
+      nblocks *= (unsigned long long)(hi[prog->id_var[a]] - lo[prog->id_var[a]] + 1);
+  out->off_lo = off_lo;
+  out->nblocks = nblocks;
+  out->sorted = 1;
+  out->fused = 1;
+  std::vector<MkCvT<int64_t>> R(MK_MAXR);
+  int64_t x[MK_MAXV];
+  bool have = false;
+  unsigned long long pk = 0, pid = 0, pidx = 0, best = ~0ull, bkey = 0;
+  for (unsigned long long idx = prog->begin; idx < prog->end; ++idx) {
+    bool hit = false;
+    for (unsigned long long j = 0; j < inner && !hit; ++j) {
+      mk_decode(lo.data(), hi.data(), nv, 0ull, idx * inner + j, x);
+      bool ovf = false;
+      int64_t cnt = 0;
+      out->instances++;
+      hit = mk_eval_point(P, x, R.data(), &ovf, &cnt);
+    }
+    if (!hit) continue;
+    unsigned long long bk = 0;
+    if (prog->shared)
+      for (int a = 2; a >= 0; --a) {
+        const int v = prog->id_var[a];
+        if (v < 0) continue;
+        bk = bk * (unsigned long long)(hi[v] - lo[v] + 1) + (unsigned long long)(x[v] - lo[v]);
+      }
+    const unsigned long long key = (unsigned long long)(R[prog->off_reg].v - off_lo) * nblocks + bk;
+    unsigned long long idk = 0;
+    for (int a = prog->shared ? 3 : 0; a < 6; ++a) {
+      const int v = prog->id_var[a];
+      if (v < 0) continue;
+      idk = idk * (unsigned long long)(hi[v] - lo[v] + 1) + (unsigned long long)(x[v] - lo[v]);
+    }
+    out->tuples++;
+    if (have) {
+      if (key < pk) {
+        out->sorted = 0;
+        return MK_OK;
+      }
+      if (key == pk && idk != pid) {
+        out->conflicts++;
+        const unsigned long long c = (idx << 32) | pidx;
+        if (c < best) {
+          best = c;
+          bkey = key;
+        }
+      }
+    } else {
+      out->first_key = key;
+      out->first_id = idk;
+      out->first_idx = idx;
+    }
+    have = true;
+    pk = key;
+    pid = idk;
+    pidx = idx;
+  }
+  out->have = have ? 1 : 0;
+  out->last_key = pk;
+  out->last_id = pid;
+  out->last_idx = pidx;
+  out->has_race = out->conflicts > 0;
+  if (out->has_race) {
+    out->idx_b = best >> 32;
+    out->idx_a = best & 0xffffffffull;
+    out->offset = (int64_t)(bkey / nblocks) + off_lo;
+  }
+  (void)ctx;
+  return MK_OK;
+}
+
 extern "C" int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out) {
   std::memset(out, 0, sizeof(*out));
+  if (prog->end > 0) return race_range(ctx, prog, out);
   const mk_problem_set& set = prog->set;
   if (set.nprob != 1) {
     ctx->err = "race sweep takes exactly one problem";

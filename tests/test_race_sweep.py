@@ -186,3 +186,36 @@ def test_device_sweep_paths_agree():
     assert seen_sorted == {True, False}
     assert seen_fused_race
     eng.close()
+
+
+@pytest.mark.gpu
+def test_device_shards_combine_to_the_whole_sweep():
+    """K2 across GPUs, one device: the launch cut into 2, 3 and 8 contiguous
+    instance ranges (what race_sweep_sharded gives each rank), each decided by
+    the fused pass, combined exactly (shard.combine_race_shards) equals the
+    whole-launch sweep; out-of-order shards report unsorted."""
+    from paper_2603_24595_b200 import shard
+    from paper_2603_24595_b200.native import Engine
+
+    eng = Engine(0)
+    keys = ("tuples", "conflicts", "has_race", "idx_a", "idx_b", "offset")
+    combined = 0
+    try:
+        for name, i, launch, expect, prog in _cases():
+            whole = eng.race_sweep(prog)
+            for world in (2, 3, 8):
+                parts = [eng.race_sweep(prog, *shard.shard_range(prog.instances, r, world))
+                         if shard.shard_range(prog.instances, r, world)[1] >
+                         shard.shard_range(prog.instances, r, world)[0] else
+                         {"sorted": 1, "have": 0, "instances": 0, "tuples": 0, "conflicts": 0,
+                          "has_race": 0}
+                         for r in range(world)]
+                got = shard.combine_race_shards(parts)
+                if got is None:
+                    assert not whole["sorted"], (name, i, world)
+                    continue
+                combined += 1
+                assert [got[k] for k in keys] == [whole[k] for k in keys], (name, i, world)
+    finally:
+        eng.close()
+    assert combined > 0

@@ -120,3 +120,80 @@ def test_record_round_trip_128_bit():
     vals = [-(1 << 100) - 3, (1 << 64) + 5, -1]
     rec = _encode([p, p], [("sat", vals), ("unknown", None)])
     assert _decode([p, p], rec) == [("sat", vals), ("unknown", None)]
+
+
+def _race_worker(rank, world, port, out_dir):
+    import json
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    from paper_2603_24595_b200 import shard
+    from paper_2603_24595_b200.native import Engine
+    from test_race_sweep import _cases
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    eng = Engine(0, EMU)
+    try:
+        rows = []
+        for name, i, launch, expect, prog in _cases():
+            if prog.instances > 400_000:
+                continue
+            got = shard.race_sweep_sharded(eng, prog)
+            rows.append([name, i] + [int(got[k]) for k in
+                                      ("tuples", "conflicts", "has_race", "idx_a", "idx_b", "offset")])
+        with open(os.path.join(out_dir, f"race{rank}.json"), "w") as fh:
+            json.dump(rows, fh)
+    finally:
+        eng.close()
+        dist.destroy_process_group()
+
+
+def test_race_sweep_sharded_equals_single(tmp_path):
+    """K2 across ranks (gloo, world 3, host emulation): every store site's
+    sharded sweep equals the single-rank sweep (tuples, conflicts, verdict,
+    first pair, offset) on every rank, whether the shards combine in the
+    fused form or fall back to the whole-launch sweep."""
+    import json
+
+    import torch.multiprocessing as mp
+
+    from paper_2603_24595_b200.native import Engine
+    from test_race_sweep import _cases
+
+    world = 3
+    port = _free_port()
+    mp.spawn(_race_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    outs = [json.load(open(os.path.join(tmp_path, f"race{r}.json"))) for r in range(world)]
+    assert outs[0] == outs[1] == outs[2] and outs[0]
+    eng = Engine(0, EMU)
+    try:
+        want = {}
+        for name, i, launch, expect, prog in _cases():
+            if prog.instances > 400_000:
+                continue
+            got = eng.race_sweep(prog)
+            want[(name, i)] = [int(got[k]) for k in
+                               ("tuples", "conflicts", "has_race", "idx_a", "idx_b", "offset")]
+    finally:
+        eng.close()
+    for row in outs[0]:
+        assert row[2:] == want[(row[0], row[1])], row
+    assert any(row[4] for row in outs[0])      # racy sites among them
+
+
+def test_combine_detects_boundary_conflict():
+    from paper_2603_24595_b200 import shard
+
+    base = {"sorted": 1, "instances": 4, "tuples": 4, "conflicts": 0, "has_race": 0,
+            "idx_a": 0, "idx_b": 0, "offset": 0, "off_lo": 0, "nblocks": 1, "have": 1}
+    a = dict(base, first_key=1, first_id=0, first_idx=0, last_key=5, last_id=3, last_idx=3)
+    b = dict(base, first_key=5, first_id=4, first_idx=4, last_key=9, last_id=7, last_idx=7)
+    got = shard.combine_race_shards([a, b])
+    assert got["conflicts"] == 1 and got["has_race"] and (got["idx_a"], got["idx_b"]) == (3, 4)
+    c = dict(b, first_key=4)
+    assert shard.combine_race_shards([a, c]) is None       # out of order across the boundary
+    d = dict(b, first_id=3)
+    assert shard.combine_race_shards([a, d])["conflicts"] == 0   # same thread
