@@ -383,6 +383,46 @@ def _race_sweep_line(chk, args, peaks, src, int_peak):
                                        "peak_source": f"peaks file: {src}"}}}
 
 
+def _race_sharded_line(chk, args, world):
+    """K2 across the ranks (shard.race_sweep_sharded): config 1's output
+    store at the N=1 line's launch (num_tokens = --race-tokens; strong
+    scaling: a launch's instance indices are 32-bit, < 2^31), each rank a
+    contiguous instance range through the fused pass, one all_gather_object
+    of the shard summaries.  Time: max over ranks of the call (device pass +
+    combine)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_24595_b200 import race, shard
+
+    doc, queries = _load_workload("rms_norm")
+    T = args.race_tokens
+    launch = {"BS": 1, "SL": T, "TC": T, "blockDim.x": 1024, "blockDim.y": 1, "blockDim.z": 1,
+              "gridDim.x": T, "gridDim.y": 1, "gridDim.z": 1}
+    progs = [race.race_program(a, o, launch)
+             for s, (a, o) in zip(doc["sites"], queries)
+             if s["site"] == "store_site" and s["line"] == 20]
+    prog = max(progs, key=lambda p: p.instances)
+    for _ in range(2):
+        shard.race_sweep_sharded(chk.engine, prog)
+    times = []
+    for _ in range(3):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        got = shard.race_sweep_sharded(chk.engine, prog)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    t = torch.tensor([min(times)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) * 1e3
+    return {"workload": f"rms_norm output store at num_tokens={T} ({world} shards)",
+            "instances": prog.instances, "accesses": got["tuples"], "has_race": bool(got["has_race"]),
+            "ms": ms, "instances_per_s": prog.instances / (ms / 1e3), "scaling": "strong",
+            "what": "max over ranks of race_sweep_sharded (fused pass on the rank's range + "
+                    "all_gather_object of the shard summaries), wall clock around synchronized calls"}
+
+
 def _access_line(chk, args, peaks, src, int_peak):
     """K2 with the specification's oracle rule (paper_2603_24595_b200.replay,
     mk_access_sweep): every load and store the reference front end executes
@@ -600,6 +640,8 @@ def run_b200(args):
         ops = "bytecode instructions executed (no ncu calibration committed)"
 
     k2 = _race_sweep_line(chk, args, peaks, src, int_peak) if rank == 0 and args.race_tokens > 0 else None
+    k2_sharded = (_race_sharded_line(chk, args, world)
+                  if world > 1 and args.race_tokens > 0 else None)
     analyze = _analyze_line(chk, args, doc) if rank == 0 and world == 1 and args.analyze else None
     access = (_access_line(chk, args, peaks, src, int_peak)
               if rank == 0 and world == 1 and args.access_tokens > 0 else None)
@@ -661,6 +703,7 @@ def run_b200(args):
             "cpu_baseline": cpu,
             "k2_race_sweep": k2,
             "k2_access_replay": access,
+            "k2_race_sharded": k2_sharded,
             "time_to_verdict": analyze,
             "k1_heavy": heavy,
             "clocks": clk,
