@@ -518,9 +518,17 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: MK_BENCH_ONE_DEVICE runs every rank on cuda:0 over gloo, so
+    # the N>1 path can be exercised on a one-GPU box (never for numbers)
+    one = bool(os.environ.get("MK_BENCH_ONE_DEVICE"))
+    if one:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2603_24595_b200 import shard
     from paper_2603_24595_b200.engine import SiteChecker, compile_all
