@@ -493,6 +493,80 @@ def _path_bound(e: Node, neg: bool, cap: int) -> int:
     return 1
 
 
+class _NoCount(Exception):
+    pass
+
+
+def _live(e: Node, cap: int, simp: Dict[Node, Node]) -> int:
+    """Number of live paths boolean_paths' traversal completes for the one
+    conjunct ``e`` (simplify is context-free, so a dead alternative is dead
+    in every combination and counts multiply / add); saturates at cap + 2.
+    Forms the traversal would raise on, or integer if-then-else, are not
+    counted (_NoCount)."""
+    top = cap + 2
+    r = simp.get(e)
+    if r is None:
+        r = ir.simplify(e)
+        simp[e] = r
+    t = r[0]
+    if t == "c":
+        if r[2] != "bool":
+            raise _NoCount()
+        return 1 if r[1] else 0
+    if t == "s":
+        if r[2] != "bool":
+            raise _NoCount()
+        return 1
+    if t == "o":
+        if r[1] == "not":
+            try:
+                return _live(_negate(r[2][0]), cap, simp)
+            except GiveUp:
+                raise _NoCount()
+        if r[1] == "and":
+            acc = 1
+            for a in r[2]:
+                acc = min(top, acc * _live(a, cap, simp))
+                if acc == 0:
+                    return 0
+            return acc
+        acc = 0
+        for a in r[2]:
+            acc = min(top, acc + _live(a, cap, simp))
+        return acc
+    if t == "i":
+        try:
+            nc = _negate(r[1])
+        except GiveUp:
+            raise _NoCount()
+        a = min(top, _live(r[1], cap, simp) * _live(r[2], cap, simp))
+        b = min(top, _live(nc, cap, simp) * _live(r[3], cap, simp))
+        return min(top, a + b)
+    if t == "p":
+        if _find_int_ite(r) is not None:
+            raise _NoCount()
+        if r[1] == "ne":
+            return min(top, _live(("p", "gt", r[2], r[3]), cap, simp)
+                       + _live(("p", "lt", r[2], r[3]), cap, simp))
+        return 1
+    raise _NoCount()
+
+
+def live_paths(assertions: Sequence[Node], cap: int) -> Optional[int]:
+    """Exact number of paths boolean_paths completes (saturated at cap + 2),
+    or None when the traversal must run (forms it raises on, int ite)."""
+    simp: Dict[Node, Node] = {}
+    acc = 1
+    try:
+        for a in assertions:
+            acc = min(cap + 2, acc * _live(a, cap, simp))
+            if acc == 0:
+                return 0
+    except _NoCount:
+        return None
+    return acc
+
+
 def component_giveup(component: Sequence[Node], bounds: Dict[str, Interval],
                      max_paths: int = 512) -> Optional[str]:
     """The reason the reference gives up on this (simplified) component in
@@ -505,6 +579,13 @@ def component_giveup(component: Sequence[Node], bounds: Dict[str, Interval],
             if total > max_paths:
                 break
         if total > max_paths:
+            # at least cap + 2 live paths: the traversal's check
+            # len(work) + done > cap fires for certain (after the (cap+1)-th
+            # completed path a live one is still pending); otherwise (or when
+            # the count does not apply) the exact traversal decides
+            live = live_paths(rewritten, max_paths)
+            if live is not None and live >= max_paths + 2:
+                raise GiveUp(f"more than {max_paths} case splits")
             count_paths(rewritten, max_paths)   # exact traversal only when needed
     except GiveUp as g:
         return str(g)
