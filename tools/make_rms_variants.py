@@ -1,16 +1,19 @@
-"""Generate the rms_norm kernel x model corpus entries (BASELINE.json
-configs[4]): the config-1 port (workloads/rms_norm, Llama-2-7B hidden 4096)
+"""Generate the rms_norm / fused_add_rms_norm kernel x model corpus entries
+(BASELINE.json configs[4]): the config-1 port (workloads/rms_norm, Llama-2-7B
+hidden 4096) and the Fig. 2 port (workloads/fused_add_rms_norm, hidden 7168)
 under other models' hidden sizes -- the model-fixed tensor shapes of the
-inferred context (input / out row width, weight length) substituted.
-Hidden sizes are the public HF configs.  Goldens come from the reference:
-python oracle/gen_golden.py rms_norm_<model>."""
+inferred context (row width of the two activations, weight length)
+substituted.  Hidden sizes are the public HF configs; fused_add_rms_norm at
+8192 is SPEC.md's section 2.3 variant.  Goldens come from the reference:
+python oracle/gen_golden.py <base>_<model>.
+
+    python tools/make_rms_variants.py [rms_norm|fused_add_rms_norm]"""
 import copy
 import json
 import os
 import shutil
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-BASE = os.path.join(ROOT, "workloads", "rms_norm")
 
 MODELS = {
     "llama2_13b": 5120,
@@ -20,10 +23,19 @@ MODELS = {
     "deepseek_v3": 7168,
 }
 
+FUSED_MODELS = {
+    "llama3_8b": 4096,
+    "llama2_13b": 5120,
+    "llama3_70b": 8192,
+    "qwen2_7b": 3584,
+}
 
-def main():
+
+def main(base_name="rms_norm"):
+    BASE = os.path.join(ROOT, "workloads", base_name)
+    models = MODELS if base_name == "rms_norm" else FUSED_MODELS
     ctx = json.load(open(os.path.join(BASE, "ctx.json")))
-    for name, hidden in MODELS.items():
+    for name, hidden in models.items():
         c = copy.deepcopy(ctx)
         for a in c["args"]:
             for k in a.get("constraints", []):
@@ -33,7 +45,7 @@ def main():
                     k["coeff"] = hidden
                 if a["position"] == 2 and k["feature"] in ("dim0", "numel"):
                     k["value"] = hidden
-        d = os.path.join(ROOT, "workloads", f"rms_norm_{name}")
+        d = os.path.join(ROOT, "workloads", f"{base_name}_{name}")
         os.makedirs(d, exist_ok=True)
         shutil.copy(os.path.join(BASE, "kernel.mk"), os.path.join(d, "kernel.mk"))
         with open(os.path.join(d, "ctx.json"), "w") as fh:
@@ -42,4 +54,6 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+
+    main(sys.argv[1] if len(sys.argv) > 1 else "rms_norm")
