@@ -63,6 +63,10 @@ CASES = [
     # missing barrier: buf[tx] stored, buf[(tx + 1) % 32] read in the same
     # epoch (a read-write race the reference's twin check cannot see)
     ("racy_rw", {"BS": 2, "SL": 40}, True),
+    # fused-MoE kernels (Mixtral-8x7B): shared counters across barriers,
+    # data-dependent (havoc) indices as existential symbols
+    ("moe_align_mixtral", {"BS": 1, "SL": 1}, None),
+    ("topk_softmax", {"BS": 1, "SL": 1}, None),
 ]
 
 
