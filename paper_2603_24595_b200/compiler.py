@@ -585,6 +585,10 @@ def _form_key(terms: Dict[object, int]) -> Tuple[Tuple, int]:
     return key, f
 
 
+_NO_QUOTIENT = bool(__import__("os").environ.get("MK_NO_QUOTIENT"))   # measurement switches
+_NO_RADIX = bool(__import__("os").environ.get("MK_NO_RADIX"))
+
+
 def _replace_node(e: Node, old: Node, new: Node) -> Node:
     """Every occurrence of the subtree ``old`` in ``e`` replaced by ``new``."""
     if e == old:
@@ -912,7 +916,7 @@ class _Presolve:
         the witness order it changes neither the model set over the query's
         symbols nor its lexicographic optimum, and it is not a witness
         symbol.  Division by a positive constant cannot raise."""
-        if self.kcount > 64:
+        if self.kcount > 64 or _NO_QUOTIENT:
             return False
         ivl = _Ivl(self.bounds)
         seen: Set[Node] = set()
@@ -974,6 +978,8 @@ class _Presolve:
         launch-dependent radix (``((seq * heads + head) * gridDim.z +
         blockIdx.z) * 128 + tid``), which a race twin query's offset
         equality hinges on; interval search cannot see it."""
+        if _NO_RADIX:
+            return False
         for idx, a in enumerate(self.atoms):
             if a[0] != "p" or a[1] != "eq":
                 continue
@@ -999,7 +1005,9 @@ class _Presolve:
             x1 = t1[2] if t1[3] == P else t1[3]
             x2 = t2[2] if t2[3] == P else t2[3]
             rest = {k: v for k, v in terms.items() if k not in (t1, t2)}
-            if any(not isinstance(k, str) for k in rest):
+            # a bare P*X1 = P*X2 (no digit) is left to the search: splitting it
+            # measured slower there (moe_align's twin offsets, 19 -> 26 ms)
+            if not rest or any(not isinstance(k, str) for k in rest):
                 continue
             # one digit pair below the radix
             pair = None

@@ -1508,7 +1508,11 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
 // optimum), otherwise the full strategy runs from scratch.
 static int run_adaptive(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* status,
                         mk_i128* point, mk_stats* stats, std::chrono::steady_clock::time_point t0) {
-  if ((lim && lim->chunk != 0) || getenv("MK_NO_PROBE"))
+  // a large set (hundreds of sites, e.g. the Fig. 7 port's 862) keeps the
+  // units busy from the roots on: the probe would only add its budget
+  int probe_max = 256;
+  if (const char* e = getenv("MK_PROBE_MAX_PROBLEMS")) probe_max = atoi(e);
+  if ((lim && lim->chunk != 0) || getenv("MK_NO_PROBE") || ds->nprob > probe_max)
     return run_set(ctx, ds, lim, status, point, stats, t0);
   // a probe step must check its deadline often: small leaves (a warp
   // enumerates at most 32 leaves per step)
