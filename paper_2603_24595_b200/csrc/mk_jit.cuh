@@ -278,6 +278,41 @@ inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
        " models += __shfl_down_sync(0xffffffffu, models, o); }\n"
        "  if ((threadIdx.x & 31) == 0) { if (done) atomicAdd(evaluated, done);"
        " if (models) atomicAdd(count, models); }\n}\n";
+  // one warp step of the fused pass over instances b0 .. b0 + 31 (lane l
+  // holds b0 + l); `guarded`: the tail step, lanes past the range idle
+  auto step = [&](bool guarded) {
+    std::ostringstream o;
+    o << "    const unsigned idx = b0 + lane;\n"
+         "    " << KT << " key = 0;\n"
+         "    bool valid = false;\n";
+    if (guarded) o << "    if (idx < uend) valid = mk_acc(" << call_args() << "done, key);\n";
+    else o << "    valid = mk_acc(" << call_args() << "done, key);\n";
+    o << "    const unsigned mask = __ballot_sync(0xffffffffu, valid);\n"
+         "    if (mask) {\n"
+         "      const unsigned lower = mask & lt;\n"
+         "      const int src = lower ? 31 - __clz(lower) : 0;\n"
+         "      " << KT << " pk = __shfl_sync(0xffffffffu, key, src);\n"
+         "      if (!lower) pk = ck;\n"
+         "      const bool ph = lower ? true : have;\n"
+         "      models += valid ? 1u : 0u;\n"
+         "      if (valid && ph && key < pk) down = true;\n"
+         "      const bool eq = valid && ph && key == pk;\n"
+         "      if (__any_sync(0xffffffffu, eq)) {\n"
+         "        const unsigned idk = valid ? mk_idk(" << id_args() << ") : 0u;\n"
+         "        unsigned pi = __shfl_sync(0xffffffffu, idk, src);\n"
+         "        const unsigned px = lower ? b0 + (unsigned)src : cx;\n"
+         "        if (eq && !lower) pi = mk_idk_of(cx);\n"
+         "        if (eq && idk != pi) { ++conf; const u64 c = ((u64)idx << 32) | px;"
+         " if (c < best) { best = c; bkey = (u64)key; } }\n"
+         "      }\n"
+         "      if (!have) { const int fl = __ffs(mask) - 1; fk = __shfl_sync(0xffffffffu, key, fl);"
+         " fx = b0 + (unsigned)fl; }\n"
+         "      const int hl = 31 - __clz(mask);\n"
+         "      ck = __shfl_sync(0xffffffffu, key, hl); cx = b0 + (unsigned)hl;\n"
+         "      have = true;\n"
+         "    }\n";
+    return o.str();
+  };
   // fused ordered scan (fast path).  rec: MK_RACE_REC u64 per warp = have,
   // first key, first identity, first index, last key, last identity, last
   // index, best conflict (idx_b << 32 | idx_a), its key, pad.
@@ -300,36 +335,13 @@ inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
        "  bool have = false, down = false;\n"
        "  " << KT << " ck = 0, fk = 0;\n"
        "  unsigned cx = 0, fx = 0;\n"
-       "  for (unsigned b0 = (unsigned)base; b0 < uend; b0 += 32) {\n"
-       "    const unsigned idx = b0 + lane;\n"
-       "    " << KT << " key = 0;\n"
-       "    bool valid = false;\n"
-       "    if (idx < uend) valid = mk_acc(" << call_args() << "done, key);\n"
-       "    const unsigned mask = __ballot_sync(0xffffffffu, valid);\n"
-       "    if (mask) {\n"
-       "      const unsigned lower = mask & lt;\n"
-       "      const int src = lower ? 31 - __clz(lower) : 0;\n"
-       "      " << KT << " pk = __shfl_sync(0xffffffffu, key, src);\n"
-       "      if (!lower) pk = ck;\n"
-       "      const bool ph = lower ? true : have;\n"
-       "      models += valid ? 1u : 0u;\n"
-       "      if (valid && ph && key < pk) down = true;\n"
-       "      const bool eq = valid && ph && key == pk;\n"
-       "      if (__any_sync(0xffffffffu, eq)) {\n"
-       "        const unsigned idk = valid ? mk_idk(" << id_args() << ") : 0u;\n"
-       "        unsigned pi = __shfl_sync(0xffffffffu, idk, src);\n"
-       "        const unsigned px = lower ? b0 + (unsigned)src : cx;\n"
-       "        if (eq && !lower) pi = mk_idk_of(cx);\n"
-       "        if (eq && idk != pi) { ++conf; const u64 c = ((u64)idx << 32) | px;"
-       " if (c < best) { best = c; bkey = (u64)key; } }\n"
-       "      }\n"
-       "      if (!have) { const int fl = __ffs(mask) - 1; fk = __shfl_sync(0xffffffffu, key, fl);"
-       " fx = b0 + (unsigned)fl; }\n"
-       "      const int hl = 31 - __clz(mask);\n"
-       "      ck = __shfl_sync(0xffffffffu, key, hl); cx = b0 + (unsigned)hl;\n"
-       "      have = true;\n"
-       "    }\n"
-    << odometer_step()
+       "  unsigned b0 = (unsigned)base;\n"
+       "  // full steps (every lane in range), then at most one guarded tail step\n"
+       "  for (; b0 + 32u <= uend; b0 += 32) {\n"
+    << step(false) << odometer_step()
+    << "  }\n"
+       "  if (b0 < uend) {\n"
+    << step(true)
     << "  }\n"
     << (count_inner ? "" : "  done = (lane == 0 && uend > (unsigned)base) ? (u64)(uend - (unsigned)base) : 0ull;\n")
     << "  u64 m64 = models;\n"
