@@ -619,6 +619,10 @@ class _Presolve:
         self.fbbt_passes = 0
         self.agg_done: Set[Tuple] = set()
         self._canon_memo: Dict[Tuple, Node] = {}
+        # comparison atoms normalised in an earlier pass, by object identity
+        # (the atom list keeps its objects across passes; hashing the nested
+        # tuples for every memo lookup dominated the pass)
+        self._norm_by_id: Dict[int, Tuple[Node, Node]] = {}
         self.cuts: Set[Node] = set()
         self._lin_memo = _Lin(self.widths)
 
@@ -668,7 +672,12 @@ class _Presolve:
     def _normalize(self, e: Node, lin: _Lin, ivl: Optional["_Ivl"] = None) -> Node:
         t = e[0]
         if t == "p":
-            return self._canon_cmp(lin, e[1], e[2], e[3])
+            got = self._norm_by_id.get(id(e))
+            if got is not None and got[0] is e:
+                return got[1]
+            n = self._canon_cmp(lin, e[1], e[2], e[3])
+            self._norm_by_id[id(e)] = (e, n)
+            return n
         if t == "o":
             args = tuple(self._normalize(a, lin, ivl) for a in e[2])
             if ivl is not None and e[1] in ("and", "or"):
