@@ -1288,11 +1288,17 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   // search prunes by them; stopped through d_stop when the search is done
 
   CK(cudaMemsetAsync(d_stop, 0, sizeof(int), s));
+  // the roots' class partition made for the dive; the search copies it
+  // (device to device) instead of partitioning again when no pre-split
+  // round runs in between
+  long long dive_nt[2] = {-1, -1};
   if (dive_steps > 0) {
     void* const dst[2] = {wb + w_dive[0][0], wb + w_dive[1][0]};
     long long nt[2];
     rc = partition_to(top, dst, nt);
     if (rc) return rc;
+    dive_nt[0] = nt[0];
+    dive_nt[1] = nt[1];
     if (nt[0] >= 0) {
       CK(cudaEventRecord(ctx->ev[5], s));
       for (int c = 0; c < 2; ++c) {
@@ -1423,8 +1429,17 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   double search_ms = 0.0;
   int search_launches = 0;
   if (!budget_hit && top > 0) {
-    rc = partition(top);
-    if (rc) return rc;
+    if (rounds == 0 && dive_nt[0] >= 0) {
+      for (int c = 0; c < 2; ++c) {
+        cls[c].ntasks = dive_nt[c];
+        if (dive_nt[c] > 0)
+          CK(cudaMemcpyAsync(cls[c].tasks, wb + w_dive[c][0], cbytes[c] * (size_t)dive_nt[c],
+                             cudaMemcpyDeviceToDevice, s));
+      }
+    } else {
+      rc = partition(top);
+      if (rc) return rc;
+    }
     if (cls[0].ntasks < 0) budget_hit = true;
     else top = 0;
   }
