@@ -49,10 +49,12 @@ def record(name: str, budget_s: float = 3600.0) -> dict:
 
     from paper_2603_24595_b200 import ir
 
-    wdir = os.path.join(ROOT, "workloads", name)
-    src = open(os.path.join(wdir, "kernel.mk")).read()
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from refpath import front_end_variant, workload_sources
+
+    src, ctx_text, variant = workload_sources(name)
     unit = typecheck(parse_unit(src, "kernel.mk"))
-    ctx = context_from_json(open(os.path.join(wdir, "ctx.json")).read())
+    ctx = context_from_json(ctx_text)
 
     current = [None]
     sites = []
@@ -110,7 +112,8 @@ def record(name: str, budget_s: float = 3600.0) -> dict:
         setattr(D.Detectors, meth, wrap)
     try:
         t0 = time.monotonic()
-        rep = analyze(unit, ctx=ctx, budget=Budget(wall_s=budget_s))
+        with front_end_variant(variant):
+            rep = analyze(unit, ctx=ctx, budget=Budget(wall_s=budget_s))
         wall = time.monotonic() - t0
     finally:
         SI.Solver.check = orig_check

@@ -67,6 +67,15 @@ class CompileError(Exception):
     ``unknown`` (mirrors the reference's honest-unknown convention)."""
 
 
+class CapacityError(RuntimeError):
+    """The query is decidable but exceeds a limit of this engine (free
+    symbols per problem, registers, an unbounded symbol after presolve).
+    The reference would decide it, so reporting ``unknown`` would break
+    parity silently: this is an operational error and propagates to the
+    caller (engine/detectors.py convention: operational errors surface as
+    Python exceptions), never a verdict and never a fallback."""
+
+
 # -- device problem --------------------------------------------------------------------
 
 @dataclass
@@ -1495,14 +1504,14 @@ class _Emitter:
             f = phys_fixed(r)
             atom_regs.append(f if f is not None else assign[r])
         if nphys > MAX_REGS:
-            raise CompileError(f"site needs {nphys} registers (> {MAX_REGS})")
+            raise CapacityError(f"site needs {nphys} registers (> {MAX_REGS})")
         return out, nphys, atom_regs
 
 
 def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
                   maximize: List[bool], atoms: List[Node]) -> Problem:
     if len(var_names) > MAX_VARS:
-        raise CompileError(f"{len(var_names)} free symbols in one component (> {MAX_VARS})")
+        raise CapacityError(f"{len(var_names)} free symbols in one component (> {MAX_VARS})")
     index = {n: i for i, n in enumerate(var_names)}
     em = _Emitter(index)
     # an atom that holds without error at every point of the root box (sound
@@ -1742,7 +1751,7 @@ def _compile_query(assertions: Sequence[Node],
             lo = [ps.bounds[n][0] for n in names]
             hi = [ps.bounds[n][1] for n in names]
             if any(v is None for v in lo + hi):
-                raise CompileError("unbounded free symbol after presolve")
+                raise CapacityError("unbounded free symbol after presolve")
             mx = [ps.maximize.get(n, False) for n in names]
             prob = _emit_problem(names, lo, hi, mx, [ps.atoms[i] for i in idxs])
             grp.problems.append(len(problems))
@@ -1754,7 +1763,7 @@ def _compile_query(assertions: Sequence[Node],
             lo = [ps.bounds[n][0] for n in rest]
             hi = [ps.bounds[n][1] for n in rest]
             if any(v is None for v in lo + hi):
-                raise CompileError("unbounded free symbol after presolve")
+                raise CapacityError("unbounded free symbol after presolve")
             mx = [ps.maximize.get(n, False) for n in rest]
             prob = _emit_problem(rest, lo, hi, mx, [])
             grp.problems.append(len(problems))

@@ -65,7 +65,8 @@ class GpuDetectors:
     checker: Optional[SiteChecker] = None
     _cache: Dict[Tuple[str, ...], QueryResult] = field(default_factory=dict)
     _screen_cache: Dict[Tuple[str, ...], str] = field(default_factory=dict)
-    screen_fallbacks: int = 0
+    screens: int = 0                  # screening queries decided on the device
+    screen_budget_unknowns: int = 0   # of those, cut off by the per-query budget
     # non-parity: record every executed access for the oracle race replay
     # (paper_2603_24595_b200.replay); off by default
     record_accesses: bool = False
@@ -282,16 +283,19 @@ class GpuDetectors:
 
     # -- branch screening (engine/executor.py:489-492), SURVEY.md 8(f) row 1 --
 
-    SCREEN_BUDGET_S = 0.05
+    # the reference grants every solver query, screening included, its own
+    # Budget.query_timeout_s (engine/state.py:38; solver/interface.py:21-28)
+    SCREEN_BUDGET_S = 30.0
 
     def screen(self, path, cond) -> str:
         """sat | unsat | unknown for path + cond, as the executor's
-        ``_screen``: feasibility only (no canonical witness), render-keyed
-        cache like ``Solver.check`` (solver/interface.py:54-60).  The engine
-        gets a short budget; a query it cannot finish in time (interval
-        branch-and-prune is weak on some unsat cores the reference's LP
-        relaxation refutes at once) goes to the reference's own solver, so
-        the exploration, and with it every finding, is the reference's."""
+        ``_screen`` (engine/executor.py:489-492): feasibility only (the engine
+        stops at the first model, MK_PF_ANY), render-keyed cache like
+        ``Solver.check`` (solver/interface.py:54-60).  Decided on the B200
+        only: there is no host or reference fallback.  A screen the device
+        cannot finish within the reference's per-query timeout is
+        ``unknown``, exactly as a reference timeout would be, and is counted
+        in ``screen_budget_unknowns``."""
         E = self._E
         assertions = list(path) + [cond]
         key = ("screen",) + tuple(E.render(a) for a in assertions)
@@ -300,22 +304,23 @@ class GpuDetectors:
             res = self.checker.feasible([ir.from_ref(a) for a in assertions],
                                         self.table.origin_of, max_seconds=self.SCREEN_BUDGET_S)
             got = res.status
+            self.screens += 1
             if got == "unknown" and res.reason == "budget":
-                got = self.solver.check(assertions).status
-                self.screen_fallbacks += 1
+                self.screen_budget_unknowns += 1
             self._screen_cache[key] = got
         return got
 
 
 def install(device: int = 0, checker: Optional[SiteChecker] = None, screening: bool = False,
-            recorders: Optional[list] = None):
+            recorders: Optional[list] = None, created: Optional[list] = None):
     """Swap the checking stage of the reference executor for the B200 engine
     (engine/executor.py:33 resolves ``Detectors`` at construction time); with
     ``screening`` the executor's branch screening (engine/executor.py:489-492)
     also runs on the engine.  With ``recorders`` (a list) every constructed
     detector also records the executed accesses for the oracle race replay
     (paper_2603_24595_b200.replay) and is appended to it.  Returns what
-    ``uninstall`` needs to restore."""
+    ``uninstall`` needs to restore.  ``created`` (a list) collects every
+    detector the executor constructs (screening counters)."""
     import minikernel.engine.executor as X
 
     prev = (X.Detectors, X.Executor._screen)
@@ -326,6 +331,8 @@ def install(device: int = 0, checker: Optional[SiteChecker] = None, screening: b
                              record_accesses=recorders is not None)
             if recorders is not None:
                 recorders.append(self)
+            if created is not None:
+                created.append(self)
 
     _Bound.__name__ = "GpuDetectors"
     X.Detectors = _Bound
