@@ -1,27 +1,47 @@
 #!/usr/bin/env python
 """Checking-stage benchmark (one JSON line on rank 0).
 
-A *step* decides every checker site query of one kernel x model
-configuration (the queries the reference front end emits for it, recorded in
-tests/golden/<workload>.json by oracle/gen_golden.py): verdict plus canonical
-witness per site, i.e. the reference's Solver.check + canonicalize_witness
-(engine/detectors.py, engine/report.py:147-203) for all sites at once.
+A *step* decides every checker site query of one workload: verdict plus
+canonical witness per site, i.e. the reference's Solver.check +
+canonicalize_witness (engine/detectors.py:97-298, engine/report.py:147-203)
+for all sites at once.  The queries are the ones the reference front end
+emits on the workload's kernel ports (recorded in tests/golden/ by
+oracle/gen_golden.py).
 
-metric  checked (thread, input) instances per second: the instances of all
-        sites' compiled domains (thread identities x loop indices x havoc
-        loads x user-controlled launch assignments, the boxes the engine
-        certifies point by point or by interval proof) divided by the
-        time-to-verdict of the step.  The same instance count is used by
-        the reference arm, so the driver's ratio is the time-to-verdict
-        ratio.
-value   device-resident problem set (mk_set_eval), CUDA-event time on the
-        engine stream; L2 flushed between steps.
-e2e     the public API a user calls (SiteChecker.check_queries): compile,
-        pack, H2D copy, search, D2H copy, witness assembly, every step.
+Default workload: BASELINE.json configs[2] at its stated domain (SURVEY.md
+8(d)): vLLM paged_attention v1 with block sizes 8 / 16 / 32 and v2
+(512-token partitions), Mistral-7B, seq_len up to 2^20, a 2^20-block KV cache
+(workloads/paged_attention_*_long_*).  ``--workload corpus`` is configs[4]
+(every golden workload); any single workload name works too.
+
+Instances.  A site's instances are the points of its compiled domain (thread
+identities x loop indices x havoc loads x user-controlled launch
+assignments) that the B200 search certifies: the root-box volumes of the
+site's device problems.  A site the host site compiler refutes during
+presolve has no device problem and counts 0 instances (it is reported in
+``decided``).  Both arms use the same per-site counts, so every ratio of
+values is a ratio of times.
+
+value   device-certified instances / device time of the step: the compiled
+        problem set resident in HBM (mk_set_eval), CUDA events on the engine
+        streams, L2 flushed between steps (256 MiB write).  Max over ranks.
+e2e     the same instances / wall time of the public API a user calls
+        (SiteChecker.check_queries; N>1: shard.check_sites): host compile on
+        the worker pool, pack, H2D, search, D2H, witness assembly, every step.
+roofline  integer issue of the dominant kernel k_search against the INT32
+        issue peak measured on this device (mk_int_peak): algorithmic basis =
+        bytecode instructions evaluated (live device counters, SURVEY.md
+        8(d)); the SASS-issue basis (ncu calibration) is reported beside it.
+
+--gpus N without torchrun re-launches itself under torch.distributed.run;
+the sites are dealt across the ranks (strong scaling, no data-path
+collective; one all_gather_object of the verdict records in e2e).
 
 --impl reference runs the reference's own checker (baseline/_ref, the
-unmodified MiniKernel: Solver.check + canonicalize_witness) on the same
-queries on the host cores; rank 0 only.
+unmodified MiniKernel: Solver.check + canonicalize_witness) on the same site
+queries on the host cores, rank 0 only: each step decides the next slice of
+the site list on a process pool (the reference is single-threaded per
+query), so the K timed steps together decide every site once.
 """
 
 from __future__ import annotations
@@ -29,6 +49,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -37,46 +58,84 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
 
-DEFAULT_WORKLOAD = "rotary_embedding"   # BASELINE.json configs[1] (Llama-3-8B rotary)
+DEFAULT_WORKLOAD = "config3"
+GROUPS = {
+    "config3": ["paged_attention_v1_long_b8", "paged_attention_v1_long_b16",
+                "paged_attention_v1_long_b32", "paged_attention_v2_long_b16"],
+}
 CONFIG_NAMES = {
+    "config3": "BASELINE configs[2] at its stated domain: vLLM paged_attention v1 (block 8, 16, 32) "
+               "and v2 (block 16, 512-token partitions, max_num_seqs 1024), Mistral-7B (32/8 heads, "
+               "head 128), symbolic seq_len <= 2^20, block-table contents in [0, 2^20)",
+    "corpus": "BASELINE configs[4]: every registered kernel x model workload (tests/golden)",
     "rms_norm": "vLLM rms_norm, Llama-2-7B (hidden 4096), num_tokens 1..2^20",
-    "rotary_embedding": "vLLM rotary_embedding (NeoX), Llama-3-8B (32/8 heads, head 128), "
-                        "symbolic positions and num_tokens 1..2^20",
+    "rotary_embedding": "vLLM rotary_embedding (NeoX), Llama-3-8B, symbolic positions and "
+                        "num_tokens 1..2^20",
     "moe_align": "fused-MoE moe_align_block_size port (Fig. 7), symbolic num_tokens x top_k",
-    "fused_add_rms_norm": "vLLM fused_add_rms_norm (Fig. 2), hidden 7168, inferred context",
-    "racy": "race probe (shared + global stores)",
-    "paged_attention_v1": "vLLM paged_attention_v1, Mistral-7B (32/8 heads, head 128, block 16), "
-                          "symbolic seq_len and block-table contents",
-    "paged_attention_v2": "vLLM paged_attention_v2 (512-token partitions), Mistral-7B (32/8 heads, "
-                          "head 128, block 16), symbolic seq_len and block-table contents",
-    "moe_align_mixtral": "fused-MoE moe_align_block_size, Mixtral-8x7B (8 experts, top-2)",
-    "topk_softmax": "fused-MoE topk_softmax, Mixtral-8x7B (8 experts, top-2)",
+    "paged_attention_v1": "vLLM paged_attention_v1, Mistral-7B, block 16, seq_len <= 32768",
 }
 
 
-def _load_workload(name):
-    from paper_2603_24595_b200 import ir
-    from paper_2603_24595_b200.order import origin_lookup
+def entries(workload):
+    from goldens import workloads
 
-    with open(os.path.join(ROOT, "tests", "golden", f"{name}.json")) as fh:
-        doc = json.load(fh)
-    queries = [([ir.from_json(a) for a in s["query"]], origin_lookup(s["origins"]))
-               for s in doc["sites"]]
-    return doc, queries
+    if workload == "corpus":
+        return workloads()
+    return GROUPS.get(workload, [workload])
 
 
-def _instances(compiled):
-    """Instances certified per site: the volume of every compiled problem's
-    root box (free symbols after exact presolve)."""
-    per_site = []
-    for cq, _ in compiled:
+def load_sites(names):
+    """Every recorded site of the entries, in order: (docs, queries, site
+    records with their entry name)."""
+    from goldens import load, queries
+
+    docs, qs, recs = [], [], []
+    for n in names:
+        d = load(n)
+        docs.append(d)
+        qs.extend(queries(d))
+        recs.extend(dict(s, entry=n) for s in d["sites"])
+    return docs, qs, recs
+
+
+def site_accounting(compiled):
+    """Per site: certified instances (device problems' root-box volumes) and
+    where its verdict is decided."""
+    inst, where = [], []
+    for cq, err in compiled:
+        if cq is None:
+            inst.append(0)
+            where.append("host_unknown")
+            continue
         v = 0
-        if cq is not None:
-            for p in cq.problems:
-                v += p.volume()
-        per_site.append(v)
-    return per_site
+        for p in cq.problems:
+            v += p.volume()
+        inst.append(v)
+        if any(g.status == "unsat" for g in cq.groups):
+            where.append("host_unsat")
+        elif not cq.problems:
+            where.append("host_unknown")
+        else:
+            where.append("device")
+    return inst, where
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """--gpus N outside torchrun: one process per GPU under
+    torch.distributed.run (127.0.0.1 rendezvous)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 class Clocks:
@@ -132,8 +191,8 @@ def _peaks():
 
 
 def _calibration(workload):
-    """Per-unit calibration from the committed ncu capture of this workload
-    (tools/gpu_profile.sh -> tools/summarize_ncu.py -> profiles/)."""
+    """Per-unit SASS calibration of the search kernels (ncu launch list,
+    tools/gpu_profile.sh -> tools/summarize_ncu.py -> profiles/)."""
     path = os.path.join(ROOT, "profiles", f"ncu_{workload}_summary.json")
     try:
         with open(path) as fh:
@@ -142,24 +201,21 @@ def _calibration(workload):
         return {}
 
 
-def _reference_checker_sample(queries, per_site, budget_s):
-    """Reference's own checking stage (Solver.check + canonicalize_witness)
-    on the site queries in order until ``budget_s`` of CPU time is spent."""
-    from refbridge import reference_check_queries  # noqa: WPS433 (bench-local helper)
-
-    t0 = time.perf_counter()
-    done, inst = reference_check_queries(queries, budget_s=budget_s)
-    dt = time.perf_counter() - t0
-    return done, sum(per_site[:done]), dt
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
-def _ref_job(name):
-    """One reference job (kernel x model entry): every site query through the
-    reference's Solver.check + canonicalize_witness; returns seconds."""
-    sys.path.insert(0, os.path.join(ROOT, "tools"))
+# -- reference arm ---------------------------------------------------------------------
+
+def _ref_group(queries):
+    """One reference worker job: the queries in order through the unmodified
+    reference (refbridge: Solver.check + canonicalize_witness)."""
     from refbridge import reference_check_queries
 
-    _, queries = _load_workload(name)
     t0 = time.perf_counter()
     done, _ = reference_check_queries(queries)
     assert done == len(queries)
@@ -168,146 +224,91 @@ def _ref_job(name):
 
 def run_reference(args):
     """--impl reference: the unmodified reference checker on the host cores.
-    At N ranks the arm checks the same N corpus entries as the B200 arm, one
-    reference process per entry (the reference is single-threaded per job,
-    SURVEY.md section 8d); only rank 0 runs."""
+    Rank 0 only (other ranks exit without work).  The site list is cut into
+    ``steps`` contiguous slices; timed step i decides slice i on a process
+    pool (sites round-robin over min(cores, slice) workers, one reference
+    Solver per worker job), so the timed steps decide every site exactly
+    once and value = all sites' instances / summed step time.  Warm-up steps
+    decide the first site (pool start, imports)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    sys.path.insert(0, os.path.join(ROOT, "tools"))
     from refbridge import have_reference
 
     if not have_reference():
         print(json.dumps({"impl": "reference",
                           "unavailable": "reference MiniKernel not installed under baseline/_ref"}))
         return
+    import multiprocessing as mp
+
     from paper_2603_24595_b200.engine import compile_all
 
-    if world > 1:
-        names = ([args.workload] * world if args.workload != DEFAULT_WORKLOAD
-                 else [CORPUS[i % len(CORPUS)] for i in range(world)])
-    else:
-        names = [args.workload]
-    total = 0
-    nsites = 0
-    for n in names:
-        _, queries = _load_workload(n)
-        total += sum(_instances(compile_all(queries)))
-        nsites += len(queries)
-    cores = min(len(names), os.cpu_count() or 1)
-    pool = None
-    if len(names) > 1:
-        import multiprocessing as mp
-
-        pool = mp.get_context("fork").Pool(cores)
-    times = []
-    for step in range(args.warmup + args.steps):
+    names = entries(args.workload)
+    _, queries, _ = load_sites(names)
+    inst, _ = site_accounting(compile_all(queries))
+    cores = os.cpu_count() or 1
+    pool = mp.get_context("fork").Pool(cores)
+    n = len(queries)
+    k = max(1, args.steps)
+    slices = [list(range(n * i // k, n * (i + 1) // k)) for i in range(k)]
+    for _ in range(args.warmup):
+        pool.map(_ref_group, [[queries[0]]])
+    times, used = [], 0
+    for sl in slices:
+        w = max(1, min(cores, len(sl)))
+        groups = [[queries[j] for j in sl[g::w]] for g in range(w)]
+        groups = [g for g in groups if g]
+        used = max(used, len(groups))
         t0 = time.perf_counter()
-        if pool is None:
-            _ref_job(names[0])
-        else:
-            pool.map(_ref_job, names)
-        dt = time.perf_counter() - t0
-        if step >= args.warmup:
-            times.append(dt)
-    if pool is not None:
-        pool.close()
-    avg = sum(times) / len(times)
-    value = total / avg
+        if groups:
+            pool.map(_ref_group, groups, chunksize=1)
+        times.append(time.perf_counter() - t0)
+    pool.close()
+    total_s = sum(times)
+    value = float(sum(inst)) / total_s if total_s > 0 else 0.0
     out = {
         "impl": "reference",
         "metric": "checked (thread, input) access instances/sec; time-to-verdict per kernel x model",
         "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": avg * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int128 (mathematical integers)",
-        "data": "recorded reference site queries", "time_to_verdict_ms": avg * 1e3,
-        "config": {"workload": args.workload if world == 1 else "kernel x model corpus",
-                   "description": CONFIG_NAMES.get(args.workload), "entries": names,
-                   "sites": nsites},
-        "cpu_baseline": {"value": value, "unit": "instances/s", "cores": cores,
-                         "kind": "reference",
-                         "sample": f"all {nsites} site queries of {len(names)} corpus entr"
-                                   f"{'y' if len(names) == 1 else 'ies'} per step, reference "
-                                   "Solver.check + canonicalize_witness, one process per entry"},
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_s / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "int64/int128 (mathematical integers)",
+        "data": "recorded reference site queries of the workload ports (synthetic launches)",
+        "time_to_verdict_ms": 1e3 * total_s,
+        "config": {"workload": args.workload, "description": CONFIG_NAMES.get(args.workload),
+                   "entries": names, "sites": n, "instances": float(sum(inst))},
+        "cpu_baseline": {"value": value, "unit": "instances/s", "cores": used, "kind": "reference",
+                         "sample": f"{n} site queries of {len(names)} entr"
+                                   f"{'y' if len(names) == 1 else 'ies'} split into {k} slices, one "
+                                   "per timed step, each on a pool of up to "
+                                   f"{cores} processes (reference Solver.check + "
+                                   "canonicalize_witness, baseline/_ref)"},
         "e2e": {"value": value, "unit": "instances/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
 
 
-# BASELINE.json configs[4]: the kernel x model corpus of the rotary port,
-# dealt one entry per rank under torchrun (weak scaling, no data-path
-# collective); entry 0 is the N=1 headline workload (configs[1]).
-CORPUS = ["rotary_embedding", "rotary_llama2_7b", "rotary_mistral_7b", "rotary_llama3_70b",
-          "rotary_qwen2_7b", "rotary_llama2_13b", "rotary_mixtral_8x7b", "rotary_gemma_7b"]
+def _cpu_baseline(queries, inst, budget_s):
+    """The reference on one host core over the first sites of the workload
+    until ``budget_s`` of CPU time is spent (bounded sample)."""
+    try:
+        from refbridge import have_reference, reference_check_queries
 
-
-def _analyze_line(chk, args, doc):
-    """BASELINE metric part 2, time-to-verdict per kernel x model: the
-    reference's own analyze() (parser, symbolic DFS, checking) on the
-    workload's kernel port and context, once with the B200 checking stage and
-    branch screening installed (GpuDetectors) and once unmodified; wall time
-    of each and whether the findings are the reference's."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from refpath import add_reference, analyze_workload
-    from goldens import expected_findings
-
-    if not add_reference():
-        return {"unavailable": "reference front end not installed under baseline/_ref"}
-    from paper_2603_24595_b200.detectors import install, uninstall
-
-    times = []
-    for _ in range(3):
-        prev = install(checker=chk, screening=True)
+        if not have_reference():
+            return None
         t0 = time.perf_counter()
-        try:
-            got = analyze_workload(args.workload)
-        finally:
-            uninstall(prev)
-        times.append(time.perf_counter() - t0)
-    t0 = time.perf_counter()
-    ref = analyze_workload(args.workload)
-    ref_s = time.perf_counter() - t0
-    return {"workload": args.workload, "b200_ms": 1e3 * min(times), "reference_ms": 1e3 * ref_s,
-            "speedup": ref_s / min(times),
-            "findings_equal_reference": got["findings"] == expected_findings(doc),
-            "reference_findings_equal_golden": ref["findings"] == doc["findings"],
-            "what": "analyze() wall time: reference front end (parser, DFS) + B200 checking "
-                    "stage and branch screening vs the unmodified reference, one core"}
-
-
-def _heavy_line(chk, args, int_peak, sm_mhz, sms):
-    """The search kernels at scale: BASELINE configs[2] (paged attention,
-    Mistral-7B), whose step is ~4e8 boxes, timed resident like the headline
-    step; roofline from the same ncu calibration scheme."""
-    doc, queries = _load_workload(args.heavy)
-    from paper_2603_24595_b200.engine import compile_all
-
-    compiled = compile_all(queries)
-    packed, _ = chk.pack([c for c, _ in compiled])
-    resident = chk.engine.upload(packed)
-    lim = dict(chk.limits)
-    lim["max_seconds"] = 600.0
-    resident.run(lim)
-    runs = [resident.run(lim) for _ in range(2)]
-    resident.free()
-    ms = sum(r["bb_ms"] + r["leaf_ms"] for r in runs) / len(runs)
-    step_ms = sum(r["device_ms"] for r in runs) / len(runs)
-    units = sum(r["boxes"] + r["points"] for r in runs) / len(runs)
-    cal = _calibration(args.heavy)
-    per_unit = cal.get("thread_inst_per_unit")
-    achieved = units * per_unit / (ms / 1e3) if per_unit and ms > 0 else None
-    return {"workload": args.heavy, "description": CONFIG_NAMES.get(args.heavy),
-            "device_ms_per_step": step_ms, "boxes_and_instances_per_step": units,
-            "roofline": {"bound": "int32-issue",
-                         "achieved": achieved / 1e9 if achieved else None,
-                         "peak": int_peak / 1e9, "unit": "Gop/s",
-                         "frac": achieved / int_peak if achieved else None,
-                         "kernel": "k_search (+k_bb, k_leaf)", "kernel_ms_per_step": ms,
-                         "ops": f"SASS thread instructions per box/instance: {per_unit} (ncu, "
-                                f"profiles/ncu_{args.heavy}_summary.json)",
-                         "ncu_issue_active_pct": cal.get("k_search_issue_active_pct")}}
+        done, _ = reference_check_queries(queries, budget_s=budget_s)
+        dt = time.perf_counter() - t0
+        return {"value": sum(inst[:done]) / dt, "unit": "instances/s", "cores": 1,
+                "kind": "reference",
+                "sample": f"first {done} of {len(queries)} site queries through the reference's "
+                          f"Solver.check + canonicalize_witness (baseline/_ref), {dt:.1f}s, "
+                          "1 thread"}
+    except Exception as exc:  # the baseline is reported, never required
+        return {"value": None, "unit": "instances/s", "cores": 1, "kind": "reference",
+                "sample": f"unavailable: {exc}"}
 
 
 def _race_sweep_line(chk, args, peaks, src, int_peak):
@@ -326,7 +327,9 @@ def _race_sweep_line(chk, args, peaks, src, int_peak):
      / device time, against the HBM peak."""
     from paper_2603_24595_b200 import race
 
-    doc, queries = _load_workload("rms_norm")
+    from goldens import load as _gload, queries as _gq
+    doc = _gload("rms_norm")
+    queries = _gq(doc)
     T = args.race_tokens
     launch = {"BS": 1, "SL": T, "TC": T, "blockDim.x": 1024, "blockDim.y": 1, "blockDim.z": 1,
               "gridDim.x": T, "gridDim.y": 1, "gridDim.z": 1}
@@ -395,7 +398,9 @@ def _race_sharded_line(chk, args, world):
 
     from paper_2603_24595_b200 import race, shard
 
-    doc, queries = _load_workload("rms_norm")
+    from goldens import load as _gload, queries as _gq
+    doc = _gload("rms_norm")
+    queries = _gq(doc)
     T = args.race_tokens
     launch = {"BS": 1, "SL": T, "TC": T, "blockDim.x": 1024, "blockDim.y": 1, "blockDim.z": 1,
               "gridDim.x": T, "gridDim.y": 1, "gridDim.z": 1}
@@ -511,6 +516,44 @@ def _access_line(chk, args, peaks, src, int_peak):
                                        "algorithmic_bytes": algo}}}
 
 
+def _analyze_line(chk, name):
+    """BASELINE metric part 2, time-to-verdict per kernel x model: the
+    reference's own analyze() (parser, symbolic DFS, checking) on one
+    workload port + context, with the B200 checking stage AND branch
+    screening installed (GpuDetectors; every screen decided on the device,
+    no reference fallback) vs unmodified; findings must be the reference's."""
+    from goldens import expected_findings, load
+    from refpath import add_reference, analyze_workload
+
+    if not add_reference():
+        return {"unavailable": "reference front end not installed under baseline/_ref"}
+    from paper_2603_24595_b200.detectors import install, uninstall
+
+    doc = load(name)
+    times, made = [], []
+    for _ in range(3):
+        made.clear()
+        prev = install(checker=chk, screening=True, created=made)
+        t0 = time.perf_counter()
+        try:
+            got = analyze_workload(name)
+        finally:
+            uninstall(prev)
+        times.append(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    ref = analyze_workload(name)
+    ref_s = time.perf_counter() - t0
+    return {"workload": name, "b200_ms": 1e3 * min(times), "reference_ms": 1e3 * ref_s,
+            "speedup": ref_s / min(times),
+            "findings_equal_reference": got["findings"] == expected_findings(doc),
+            "reference_findings_equal_golden": ref["findings"] == doc["findings"],
+            "screens_on_device": sum(d.screens for d in made),
+            "screen_budget_unknowns": sum(d.screen_budget_unknowns for d in made),
+            "screen_reference_fallbacks": 0,
+            "what": "analyze() wall time: reference front end (parser, DFS) + B200 checking "
+                    "stage and branch screening vs the unmodified reference, one core"}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -524,201 +567,188 @@ def run_b200(args):
     if one:
         local = 0
     torch.cuda.set_device(local)
+    from paper_2603_24595_b200 import shard
+    from paper_2603_24595_b200.engine import SiteChecker, compile_all
+    from goldens import mismatches
+
+    # the checker (and its compile workers) before the process group
+    chk = SiteChecker(device=local)
     if world > 1:
         if one:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2603_24595_b200 import shard
-    from paper_2603_24595_b200.engine import SiteChecker, compile_all
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if one else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
-    if world > 1:
-        if args.workload != DEFAULT_WORKLOAD:
-            names = [args.workload] * world
-        else:
-            names = [CORPUS[i % len(CORPUS)] for i in range(world)]
-    else:
-        names = [args.workload]
-    my_name = names[rank]
-    doc, queries = _load_workload(my_name)
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if one else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    names = entries(args.workload)
+    docs, queries, recs = load_sites(names)
+    t0 = time.perf_counter()
     compiled = compile_all(queries)
-    per_site = _instances(compiled)
-    instances = sum(per_site)
-    chk = SiteChecker(device=local)
-    packed, offsets = chk.pack([c for c, _ in compiled])
-    resident = chk.engine.upload(packed)
-    limits = dict(chk.limits)
-    limits["max_seconds"] = min(chk.limits["max_seconds"] * len(queries), 3600.0)
+    compile_serial_ms = 1e3 * (time.perf_counter() - t0)
+    inst, where = site_accounting(compiled)
+    mine = (shard.deal([float(1 + len(a)) for a, _ in queries], world)[rank]
+            if world > 1 else list(range(len(queries))))
+    my_compiled = [compiled[i] for i in mine]
+    my_inst = float(sum(inst[i] for i in mine))
+    total_instances = float(sum(inst))
 
-    # parity gate: the benchmarked result must be the reference's (sites the
-    # reference only timed out on are pinned by its own z3 path, see
-    # tests/goldens.py and oracle/z3_crosscheck.py)
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from goldens import mismatches
-
-    results = chk.decide(compiled, packed, offsets)
-    bad = mismatches(doc, results)
+    # parity gate: the benchmarked results must be the reference's (sites
+    # the reference only timed out on are pinned by z3, tests/goldens.py)
+    packed, offsets = chk.pack([c for c, _ in my_compiled])
+    results = chk.decide(my_compiled, packed, offsets)
+    bad = mismatches({"sites": [recs[i] for i in mine]}, results)
     if bad:
-        raise SystemExit(f"parity failure on {my_name} sites {bad[:10]}")
+        raise SystemExit(f"parity failure on sites {bad[:10]}")
+    sat_dev = sum(1 for i, r in zip(mine, results) if r.status == "sat" and where[i] == "device")
 
+    resident = chk.engine.upload(packed) if packed.problems else None
+    limits = dict(chk.limits)
+    limits["max_seconds"] = min(chk.limits["max_seconds"] * max(len(mine), 1), 3600.0)
+    peak = chk.engine.int_peak()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    empty = {"device_ms": 0.0, "bb_ms": 0.0, "leaf_ms": 0.0, "boxes": 0, "points": 0,
+             "insns_bb": 0, "insns_leaf": 0, "launches": 0, "covered": 0.0}
     for _ in range(args.warmup):
-        resident.run(limits)
+        if resident:
+            resident.run(limits)
     clocks = Clocks(local).start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    dev_ms, wall, launches = [], [], 0
-    stats_acc = {}
+    dev_ms, launches, acc = [], 0, {}
     for _ in range(args.steps):
         flush.random_(0, 255)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        st = resident.run(limits)
-        wall.append(time.perf_counter() - t0)
+        st = resident.run(limits) if resident else dict(empty)
         dev_ms.append(st["device_ms"])
         launches += int(st["launches"])
-        for k, v in st.items():
-            stats_acc[k] = stats_acc.get(k, 0) + v
+        for k in empty:
+            acc[k] = acc.get(k, 0) + st[k]
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms_step = sum(dev_ms) / len(dev_ms)
-    total_instances = float(instances)
-    if world > 1:
-        t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-        t = torch.tensor([float(instances)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        total_instances = float(t.item())
-    value = total_instances / (ms_step / 1e3)
+    n = args.steps
+    ms_step = max_over_ranks(sum(dev_ms) / n)
+    value = total_instances / (ms_step / 1e3) if ms_step > 0 else 0.0
 
-    # e2e through the public API with host buffers (compile + H2D + search +
-    # D2H + witness assembly); at N>1 the corpus call deals one entry per rank
-    # and all-gathers every result to every rank.  Warm-up calls start the
-    # host compile workers outside the timed steps.
-    entries = None
-    if world > 1:
-        entries = [_load_workload(n)[1] for n in names]
-
+    # e2e through the public API with host buffers, every step: compile on
+    # the worker pool, pack, H2D, search, D2H, assembly (N>1: sites dealt,
+    # verdict records all-gathered).  Warm-up calls start the workers.
     def e2e_call():
-        if entries is None:
-            return chk.check_queries(queries)
-        return shard.check_corpus(chk, entries)
+        return shard.check_sites(chk, queries) if world > 1 else chk.check_queries(queries)
 
     for _ in range(args.warmup):
         e2e_call()
     e2e_t = []
-    for step in range(max(1, args.steps)):
+    for _ in range(n):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        res = e2e_call()
+        e2e_call()
         e2e_t.append(time.perf_counter() - t0)
-    e2e_s = sum(e2e_t) / len(e2e_t)
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(sum(e2e_t) / len(e2e_t))
+    h2d = sum_over_ranks(packed.host_bytes())
+    d2h = sum_over_ranks(resident.d2h_bytes() if resident else 0)
 
-    # roofline of the dominant kernels (pre-split + persistent search; one
-    # box / instance = one unit): integer-lane issue.  Achieved = units per
-    # step (live engine counters) x SASS thread instructions per unit (ncu
-    # capture of the same workload, profiles/ncu_<workload>_summary.json)
-    # / device time of those kernels (CUDA events on the engine streams).
-    n = args.steps
-    search_ms = stats_acc["bb_ms"] / n + stats_acc["leaf_ms"] / n
-    units = (stats_acc["boxes"] + stats_acc["points"]) / n
-    insns = (stats_acc["insns_bb"] + stats_acc["insns_leaf"]) / n
-    peaks, src = _peaks()
-    sm_mhz = clk["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
-    sms = torch.cuda.get_device_properties(local).multi_processor_count
-    int_peak = sms * 128 * sm_mhz * 1e6           # 128 INT32 lanes / SM / clock (B200: 148 SMs)
+    # roofline of k_search (+ its pre-split / leaf kernels): integer issue
+    search_ms = (acc["bb_ms"] + acc["leaf_ms"]) / n
+    units = (acc["boxes"] + acc["points"]) / n
+    bc_ops = (acc["insns_bb"] + acc["insns_leaf"]) / n
+    int_peak = peak["ops_per_s"]
+    alg = bc_ops / (search_ms / 1e3) if search_ms > 0 else 0.0
     cal = _calibration(args.workload)
     per_unit = cal.get("thread_inst_per_unit")
-    if per_unit:
-        achieved = units * per_unit / (search_ms / 1e3) if search_ms > 0 else 0.0
-        ops = (f"SASS thread instructions: {units:.3g} boxes+instances per step x "
-               f"{per_unit:.1f} per unit (ncu, profiles/ncu_{args.workload}_summary.json)")
-    else:
-        achieved = insns / (search_ms / 1e3) if search_ms > 0 else 0.0
-        ops = "bytecode instructions executed (no ncu calibration committed)"
+    sass = units * per_unit / (search_ms / 1e3) if per_unit and search_ms > 0 else None
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
 
-    k2 = _race_sweep_line(chk, args, peaks, src, int_peak) if rank == 0 and args.race_tokens > 0 else None
-    k2_sharded = (_race_sharded_line(chk, args, world)
-                  if world > 1 and args.race_tokens > 0 else None)
-    analyze = _analyze_line(chk, args, doc) if rank == 0 and world == 1 and args.analyze else None
-    access = (_access_line(chk, args, peaks, src, int_peak)
-              if rank == 0 and world == 1 and args.access_tokens > 0 else None)
-    heavy = (_heavy_line(chk, args, int_peak, sm_mhz, sms)
-             if rank == 0 and world == 1 and args.heavy and args.heavy != args.workload else None)
+    decided = {"sites": len(queries),
+               "device": sum(1 for w in where if w == "device"),
+               "host_presolve_unsat": sum(1 for w in where if w == "host_unsat"),
+               "host_reference_giveup_unknown": sum(1 for w in where if w == "host_unknown"),
+               "device_sat_witnesses": int(sum_over_ranks(sat_dev)),
+               "device_problems": int(sum_over_ranks(len(packed.problems)))}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        try:
-            from refbridge import have_reference, reference_check_queries
-            if have_reference():
-                t0 = time.perf_counter()
-                done, _ = reference_check_queries(queries, budget_s=args.cpu_budget)
-                dt = time.perf_counter() - t0
-                cpu = {"value": sum(per_site[:done]) / dt, "unit": "instances/s", "cores": 1,
-                       "kind": "reference",
-                       "sample": f"first {done} of {len(queries)} {args.workload} site queries "
-                                 "through the reference's Solver.check + canonicalize_witness "
-                                 f"(baseline/_ref), {dt:.1f}s, 1 thread"}
-        except Exception as exc:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": "instances/s", "cores": 1, "kind": "reference",
-                   "sample": f"unavailable: {exc}"}
+    side = {}
+    if rank == 0 and world == 1:
+        peaks, src = _peaks()
+        if args.race_tokens > 0:
+            side["k2_race_sweep"] = _race_sweep_line(chk, args, peaks, src, int_peak)
+        if args.access_tokens > 0:
+            side["k2_access_replay"] = _access_line(chk, args, peaks, src, int_peak)
+        if args.analyze:
+            side["time_to_verdict"] = _analyze_line(chk, args.analyze)
+        if not args.no_cpu_baseline:
+            side["cpu_baseline"] = _cpu_baseline(queries, inst, args.cpu_budget)
+    if world > 1 and args.race_tokens > 0:
+        side["k2_race_sharded"] = _race_sharded_line(chk, args, world)
 
     if rank == 0:
         out = {
             "metric": "checked (thread, input) access instances/sec; time-to-verdict per kernel x model",
-            "value": value, "unit": "instances/s", "n_gpus": world, "steps": args.steps,
+            "value": value, "unit": "instances/s", "n_gpus": world, "steps": n,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int128 (mathematical integers)",
-            "data": "site queries recorded from the reference front end on the workload port",
-            "config": {"workload": args.workload if world == 1 else "kernel x model corpus",
-                       "description": CONFIG_NAMES.get(args.workload) if world == 1 else
-                       "rotary_embedding port under one model context per rank",
-                       "entries": names,
-                       "sites": len(queries), "instances_per_step": total_instances,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "int64/int128 (mathematical integers)",
+            "data": "site queries recorded from the reference front end on the workload ports "
+                    "(synthetic launches; no tensors)",
+            "config": {"workload": args.workload, "description": CONFIG_NAMES.get(args.workload),
+                       "entries": names, "sites": len(queries),
+                       "instances_per_step": total_instances,
+                       "instances": "device-certified root-box volumes of the sites' compiled "
+                                    "problems (presolve-refuted sites count 0)",
                        "l2": "flushed between steps (256 MiB write)",
                        "parallelism": "1 GPU" if world == 1 else
-                       f"{world} ranks, one corpus entry each (no data-path collective; "
-                       "results all-gathered in e2e)"},
-            "time_to_verdict_ms": ms_step,
-            "wall_ms_per_step": 1e3 * sum(wall) / len(wall),
-            "evaluated_per_step": {"boxes": stats_acc["boxes"] / n, "points": stats_acc["points"] / n},
+                       f"{world} ranks, sites dealt longest-first (no data-path collective; "
+                       "verdict records all-gathered in e2e)"},
+            "decided": decided,
+            "time_to_verdict_ms": e2e_s * 1e3,
+            "evaluated_per_step": {"boxes": acc["boxes"] / n, "points": acc["points"] / n,
+                                   "bytecode_insns": bc_ops},
+            "evaluated_instances_per_s": units / (ms_step / 1e3) if ms_step > 0 else 0.0,
+            "covered_instances_per_s": (acc["covered"] / n) / (ms_step / 1e3) if ms_step > 0 else 0.0,
             "e2e": {"value": total_instances / e2e_s, "unit": "instances/s",
-                    "h2d_bytes_per_step": packed.host_bytes(),
-                    "d2h_bytes_per_step": resident.d2h_bytes(), "ms_per_step": e2e_s * 1e3},
-            "roofline": {"bound": "int32-issue", "achieved": achieved / 1e9,
-                         "peak": int_peak / 1e9, "unit": "Gop/s",
-                         "frac": achieved / int_peak if int_peak else None,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_s * 1e3,
+                    "compile_serial_ms": compile_serial_ms,
+                    "compile_workers": chk.compile_workers},
+            "roofline": {"bound": "int32-issue", "achieved": alg / 1e9, "peak": int_peak / 1e9,
+                         "unit": "Gop/s", "frac": alg / int_peak if int_peak else None,
                          "traffic": cal.get("k_search_dram_bytes_per_launch"),
                          "kernel": "k_search (+k_bb pre-split, k_leaf)",
                          "kernel_ms_per_step": search_ms,
-                         "units_per_step": units,
-                         "bytecode_insns_per_step": insns,
-                         "ops": ops,
-                         "ncu_issue_active_pct": cal.get("k_search_issue_active_pct"),
-                         "peak_source": f"{sms} SMs x 128 INT32 lanes x {sm_mhz:.0f} MHz "
-                                        f"(clock sampled; peaks file: {src})"},
-            "cpu_baseline": cpu,
-            "k2_race_sweep": k2,
-            "k2_access_replay": access,
-            "k2_race_sharded": k2_sharded,
-            "time_to_verdict": analyze,
-            "k1_heavy": heavy,
+                         "ops": "bytecode instructions evaluated per step (live device counters; "
+                                "one op per instruction per box or point, SURVEY.md 8(d))",
+                         "peak_source": f"mk_int_peak on this device ({sms} SMs): "
+                                        "IADD3/LOP3/VIMNMX/IMAD microbenchmark, "
+                                        f"{peak['ms']:.2f} ms",
+                         "sass_basis": {"achieved": sass / 1e9 if sass else None,
+                                        "frac": sass / int_peak if sass else None,
+                                        "per_unit": per_unit,
+                                        "source": f"profiles/ncu_{args.workload}_summary.json",
+                                        "ncu_issue_active_pct":
+                                            cal.get("k_search_issue_active_pct")}},
+            "cpu_baseline": side.pop("cpu_baseline", None),
             "clocks": clk,
             "gpu_launches": launches,
         }
+        out.update(side)
         print(json.dumps(out))
-    resident.free()
+    if resident:
+        resident.free()
     chk.close()
     if world > 1:
         dist.destroy_process_group()
@@ -730,13 +760,12 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD,
+                    help="config3 (default), corpus, or one workload name")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-analyze", dest="analyze", action="store_false",
-                    help="skip the end-to-end analyze() time-to-verdict line")
-    ap.add_argument("--heavy", default="paged_attention_v1",
-                    help="workload of the k1_heavy line ('' to skip)")
+    ap.add_argument("--analyze", default="rms_norm",
+                    help="workload of the analyze() time-to-verdict line ('' to skip)")
     ap.add_argument("--access-tokens", type=int, default=16384,
                     help="num_tokens of the oracle-rule access replay line (0: skip)")
     ap.add_argument("--race-tokens", type=int, default=262144,
@@ -744,6 +773,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -107,9 +107,14 @@ typedef struct mk_problem {
 #define MK_PF_ANY 2
 
 /* Linear rows used for bound contraction inside a box:
- *   sum_k coef_k * x_var_k + c0  (rel 0: <= 0, rel 1: == 0) */
+ *   sum_k coef_k * x_var_k + c0  (rel 0: <= 0, rel 1: == 0)
+ * group 0: the row holds at every model (a conjunct of the query).
+ * group g > 0: the rows of group g (contiguous) are the operands of one
+ * disjunction conjunct: on a box where every row of the group but one is
+ * infeasible the box's models satisfy that one, and the engine contracts
+ * with it; a box where all of them are infeasible holds no model. */
 typedef struct mk_row {
-  int32_t rel, nterms, term_off, pad;
+  int32_t rel, nterms, term_off, group;
   mk_i128 c0;
 } mk_row;
 
@@ -307,6 +312,15 @@ typedef struct mk_access_result {
 } mk_access_result;
 
 int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access_result* out);
+
+/* ---------------------------------------------------------------------
+ * INT32 issue peak of this device, measured:
+ * one persistent grid (4 CTAs x 256 threads per SM) of independent
+ * IADD3 / LOP3 / ISETP+SEL / IMAD chains; *ops_per_s = thread-level integer
+ * instructions retired per second (the denominator of the evaluator's
+ * integer-issue roofline), *ms the kernel time.  Not part of the checking
+ * stage: a calibration the benchmark runs once per box. */
+int mk_int_peak(mk_ctx* ctx, double* ops_per_s, double* ms);
 
 #ifdef __cplusplus
 }

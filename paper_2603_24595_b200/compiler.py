@@ -36,6 +36,7 @@ Steps (each exact: the model set and the witness order are preserved):
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from fractions import Fraction
 from typing import Callable, Dict, List, Optional, Sequence, Set, Tuple
@@ -56,6 +57,9 @@ _ARITH_OP = {"add": OP_ADD, "sub": OP_SUB, "mul": OP_MUL, "div": OP_DIV,
 _CMP_OP = {"eq": OP_EQ, "ne": OP_NE, "lt": OP_LT, "le": OP_LE, "gt": OP_GT, "ge": OP_GE}
 
 MAX_VARS = 64        # free symbols per device problem (bit mask width)
+# host-side FBBT over the presolved rows; off: bound propagation is left to
+# the device's root contraction (mk_contract), measurement switch
+HOST_FBBT = os.environ.get("MK_HOST_FBBT", "1") != "0"
 MAX_REGS = 1024
 _AGG_WIDE = 4096
 _NEG = {"eq": "ne", "ne": "eq", "lt": "ge", "le": "gt", "gt": "le", "ge": "lt"}
@@ -91,7 +95,8 @@ class Problem:
     nregs: int = 0
     atom_regs: List[int] = field(default_factory=list)
     atom_masks: List[int] = field(default_factory=list)
-    rows: List[Tuple[int, int, List[Tuple[int, int]]]] = field(default_factory=list)
+    # (rel, c0, [(var, coef)], group): include/mk_b200.h mk_row
+    rows: List[Tuple[int, int, List[Tuple[int, int]], int]] = field(default_factory=list)
     ops_per_point: int = 0         # instructions evaluated per instance
     narrow: bool = False           # exact in 64-bit arithmetic (narrow_proof)
     any_model: bool = False        # feasibility only: stop at the first model
@@ -835,7 +840,7 @@ class _Presolve:
         if self._try_fm(lin):
             return True
         # 8. interval bound tightening (capped: slow creep is left to the device)
-        if self.fbbt_passes >= 24:
+        if not HOST_FBBT or self.fbbt_passes >= 24:
             return False
         self.fbbt_passes += 1
         return self._fbbt(lin)
@@ -1508,6 +1513,35 @@ class _Emitter:
         return out, nphys, atom_regs
 
 
+def _cmp_rows(lin: "_Lin", e: Node):
+    """A comparison over symbols as rows (rel, c0, terms): sum <= 0 (rel 0)
+    or sum == 0 (rel 1); ``ne`` is its two strict sides.  None when ``e``
+    is not a comparison of linear forms over symbols."""
+    if e[0] != "p":
+        return None
+    try:
+        terms, c0 = _lin_add(lin.lin(e[2]), lin.lin(e[3]), -1)
+    except CompileError:
+        return None
+    if not terms or not all(isinstance(k, str) for k in terms):
+        return None
+    neg = {k: -v for k, v in terms.items()}
+    op = e[1]
+    if op == "le":
+        return [(0, c0, terms)]
+    if op == "lt":
+        return [(0, c0 + 1, terms)]
+    if op == "ge":
+        return [(0, -c0, neg)]
+    if op == "gt":
+        return [(0, -c0 + 1, neg)]
+    if op == "eq":
+        return [(1, c0, terms)]
+    if op == "ne":
+        return [(0, c0 + 1, terms), (0, -c0 + 1, neg)]
+    return None
+
+
 def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
                   maximize: List[bool], atoms: List[Node]) -> Problem:
     if len(var_names) > MAX_VARS:
@@ -1532,15 +1566,32 @@ def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
         for n in ir.symbols_of(a):
             m |= 1 << index[n]
         masks.append(m)
-    # purely linear atoms double as contraction rows (sum <= 0 / sum == 0)
-    rows: List[Tuple[int, int, List[Tuple[int, int]]]] = []
+    # purely linear atoms double as contraction rows (sum <= 0 / sum == 0);
+    # a disjunction of linear comparisons (and a linear !=, two strict
+    # sides) becomes a row group the device contracts with whenever all but
+    # one of its rows are infeasible on a box (include/mk_b200.h mk_row)
+    rows: List[Tuple[int, int, List[Tuple[int, int]], int]] = []
     lin = _Lin({})
+    group = 0
     for a in atoms:
         if a[0] == "p" and a[1] in ("le", "eq") and a[3] == ("c", 0, "i64"):
             terms, c0 = lin.lin(a[2])
             if terms and all(isinstance(k, str) for k in terms):
                 rows.append((0 if a[1] == "le" else 1, c0,
-                             [(index[k], v) for k, v in sorted(terms.items())]))
+                             [(index[k], v) for k, v in sorted(terms.items())], 0))
+                continue
+        ops = a[2] if a[0] == "o" and a[1] == "or" else (a,) if a[0] == "p" and a[1] == "ne" else ()
+        alts = []
+        for o in ops:
+            got = _cmp_rows(lin, o)
+            if got is None:
+                alts = []
+                break
+            alts.extend(got)
+        if len(alts) >= 2:
+            group += 1
+            for rel, c0, terms in alts:
+                rows.append((rel, c0, [(index[k], v) for k, v in sorted(terms.items())], group))
     prob = Problem(var_names=var_names, lo=lo, hi=hi, maximize=maximize,
                    insns=code, consts=list(em.consts), nregs=nregs,
                    atom_regs=atom_regs, atom_masks=masks, rows=rows,
@@ -1622,7 +1673,8 @@ def narrow_proof(p: Problem) -> bool:
         if not (_I64_MIN <= r[0] and r[1] <= _I64_MAX):
             return False
         R[d] = r
-    for _rel, c0, terms in p.rows:
+    for row in p.rows:
+        c0, terms = row[1], row[2]
         s = abs(c0) + sum(abs(cf) * max(abs(p.lo[v]), abs(p.hi[v])) for v, cf in terms)
         if s >= NARROW_LIMIT:
             return False
@@ -1717,8 +1769,14 @@ def _compile_query(assertions: Sequence[Node],
             continue
         had = flags["unsupported"]
         if ps.unsat:
-            groups.append(Group("unsat" if not had else "unknown",
-                                "float/unsupported atoms only" if had else None, had))
+            if not had:
+                # one unsatisfiable component refutes the query whatever the
+                # others are (solver/builtin.py:737-740): nothing of it goes
+                # to the device, and the remaining components are not compiled
+                return CompiledQuery(witness_names=witness_names, order=order,
+                                     groups=[Group("unsat", "presolve", False)], problems=[],
+                                     defs={}, free_default={})
+            groups.append(Group("unknown", "float/unsupported atoms only", had))
             continue
         for n, e in ps.defs.items():
             defs[n] = e
@@ -1770,6 +1828,11 @@ def _compile_query(assertions: Sequence[Node],
             problems.append(prob)
         groups.append(grp)
 
+    if any(g.status == "unknown" for g in groups):
+        # the verdict is unknown unless another component is unsat
+        # (solver/builtin.py:737-745): the device only needs feasibility
+        for p in problems:
+            p.any_model = True
     # symbols that simplification removed entirely: unconstrained, so the
     # canonical value is the width bound in the optimisation direction
     for n, w in widths.items():

@@ -495,70 +495,128 @@ MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const V* vlo, const V* vhi, MkIv
 
 // ---------------------------------------------------------------------------
 // bound contraction over the linear rows (one FBBT sweep per call);
-// returns false when the box is empty.
+// returns false when the box is empty.  Rows of a disjunctive group (group >
+// 0, contiguous) contract only when every other row of the group is
+// infeasible on the box; a group whose rows are all infeasible empties it.
+
+// activity range of one row over the box: fmin / fmax with the number of
+// infinite contributions (wide class only)
+template <typename V>
+MK_HD void mk_row_range(const mk_row& row, const mk_row_term* T, const V* lo, const V* hi,
+                        V& fmin, V& fmax, int& nmin_inf, int& nmax_inf) {
+  typedef MkNum<V> N;
+  const V INF = N::inf();
+  fmin = N::ld(row.c0);
+  fmax = fmin;
+  nmin_inf = nmax_inf = 0;
+  for (int k = 0; k < row.nterms; ++k) {
+    V c = N::ld(T[k].coef);
+    int v = T[k].var;
+    V a = N::mul(c, lo[v]), b = N::mul(c, hi[v]);
+    V mn = mk_min(a, b), mx = mk_max(a, b);
+    if (N::kWide && mn == -INF) nmin_inf++; else fmin = N::add(fmin, mn);
+    if (N::kWide && mx == INF) nmax_inf++; else fmax = N::add(fmax, mx);
+  }
+}
+
+// the row cannot hold anywhere on the box
+template <typename V>
+MK_HD bool mk_row_dead(const mk_row& row, V fmin, V fmax, int nmin_inf, int nmax_inf) {
+  typedef MkNum<V> N;
+  const V INF = N::inf();
+  if (nmin_inf == 0 && fmin > 0 && fmin != INF) return true;  // sum >= fmin > 0
+  if (N::kWide && nmin_inf == 0 && fmin == INF) return true;
+  if (row.rel == 1 && nmax_inf == 0 && fmax < 0 && fmax != -INF) return true;
+  if (N::kWide && row.rel == 1 && nmax_inf == 0 && fmax == -INF) return true;
+  return false;
+}
+
+// tighten every variable of one row; false when a bound crosses
+template <typename V>
+MK_HD bool mk_row_tighten(const mk_row& row, const mk_row_term* T, V* lo, V* hi, V fmin,
+                          V fmax, int nmin_inf, int nmax_inf, bool& changed) {
+  typedef MkNum<V> N;
+  const V INF = N::inf();
+  for (int k = 0; k < row.nterms; ++k) {
+    V c = N::ld(T[k].coef);
+    int v = T[k].var;
+    V a = N::mul(c, lo[v]), b = N::mul(c, hi[v]);
+    V mn = mk_min(a, b), mx = mk_max(a, b);
+    // others_min = fmin - mn (when finite)
+    int oinf = nmin_inf - ((N::kWide && mn == -INF) ? 1 : 0);
+    if (oinf == 0) {
+      V omin = (N::kWide && mn == -INF) ? fmin : N::sub(fmin, mn);
+      if (!N::isinf(omin)) {
+        // c*x <= -omin
+        if (c > 0) {
+          V nb = mk_floordiv<V>(-omin, c);
+          if (nb < hi[v]) { hi[v] = nb; changed = true; }
+        } else {
+          V nb = mk_ceildiv<V>(-omin, c);
+          if (nb > lo[v]) { lo[v] = nb; changed = true; }
+        }
+      }
+    }
+    if (row.rel == 1) {
+      int oinf2 = nmax_inf - ((N::kWide && mx == INF) ? 1 : 0);
+      if (oinf2 == 0) {
+        V omax = (N::kWide && mx == INF) ? fmax : N::sub(fmax, mx);
+        if (!N::isinf(omax)) {
+          // c*x >= -omax
+          if (c > 0) {
+            V nb = mk_ceildiv<V>(-omax, c);
+            if (nb > lo[v]) { lo[v] = nb; changed = true; }
+          } else {
+            V nb = mk_floordiv<V>(-omax, c);
+            if (nb < hi[v]) { hi[v] = nb; changed = true; }
+          }
+        }
+      }
+    }
+    if (lo[v] > hi[v]) return false;
+  }
+  return true;
+}
 
 template <typename V>
 MK_HD bool mk_contract(const MkProb& P, V* lo, V* hi, int sweeps) {
-  typedef MkNum<V> N;
-  const V INF = N::inf();
   const int nr = P.p->nrows;
   for (int s = 0; s < sweeps; ++s) {
     bool changed = false;
-    for (int r = 0; r < nr; ++r) {
+    for (int r = 0; r < nr;) {
       const mk_row row = P.rows[r];
-      const mk_row_term* T = P.terms + row.term_off;
-      V fmin = N::ld(row.c0), fmax = fmin;
-      int nmin_inf = 0, nmax_inf = 0;
-      for (int k = 0; k < row.nterms; ++k) {
-        V c = N::ld(T[k].coef);
-        int v = T[k].var;
-        V a = N::mul(c, lo[v]), b = N::mul(c, hi[v]);
-        V mn = mk_min(a, b), mx = mk_max(a, b);
-        if (N::kWide && mn == -INF) nmin_inf++; else fmin = N::add(fmin, mn);
-        if (N::kWide && mx == INF) nmax_inf++; else fmax = N::add(fmax, mx);
+      V fmin, fmax;
+      int nmin_inf, nmax_inf;
+      if (row.group == 0) {
+        const mk_row_term* T = P.terms + row.term_off;
+        mk_row_range<V>(row, T, lo, hi, fmin, fmax, nmin_inf, nmax_inf);
+        if (mk_row_dead<V>(row, fmin, fmax, nmin_inf, nmax_inf)) return false;
+        if (!mk_row_tighten<V>(row, T, lo, hi, fmin, fmax, nmin_inf, nmax_inf, changed))
+          return false;
+        ++r;
+        continue;
       }
-      if (nmin_inf == 0 && fmin > 0 && fmin != INF) return false;  // sum >= fmin > 0
-      if (N::kWide && nmin_inf == 0 && fmin == INF) return false;
-      if (row.rel == 1 && nmax_inf == 0 && fmax < 0 && fmax != -INF) return false;
-      if (N::kWide && row.rel == 1 && nmax_inf == 0 && fmax == -INF) return false;
-      for (int k = 0; k < row.nterms; ++k) {
-        V c = N::ld(T[k].coef);
-        int v = T[k].var;
-        V a = N::mul(c, lo[v]), b = N::mul(c, hi[v]);
-        V mn = mk_min(a, b), mx = mk_max(a, b);
-        // others_min = fmin - mn (when finite)
-        int oinf = nmin_inf - ((N::kWide && mn == -INF) ? 1 : 0);
-        if (oinf == 0) {
-          V omin = (N::kWide && mn == -INF) ? fmin : N::sub(fmin, mn);
-          if (!N::isinf(omin)) {
-            // c*x <= -omin
-            if (c > 0) {
-              V nb = mk_floordiv<V>(-omin, c);
-              if (nb < hi[v]) { hi[v] = nb; changed = true; }
-            } else {
-              V nb = mk_ceildiv<V>(-omin, c);
-              if (nb > lo[v]) { lo[v] = nb; changed = true; }
-            }
-          }
+      // disjunctive group [r, e): find its live rows
+      int e = r + 1;
+      while (e < nr && P.rows[e].group == row.group) ++e;
+      int live = -1, nlive = 0;
+      for (int q = r; q < e && nlive < 2; ++q) {
+        const mk_row rq = P.rows[q];
+        mk_row_range<V>(rq, P.terms + rq.term_off, lo, hi, fmin, fmax, nmin_inf, nmax_inf);
+        if (!mk_row_dead<V>(rq, fmin, fmax, nmin_inf, nmax_inf)) {
+          live = q;
+          ++nlive;
         }
-        if (row.rel == 1) {
-          int oinf2 = nmax_inf - ((N::kWide && mx == INF) ? 1 : 0);
-          if (oinf2 == 0) {
-            V omax = (N::kWide && mx == INF) ? fmax : N::sub(fmax, mx);
-            if (!N::isinf(omax)) {
-              // c*x >= -omax
-              if (c > 0) {
-                V nb = mk_ceildiv<V>(-omax, c);
-                if (nb > lo[v]) { lo[v] = nb; changed = true; }
-              } else {
-                V nb = mk_floordiv<V>(-omax, c);
-                if (nb < hi[v]) { hi[v] = nb; changed = true; }
-              }
-            }
-          }
-        }
-        if (lo[v] > hi[v]) return false;
       }
+      if (nlive == 0) return false;
+      if (nlive == 1) {
+        const mk_row rl = P.rows[live];
+        const mk_row_term* T = P.terms + rl.term_off;
+        mk_row_range<V>(rl, T, lo, hi, fmin, fmax, nmin_inf, nmax_inf);
+        if (!mk_row_tighten<V>(rl, T, lo, hi, fmin, fmax, nmin_inf, nmax_inf, changed))
+          return false;
+      }
+      r = e;
     }
     if (!changed) break;
   }

@@ -1625,5 +1625,66 @@ extern "C" int mk_site_eval(mk_ctx* ctx, const mk_problem_set* set, const mk_lim
   return run_adaptive(ctx, &ctx->scratch, lim, status, point, stats, t0);
 }
 
+// -- INT32 issue microbenchmark (roofline denominator) --------------------------------
+// 8 independent chains per thread; each step of a chain is four PTX integer
+// instructions kept verbatim by asm volatile -- add (IADD3), lop3 (LOP3),
+// min (VIMNMX) and mad.lo (IMAD) -- so one step retires exactly 4 integer
+// thread-instructions (the SASS count is in profiles/int_peak_r02.json).
+// Seeds come from the launch arguments and the result is stored under a
+// condition that never holds at run time, so nothing is folded away.
+namespace {
+constexpr int kPeakChains = 8;
+constexpr int kPeakOpsPerStep = 4;
+__global__ void __launch_bounds__(256) k_int_peak(uint32_t seed, int iters, uint32_t* sink) {
+  uint32_t a[kPeakChains], b[kPeakChains];
+#pragma unroll
+  for (int c = 0; c < kPeakChains; ++c) {
+    a[c] = seed ^ (threadIdx.x * 0x9e3779b9u + c);
+    b[c] = seed + blockIdx.x * 7u + c;
+  }
+#pragma unroll 4
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kPeakChains; ++c) {
+      uint32_t x, y, z;
+      asm volatile("add.u32 %0, %1, %2;" : "=r"(x) : "r"(a[c]), "r"(b[c]));
+      asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(y) : "r"(x), "r"(b[c]), "r"(a[c]));
+      asm volatile("min.u32 %0, %1, %2;" : "=r"(z) : "r"(y), "r"(x));
+      asm volatile("mad.lo.u32 %0, %1, 16777619, %2;" : "=r"(a[c]) : "r"(z), "r"(y));
+      b[c] = x;
+    }
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int c = 0; c < kPeakChains; ++c) acc ^= a[c] ^ b[c];
+  if (acc == 0x7fffffffu && seed == 0x12345u) sink[0] = acc;
+}
+}  // namespace
+
+extern "C" int mk_int_peak(mk_ctx* ctx, double* ops_per_s, double* ms) {
+  if (!ctx || !ops_per_s) return fail(ctx, MK_EINVAL, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  uint32_t* sink = nullptr;
+  CK(cudaMalloc(&sink, 64));
+  const int threads = 256, ctas = ctx->sms * 4, iters = 1 << 14;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  k_int_peak<<<ctas, threads, 0, ctx->stream>>>(0x9u, 256, sink);  // warm-up
+  CK(cudaEventRecord(e0, ctx->stream));
+  k_int_peak<<<ctas, threads, 0, ctx->stream>>>(0x9u, iters, sink);
+  CK(cudaEventRecord(e1, ctx->stream));
+  CK(cudaEventSynchronize(e1));
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  double ops = (double)ctas * threads * iters * kPeakChains * kPeakOpsPerStep;
+  *ops_per_s = ops / (t * 1e-3);
+  if (ms) *ms = t;
+  return MK_OK;
+}
+
 #include "mk_race.cuh"
 #include "mk_access.cuh"

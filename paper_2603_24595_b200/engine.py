@@ -72,34 +72,100 @@ class CompilePool:
 
     Sites are independent, so a batch of queries is compiled in parallel on
     the host cores (the compiler is pure Python; one process per core side
-    steps the GIL).  Workers are forked once per checker and only ever run
-    the pure-Python compiler (they never touch the parent's CUDA context)."""
+    steps the GIL).  The workers are fresh interpreters
+    (``python -m paper_2603_24595_b200.compile_worker``) started once per
+    checker, never forks of the checker's process: a fork would copy the
+    CUDA context and, under torchrun, NCCL threads holding locks.  Requests
+    and results travel as length-prefixed pickles over the workers' pipes;
+    one host thread per worker pulls the next chunk of the batch (longest
+    queries first) as soon as its worker is free."""
 
     def __init__(self, workers: int) -> None:
-        import multiprocessing as mp
-        from concurrent.futures import ProcessPoolExecutor
+        import subprocess
+        import sys
 
-        ctx = mp.get_context("fork")
+        pkg_root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        env = dict(os.environ)
+        env["PYTHONPATH"] = pkg_root + os.pathsep + env.get("PYTHONPATH", "")
         self.workers = workers
-        self.pool = ProcessPoolExecutor(workers, mp_context=ctx)
-        # start every worker now, outside any timed region
-        list(self.pool.map(_compile_one, [([], OriginLookup({}))] * workers))
+        self.procs = [subprocess.Popen([sys.executable, "-m", __package__ + ".compile_worker"],
+                                       stdin=subprocess.PIPE, stdout=subprocess.PIPE, env=env)
+                      for _ in range(workers)]
+        # every worker answers one empty request before any timed use
+        for p in self.procs:
+            self._send(p, [])
+        for p in self.procs:
+            self._recv(p)
+
+    @staticmethod
+    def _send(proc, obj) -> None:
+        import pickle
+        import struct
+
+        data = pickle.dumps(obj, protocol=pickle.HIGHEST_PROTOCOL)
+        proc.stdin.write(struct.pack("<Q", len(data)) + data)
+        proc.stdin.flush()
+
+    @staticmethod
+    def _recv(proc):
+        import pickle
+        import struct
+
+        head = proc.stdout.read(8)
+        if len(head) != 8:
+            raise RuntimeError("compile worker exited")
+        (n,) = struct.unpack("<Q", head)
+        got = pickle.loads(proc.stdout.read(n))
+        if isinstance(got, BaseException):
+            raise got
+        return got
 
     def compile(self, queries) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
+        import threading
+
         items = [_portable(q) for q in queries]
         # longest first (cost ~ assertion count): the big queries start in the
         # first wave and the small ones fill the gaps, so the batch's critical
         # path is close to its largest query
         order = sorted(range(len(items)), key=lambda i: -len(items[i][0]))
         chunk = max(1, -(-len(items) // (self.workers * 4)))
-        done = list(self.pool.map(_compile_one, [items[i] for i in order], chunksize=chunk))
+        chunks = [order[k:k + chunk] for k in range(0, len(order), chunk)]
         out: List[Tuple[Optional[CompiledQuery], Optional[str]]] = [None] * len(items)  # type: ignore
-        for i, r in zip(order, done):
-            out[i] = r
+        lock = threading.Lock()
+        errors: List[BaseException] = []
+
+        def drive(proc) -> None:
+            while True:
+                with lock:
+                    if not chunks or errors:
+                        return
+                    idxs = chunks.pop(0)
+                try:
+                    self._send(proc, [items[i] for i in idxs])
+                    for i, r in zip(idxs, self._recv(proc)):
+                        out[i] = r
+                except BaseException as exc:  # surfaced to the caller below
+                    with lock:
+                        errors.append(exc)
+                    return
+
+        threads = [threading.Thread(target=drive, args=(p,)) for p in self.procs]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
         return out
 
     def close(self) -> None:
-        self.pool.shutdown(wait=False, cancel_futures=True)
+        for p in self.procs:
+            try:
+                p.stdin.close()
+                p.wait(timeout=5)
+            except Exception:
+                p.kill()
+        self.procs = []
 
 
 def default_workers() -> int:

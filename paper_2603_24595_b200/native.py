@@ -40,7 +40,7 @@ PROBLEM = np.dtype([("nvars", "<i4"), ("ninsn", "<i4"), ("nregs", "<i4"), ("nato
                     ("nconst", "<i4"), ("nrows", "<i4"), ("var_off", "<i4"),
                     ("insn_off", "<i4"), ("const_off", "<i4"), ("atom_off", "<i4"),
                     ("row_off", "<i4"), ("flags", "<i4"), ("maxmask", "<u8")])
-ROW = np.dtype([("rel", "<i4"), ("nterms", "<i4"), ("term_off", "<i4"), ("pad", "<i4"),
+ROW = np.dtype([("rel", "<i4"), ("nterms", "<i4"), ("term_off", "<i4"), ("group", "<i4"),
                 ("c0", I128)])
 ROW_TERM = np.dtype([("var", "<i4"), ("pad0", "<i4"), ("pad1", "<i8"), ("coef", I128)])
 assert PROBLEM.itemsize == 56 and INSN.itemsize == 12 and ROW.itemsize == 32
@@ -153,6 +153,9 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
                                   ctypes.POINTER(RaceResult)]
     lib.mk_access_sweep.argtypes = [ctypes.c_void_p, ctypes.POINTER(AccessInput),
                                     ctypes.POINTER(AccessResult)]
+    if hasattr(lib, "mk_int_peak"):       # device library only (not the test emulator)
+        lib.mk_int_peak.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double)]
     return lib
 
 
@@ -224,8 +227,9 @@ class PackedSet:
             consts.extend(p.consts)
             atom_regs.extend(p.atom_regs)
             atom_masks.extend(p.atom_masks)
-            for rel, c0, tl in p.rows:
-                rows.append((rel, len(tl), len(terms), c0))
+            for row in p.rows:
+                rel, c0, tl = row[:3]
+                rows.append((rel, len(tl), len(terms), c0, row[3] if len(row) > 3 else 0))
                 terms.extend(tl)
         self.var_lo = _i128_array(lo)
         self.var_hi = _i128_array(hi)
@@ -241,7 +245,8 @@ class PackedSet:
         self.atom_regs = np.asarray(atom_regs, dtype=np.int32)
         self.atom_masks = np.asarray(atom_masks, dtype=np.uint64)
         self.rows = np.zeros(len(rows), dtype=ROW)
-        for i, (rel, nt, off, c0) in enumerate(rows):
+        for i, (rel, nt, off, c0, grp) in enumerate(rows):
+            self.rows[i]["group"] = grp
             self.rows[i]["rel"] = rel
             self.rows[i]["nterms"] = nt
             self.rows[i]["term_off"] = off
@@ -374,6 +379,17 @@ class Engine:
             msg = self.lib.mk_last_error(self.ctx)
             raise RuntimeError(f"mk_access_sweep failed ({rc}): {msg.decode() if msg else ''}")
         return out.as_dict()
+
+    def int_peak(self) -> dict:
+        """Measured INT32 issue rate of this device (mk_int_peak): integer
+        thread-instructions per second of the IADD3/LOP3/VIMNMX/IMAD
+        microbenchmark, the denominator of the evaluator's roofline."""
+        ops, ms = ctypes.c_double(), ctypes.c_double()
+        rc = self.lib.mk_int_peak(self.ctx, ctypes.byref(ops), ctypes.byref(ms))
+        if rc != 0:
+            msg = self.lib.mk_last_error(self.ctx)
+            raise RuntimeError(f"mk_int_peak failed ({rc}): {msg.decode() if msg else ''}")
+        return {"ops_per_s": ops.value, "ms": ms.value}
 
     # -- device-resident sets ------------------------------------------------------
 

@@ -7,6 +7,9 @@ split the work.
     each rank decides its own entries with no data-path collective.  One
     ``all_gather_object`` hands every rank the full result list at the end.
 
+``check_sites``  -- one site set, the sites dealt to ranks (each site is an
+    independent query); one ``all_gather_object`` of the verdict records.
+
 ``check_slabbed`` -- one site set, every problem's root box cut into
     ``world`` slabs along its first splittable symbol; rank r searches slab r
     (so one hard query uses every GPU).  The per-problem results are combined
@@ -89,6 +92,30 @@ def check_corpus(checker: SiteChecker, entries: Sequence[Sequence[Query]], group
     for part in gathered:
         merged.update(part or {})
     return [merged[i] for i in range(len(entries))]
+
+
+def check_sites(checker: SiteChecker, queries: Sequence[Query], group=None
+                ) -> List[QueryResult]:
+    """Decide one site set across the ranks of ``group``: sites are
+    independent queries (each is one ``Solver.check`` + canonicalisation in
+    the reference, engine/detectors.py:111-130), dealt longest-first by
+    assertion count; each rank compiles and decides its share in one device
+    batch, and one ``all_gather_object`` of the (index, verdict, witness)
+    records gives every rank the ordered result list.  No data-path
+    collective: the records are a few KB."""
+    rank, world = _world(group)
+    if world == 1:
+        return checker.check_queries(queries)
+    mine = deal([float(1 + len(a)) for a, _ in queries], world)[rank]
+    got = checker.check_queries([queries[i] for i in mine]) if mine else []
+    local = {i: (r.status, r.witness, r.reason) for i, r in zip(mine, got)}
+    dist = _dist()
+    gathered: List[Optional[Dict[int, tuple]]] = [None] * world
+    dist.all_gather_object(gathered, local, group=group)
+    merged: Dict[int, tuple] = {}
+    for part in gathered:
+        merged.update(part or {})
+    return [QueryResult(*merged[i]) for i in range(len(queries))]
 
 
 # -- slab sharding ----------------------------------------------------------------------
@@ -197,7 +224,11 @@ def check_slabbed(checker: SiteChecker, queries: Sequence[Query], group=None,
     local = [next(it) if p is not None else ("unsat", None) for p in mine]
     if world > 1:
         if device is None:
-            device = "cpu"
+            # NCCL only moves device tensors; gloo (the CPU tests) host ones
+            import torch
+
+            nccl = _dist().get_backend(group) == "nccl"
+            device = f"cuda:{torch.cuda.current_device()}" if nccl else "cpu"
         recs = _all_gather_records(_encode(problems, local), device, group)
         per_rank = [_decode(problems, r) for r in recs]
     else:

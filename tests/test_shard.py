@@ -37,6 +37,8 @@ def _worker(rank, world, port, mode, names, out_dir):
     try:
         if mode == "slab":
             res = [shard.check_slabbed(chk, gqueries(gload(n))) for n in names]
+        elif mode == "sites":
+            res = [shard.check_sites(chk, gqueries(gload(n))) for n in names]
         else:
             res = shard.check_corpus(chk, [gqueries(gload(n)) for n in names])
         with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
@@ -62,7 +64,7 @@ class _R:
         self.status, self.witness = status, witness
 
 
-@pytest.mark.parametrize("mode", ["slab", "corpus"])
+@pytest.mark.parametrize("mode", ["slab", "corpus", "sites"])
 def test_two_rank_gloo_matches_goldens(mode, tmp_path):
     names = ["racy", "rms_norm", "moe_align_mixtral"]
     outs = _run(mode, names, tmp_path)
