@@ -247,6 +247,8 @@ typedef struct mk_race_result {
   uint64_t first_key, first_id, first_idx, last_key, last_id, last_idx;
   int64_t off_lo;       /* key -> byte offset: key / nblocks + off_lo */
   uint64_t nblocks;
+  int32_t sort_passes;  /* onesweep digit passes the HBM sort ran (mk_sort.cuh) */
+  int32_t pad;
 } mk_race_result;
 
 int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_result* out);
@@ -309,9 +311,21 @@ typedef struct mk_access_result {
   double gen_ms, sort_ms, scan_ms;
   int32_t fast;          /* 1: decided by the owner-table pass (no sort) */
   int32_t jit;           /* 1: generator specialised at run time (NVRTC) */
+  int32_t sort_passes;   /* onesweep digit passes the HBM sort ran (mk_sort.cuh) */
+  int32_t pad;
 } mk_access_result;
 
 int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access_result* out);
+
+/* ---------------------------------------------------------------------
+ * The K2 HBM sort on its own (the stable radix sort both race sweeps use,
+ * csrc/mk_sort.cuh): sorts n (key, value) pairs on the low `bits` key bits,
+ * host buffers in and out (copied to HBM, sorted, copied back).  *ms = the
+ * device time of the sort (CUDA events; copies excluded), *passes = digit
+ * passes run.  force != 0 runs every digit pass even when the keys arrive
+ * ordered (measurement).  Exposed for the parity tests and the benchmark. */
+int mk_sort_pairs_u64(mk_ctx* ctx, uint64_t* keys, uint64_t* vals, uint64_t n, int32_t bits,
+                      int32_t force, double* ms, int32_t* passes);
 
 /* ---------------------------------------------------------------------
  * INT32 issue peak of this device, measured:

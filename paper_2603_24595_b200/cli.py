@@ -94,13 +94,12 @@ def cmd_analyze(a) -> int:
 
 def cmd_infer(a) -> int:
     _reference()
-    from minikernel.context import context_to_json, infer_context, parse_log
+    from .context import infer_context_json
 
     with open(a.log) as fh:
-        log = parse_log(fh.read(), a.log)
-    ctx = infer_context(log, a.kernel)
+        text = infer_context_json(fh.read(), a.kernel, a.log)
     with open(a.out, "w") as fh:
-        fh.write(context_to_json(ctx))
+        fh.write(text)
     return 0
 
 

@@ -12,8 +12,10 @@
 //               evaluate the access's path bytecode (exact int64), emit one
 //               (key, val) tuple per granule the access covers, or sentinels
 //               when the path fails;
-//   cub select  order-preserving compaction of the executed tuples;
-//   cub sort    radix sort of the 64-bit keys (value = identity | slot);
+//   compact     order-preserving compaction of the executed tuples
+//               (mksort::compact, mk_sort.cuh);
+//   sort        radix sort of the 64-bit keys (value = identity | slot),
+//               mksort::sort_pairs (hand-written onesweep, mk_sort.cuh);
 //   k_acc_scan  segments of equal granule: a segment races iff its head is a
 //               write (writes sort first) and some element has another
 //               identity; the head thread walks its segment and stops at the
@@ -197,9 +199,6 @@ __global__ void __launch_bounds__(ACC_THREADS) k_acc_scan(const unsigned long lo
   }
 }
 
-struct NotAll1 {
-  __host__ __device__ bool operator()(const unsigned long long& k) const { return k != ~0ull; }
-};
 
 }  // namespace
 
@@ -271,21 +270,7 @@ extern "C" int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access
   char* base = static_cast<char*>(ds->d);
   cudaStream_t s = ctx->stream;
   const int n = (int)slots;
-  size_t cub_bytes = 0;
-  {
-    cub::DoubleBuffer<unsigned long long> kb(nullptr, nullptr), vb(nullptr, nullptr);
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, kb, vb, n > 0 ? n : 1, 0, 64, s));
-    size_t t1 = 0, t2 = 0;
-    auto flags = thrust::make_transform_iterator((const unsigned long long*)nullptr, NotAll1{});
-    CK(cub::DeviceSelect::If(nullptr, t1, (const unsigned long long*)nullptr,
-                             (unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                             n > 0 ? n : 1, NotAll1{}, s));
-    CK(cub::DeviceSelect::Flagged(nullptr, t2, (const unsigned long long*)nullptr, flags,
-                                  (unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                  n > 0 ? n : 1, s));
-    if (t1 > cub_bytes) cub_bytes = t1;
-    if (t2 > cub_bytes) cub_bytes = t2;
-  }
+  const size_t sort_ws = mksort::workspace_bytes(slots);
   size_t off = 0;
   auto place = [&](size_t bytes) {
     size_t o = off;
@@ -296,7 +281,7 @@ extern "C" int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access
   const size_t o_ctr = place(sizeof(unsigned long long) * 8);
   const size_t o_k0 = place(8ull * slots + 8), o_k1 = place(8ull * slots + 8);
   const size_t o_v0 = place(8ull * slots + 8), o_v1 = place(8ull * slots + 8);
-  const size_t o_cub = place(cub_bytes + 256);
+  const size_t o_ws = place(sort_ws);
   rc = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, off);
   if (rc) return rc;
   char* wb = static_cast<char*>(ctx->d_work);
@@ -435,11 +420,8 @@ extern "C" int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access
   unsigned long long* vc = v0;
   unsigned long long* vo = v1;
   if (h[1] != slots) {
-    size_t tb = cub_bytes;
-    CK(cub::DeviceSelect::If(wb + o_cub, tb, k0, k1, ctr + 5, n, NotAll1{}, s));
-    auto flags = thrust::make_transform_iterator((const unsigned long long*)k0, NotAll1{});
-    tb = cub_bytes;
-    CK(cub::DeviceSelect::Flagged(wb + o_cub, tb, v0, flags, v1, ctr + 5, n, s));
+    CK((mksort::compact<unsigned long long, unsigned long long>(k0, v0, k1, v1, slots, ~0ull,
+                                                               wb + o_ws, ctr + 5, s)));
     kc = k1;
     ko = k0;
     vc = v1;
@@ -450,14 +432,18 @@ extern "C" int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access
   // key bits in use (host bound: every key < 2^key_bits)
   int bits = in->key_bits;
   if (bits < 1 || bits > 64) bits = 64;
-  cub::DoubleBuffer<unsigned long long> kb(kc, ko), vb(vc, vo);
   const unsigned long long m = h[1];
+  unsigned long long* ks = kc;
+  unsigned long long* vs = vc;
   {
-    size_t tb = cub_bytes;
-    CK(cub::DeviceRadixSort::SortPairs(wb + o_cub, tb, kb, vb, (int)m, 0, bits, s));
+    mksort::SortInfo si{};
+    CK((mksort::sort_pairs<unsigned long long, unsigned long long>(kc, vc, ko, vo, m, bits,
+                                                                  wb + o_ws, ctx->sms, s, &ks,
+                                                                  &vs, &si)));
+    out->sort_passes = si.passes_run;
   }
   CK(cudaEventRecord(ctx->ev[2], s));
-  k_acc_scan<<<grid, ACC_THREADS, 0, s>>>(kb.Current(), vb.Current(), ctr + 5, ctr);
+  k_acc_scan<<<grid, ACC_THREADS, 0, s>>>(ks, vs, ctr + 5, ctr);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[3], s));
   CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -467,8 +453,8 @@ extern "C" int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access
   if (out->has_race) {
     const unsigned long long i = h[4] >> 32, j = i + (h[4] & 0xffffffffull);
     unsigned long long va = 0, vb2 = 0;
-    CK(cudaMemcpy(&va, vb.Current() + i, sizeof(va), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&vb2, vb.Current() + j, sizeof(vb2), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&va, vs + i, sizeof(va), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&vb2, vs + j, sizeof(vb2), cudaMemcpyDeviceToHost));
     out->slot_a = va & 0xffffffffull;
     out->slot_b = vb2 & 0xffffffffull;
   }

@@ -29,9 +29,11 @@
 #if defined(__CUDACC__)
 #define MK_HD __host__ __device__ __forceinline__
 #define MK_HDM __host__ __device__ __forceinline__ static
+#define MK_HDF __host__ __device__ __forceinline__   /* non-static member functions */
 #else
 #define MK_HD static inline
 #define MK_HDM static inline
+#define MK_HDF inline
 #endif
 
 typedef __int128 i128;
@@ -432,6 +434,91 @@ struct MkBoxVerdict {
   uint64_t und_mask;  // symbols of undecided atoms
 };
 
+// register access policies of the evaluators.  MkIvFile: one file holding
+// every register (variables and constants copied in first).  MkIvTemps: the
+// file holds only the temporaries (registers >= nvars + nconst); variables
+// are read from the box and constants from the problem's constant table, so
+// a box evaluation neither copies them nor keeps them in per-thread (local)
+// memory -- the k_search hot path.
+template <typename V>
+struct MkIvFile {
+  MkIvT<V>* R;
+  MK_HDF MkIvT<V> get(int r) const { return R[r]; }
+  MK_HDF void set(int r, const MkIvT<V>& x) { R[r] = x; }
+};
+
+template <typename V>
+struct MkIvTemps {
+  const MkProb* P;
+  const V* lo;
+  const V* hi;
+  MkIvT<V>* T;
+  int nv, base;
+  MK_HDF MkIvT<V> get(int r) const {
+    if (r >= base) return T[r - base];
+    MkIvT<V> o;
+    o.fl = MK_FL_OK;
+    if (r < nv) {
+      o.lo = lo[r];
+      o.hi = hi[r];
+    } else {
+      const V c = MkNum<V>::ld(P->consts[r - nv]);
+      o.lo = c;
+      o.hi = c;
+    }
+    return o;
+  }
+  MK_HDF void set(int r, const MkIvT<V>& x) { T[r - base] = x; }
+};
+
+template <typename V, typename Regs>
+MK_HD MkBoxVerdict mk_eval_box_impl(const MkProb& P, Regs R, int64_t* insn_count) {
+  const int n = P.p->ninsn;
+  MkBoxVerdict v;
+  v.any_false = false;
+  v.all_true = true;
+  v.overflow = false;
+  v.und_mask = 0;
+  for (int k = 0; k < n; ++k) {
+    const mk_insn in = P.insns[k];
+    switch (in.op) {
+      case MK_OP_ATOM: {
+        const MkIvT<V> r = R.get(in.a);
+        bool ok = r.fl & MK_FL_OK;
+        bool may_true = ok && r.hi == 1;
+        bool sure_true = ok && r.lo == 1 && !(r.fl & MK_FL_ERR);
+        if (!may_true) {
+          *insn_count += k + 1;
+          v.any_false = true;
+          v.all_true = false;
+          return v;
+        }
+        if (!sure_true) {
+          v.all_true = false;
+          v.und_mask |= P.atom_masks[in.b];
+        }
+        break;
+      }
+      case MK_OP_AND: R.set(in.dst, mk_iv_and(R.get(in.a), R.get(in.b))); break;
+      case MK_OP_OR: R.set(in.dst, mk_iv_or(R.get(in.a), R.get(in.b))); break;
+      case MK_OP_NOT: {
+        MkIvT<V> a = R.get(in.a), r;
+        r.lo = 1 - a.hi;
+        r.hi = 1 - a.lo;
+        r.fl = a.fl;
+        R.set(in.dst, r);
+        break;
+      }
+      case MK_OP_ITE: R.set(in.dst, mk_iv_ite(R.get(in.a), R.get(in.b), R.get(in.c))); break;
+      default: R.set(in.dst, mk_iv_binop<V>(in.op, R.get(in.a), R.get(in.b))); break;
+    }
+  }
+  *insn_count += n;
+  return v;
+}
+
+// every register in R (variables and constants copied in): the race / access
+// generators read arbitrary registers (the offset) after the evaluation
 template <typename V>
 MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const V* vlo, const V* vhi, MkIvT<V>* R,
                                int64_t* insn_count) {
@@ -449,48 +536,15 @@ MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const V* vlo, const V* vhi, MkIv
     R[nv + i].hi = c;
     R[nv + i].fl = MK_FL_OK;
   }
-  const int n = P.p->ninsn;
-  MkBoxVerdict v;
-  v.any_false = false;
-  v.all_true = true;
-  v.overflow = false;
-  v.und_mask = 0;
-  for (int k = 0; k < n; ++k) {
-    const mk_insn in = P.insns[k];
-    switch (in.op) {
-      case MK_OP_ATOM: {
-        const MkIvT<V> r = R[in.a];
-        bool ok = r.fl & MK_FL_OK;
-        bool may_true = ok && r.hi == 1;
-        bool sure_true = ok && r.lo == 1 && !(r.fl & MK_FL_ERR);
-        if (!may_true) {
-          *insn_count += k + 1;
-          v.any_false = true;
-          v.all_true = false;
-          return v;
-        }
-        if (!sure_true) {
-          v.all_true = false;
-          v.und_mask |= P.atom_masks[in.b];
-        }
-        break;
-      }
-      case MK_OP_AND: R[in.dst] = mk_iv_and(R[in.a], R[in.b]); break;
-      case MK_OP_OR: R[in.dst] = mk_iv_or(R[in.a], R[in.b]); break;
-      case MK_OP_NOT: {
-        MkIvT<V> a = R[in.a], r;
-        r.lo = 1 - a.hi;
-        r.hi = 1 - a.lo;
-        r.fl = a.fl;
-        R[in.dst] = r;
-        break;
-      }
-      case MK_OP_ITE: R[in.dst] = mk_iv_ite(R[in.a], R[in.b], R[in.c]); break;
-      default: R[in.dst] = mk_iv_binop<V>(in.op, R[in.a], R[in.b]); break;
-    }
-  }
-  *insn_count += n;
-  return v;
+  return mk_eval_box_impl<V>(P, MkIvFile<V>{R}, insn_count);
+}
+
+// temporaries only in T (registers nvars + nconst ... nregs - 1)
+template <typename V>
+MK_HD MkBoxVerdict mk_eval_box_t(const MkProb& P, const V* vlo, const V* vhi, MkIvT<V>* T,
+                                 int64_t* insn_count) {
+  const int nv = P.p->nvars;
+  return mk_eval_box_impl<V>(P, MkIvTemps<V>{&P, vlo, vhi, T, nv, nv + P.p->nconst}, insn_count);
 }
 
 // ---------------------------------------------------------------------------
@@ -635,18 +689,36 @@ struct MkCvT {
 typedef MkCvT<i128> MkCv;
 
 template <typename V>
-MK_HD bool mk_eval_point(const MkProb& P, const V* x, MkCvT<V>* R, bool* overflow,
-                         int64_t* insn_count) {
+struct MkCvFile {
+  MkCvT<V>* R;
+  MK_HDF MkCvT<V> get(int r) const { return R[r]; }
+  MK_HDF void set(int r, const MkCvT<V>& x) { R[r] = x; }
+};
+
+template <typename V>
+struct MkCvTemps {
+  const MkProb* P;
+  const V* x;
+  MkCvT<V>* T;
+  int nv, base;
+  MK_HDF MkCvT<V> get(int r) const {
+    if (r >= base) return T[r - base];
+    MkCvT<V> o;
+    o.err = 0;
+    o.v = r < nv ? x[r] : MkNum<V>::ld(P->consts[r - nv]);
+    return o;
+  }
+  MK_HDF void set(int r, const MkCvT<V>& v) { T[r - base] = v; }
+};
+
+template <typename V, typename Regs>
+MK_HD bool mk_eval_point_impl(const MkProb& P, Regs R, bool* overflow, int64_t* insn_count) {
   typedef MkNum<V> N;
-  const int nv = P.p->nvars;
-  const int nc = P.p->nconst;
-  for (int i = 0; i < nv; ++i) { R[i].v = x[i]; R[i].err = 0; }
-  for (int i = 0; i < nc; ++i) { R[nv + i].v = N::ld(P.consts[i]); R[nv + i].err = 0; }
   const int n = P.p->ninsn;
   bool ovf = false;
   for (int k = 0; k < n; ++k) {
     const mk_insn in = P.insns[k];
-    const MkCvT<V> a = R[in.a], b = R[in.b];
+    const MkCvT<V> a = R.get(in.a), b = R.get(in.b);
     if (in.op == MK_OP_ATOM) {
       if (a.err || !a.v) {
         *insn_count += k + 1;
@@ -669,7 +741,7 @@ MK_HD bool mk_eval_point(const MkProb& P, const V* x, MkCvT<V>* R, bool* overflo
         r.err = a.err; r.v = a.v ? 0 : 1;
         break;
       case MK_OP_ITE: {
-        const MkCvT<V> c = R[in.c];
+        const MkCvT<V> c = R.get(in.c);
         if (a.err) r.err = 1; else r = a.v ? b : c;
         break;
       }
@@ -703,11 +775,31 @@ MK_HD bool mk_eval_point(const MkProb& P, const V* x, MkCvT<V>* R, bool* overflo
         }
       }
     }
-    R[in.dst] = r;
+    R.set(in.dst, r);
   }
   *insn_count += n;
   if (ovf) *overflow = true;
   return true;
+}
+
+template <typename V>
+MK_HD bool mk_eval_point(const MkProb& P, const V* x, MkCvT<V>* R, bool* overflow,
+                         int64_t* insn_count) {
+  typedef MkNum<V> N;
+  const int nv = P.p->nvars;
+  const int nc = P.p->nconst;
+  for (int i = 0; i < nv; ++i) { R[i].v = x[i]; R[i].err = 0; }
+  for (int i = 0; i < nc; ++i) { R[nv + i].v = N::ld(P.consts[i]); R[nv + i].err = 0; }
+  return mk_eval_point_impl<V>(P, MkCvFile<V>{R}, overflow, insn_count);
+}
+
+// temporaries only in T (the k_search leaf enumeration)
+template <typename V>
+MK_HD bool mk_eval_point_t(const MkProb& P, const V* x, MkCvT<V>* T, bool* overflow,
+                           int64_t* insn_count) {
+  const int nv = P.p->nvars;
+  return mk_eval_point_impl<V>(P, MkCvTemps<V>{&P, x, T, nv, nv + P.p->nconst}, overflow,
+                               insn_count);
 }
 
 // lexicographic comparison in witness order: true when x is strictly better

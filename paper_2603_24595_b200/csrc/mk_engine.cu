@@ -346,8 +346,8 @@ __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo,
   if constexpr (SH != 0) {
     v = sh_eval_box(P, lo, hi, mk_dyn_sh, mk_dyn_sh + SH_R * blockDim.x, &cnt);
   } else {
-    MkIvT<V> R[CAPR];
-    v = mk_eval_box(P, lo, hi, R, &cnt);
+    MkIvT<V> R[CAPR];   // temporaries only: variables and constants are read in place
+    v = mk_eval_box_t(P, lo, hi, R, &cnt);
   }
   st.insns_bb += (unsigned long long)cnt;
   if (v.any_false) {
@@ -506,7 +506,7 @@ __device__ void warp_enumerate(const DevSet& D, int pid, const mk_problem& p, co
         model = sh_eval_point(P, x, mk_dyn_sh);
         cnt += p.ninsn;
       } else {
-        model = mk_eval_point(P, x, R, &ovf, &cnt);
+        model = mk_eval_point_t(P, x, R, &ovf, &cnt);
       }
     }
     unsigned m = __ballot_sync(FULL, model);
@@ -1688,3 +1688,44 @@ extern "C" int mk_int_peak(mk_ctx* ctx, double* ops_per_s, double* ms) {
 
 #include "mk_race.cuh"
 #include "mk_access.cuh"
+
+extern "C" int mk_sort_pairs_u64(mk_ctx* ctx, uint64_t* keys, uint64_t* vals, uint64_t n,
+                                 int32_t bits, int32_t force, double* ms, int32_t* passes) {
+  if (!ctx || (n && (!keys || !vals))) return fail(ctx, MK_EINVAL, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const size_t tb = 8ull * (n + 1);
+  size_t off = 0;
+  auto place = [&](size_t bytes) {
+    size_t o = off;
+    off = (off + bytes + 255) / 256 * 256;
+    return o;
+  };
+  const size_t o_k0 = place(tb), o_k1 = place(tb), o_v0 = place(tb), o_v1 = place(tb);
+  const size_t o_ws = place(mksort::workspace_bytes(n));
+  int rc = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, off);
+  if (rc) return rc;
+  char* wb = static_cast<char*>(ctx->d_work);
+  typedef unsigned long long u64;
+  u64* k0 = reinterpret_cast<u64*>(wb + o_k0);
+  u64* k1 = reinterpret_cast<u64*>(wb + o_k1);
+  u64* v0 = reinterpret_cast<u64*>(wb + o_v0);
+  u64* v1 = reinterpret_cast<u64*>(wb + o_v1);
+  CK(cudaMemcpyAsync(k0, keys, 8 * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(v0, vals, 8 * n, cudaMemcpyHostToDevice, s));
+  u64* ks = k0;
+  u64* vs = v0;
+  mksort::SortInfo si{};
+  CK(cudaEventRecord(ctx->ev[0], s));
+  CK((mksort::sort_pairs<u64, u64>(k0, v0, k1, v1, n, bits, wb + o_ws, ctx->sms, s, &ks, &vs, &si,
+                                  force != 0)));
+  CK(cudaEventRecord(ctx->ev[1], s));
+  CK(cudaMemcpyAsync(keys, ks, 8 * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(vals, vs, 8 * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  float t = 0.f;
+  cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]);
+  if (ms) *ms = t;
+  if (passes) *passes = si.passes_run;
+  return MK_OK;
+}

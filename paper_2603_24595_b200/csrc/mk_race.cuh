@@ -14,13 +14,14 @@
 //                lexicographic order, evaluate the path bytecode in exact
 //                int64, write (key, instance index) to the instance's slot
 //                (a sentinel key when the path fails);
-//   cub::DeviceRadixSort::SortPairs over the key bits in HBM;
+//   mksort::sort_pairs (mk_sort.cuh, hand-written onesweep LSD radix sort)
+//                over the key bits in HBM;
 //   k_race_scan  adjacent tuples with equal key and distinct identity are a
 //                conflict (every race has at least one adjacent witness
 //                pair after the sort); warp-aggregated count + atomicMin of
 //                the first conflicting position.
 
-#include <thrust/iterator/transform_iterator.h>
+#include "mk_sort.cuh"
 
 namespace {
 
@@ -185,22 +186,38 @@ __global__ void __launch_bounds__(RACE_THREADS) k_race_scan(RaceDev R, const K* 
 // [4] out-of-order flag [5] key of the first conflict.
 constexpr int MK_RACE_REC = 10;
 
-struct MaxInt {
-  __device__ int operator()(int a, int b) const { return a > b ? a : b; }
-};
+// exclusive max-scan over a 1024-thread block (identity -1): warp shuffles,
+// then the 32 warp maxima
+__device__ __forceinline__ int block_excl_max_1024(int x) {
+  __shared__ int wmax[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o && a > incl) incl = a;
+  }
+  if (lane == 31) wmax[warp] = incl;
+  __syncthreads();
+  int before = -1;
+  for (int w = 0; w < warp; ++w)
+    if (wmax[w] > before) before = wmax[w];
+  int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = -1;
+  const int out = excl > before ? excl : before;
+  __syncthreads();
+  return out;
+}
 
 __global__ void __launch_bounds__(1024) k_race_bound(const unsigned long long* rec, int W,
                                                      unsigned long long* ctr) {
-  typedef cub::BlockScan<int, 1024> Scan;
-  __shared__ typename Scan::TempStorage tmp;
   const int per = (W + 1023) / 1024;
   const int b = threadIdx.x * per;
   const int e = min(W, b + per);
   int last = -1;
   for (int w = b; w < e; ++w)
     if (rec[(size_t)w * MK_RACE_REC]) last = w;
-  int prev = -1;
-  Scan(tmp).ExclusiveScan(last, prev, -1, MaxInt());
+  int prev = block_excl_max_1024(last);
   const int prev0 = prev;
   // the range's first and last access (shard combination across GPUs)
   __shared__ int s_first, s_last;
@@ -266,12 +283,6 @@ __global__ void __launch_bounds__(1024) k_race_bound(const unsigned long long* r
   }
 }
 
-template <typename K>
-struct NotSentinel {
-  K sentinel;
-  __host__ __device__ bool operator()(const K& k) const { return k != sentinel; }
-};
-
 }  // namespace
 
 
@@ -312,22 +323,8 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
                     mk_race_result* out, char* base, unsigned long long* ctr,
                     const mk_race_prog* prog, const int64_t* hlo, const int64_t* hhi) {
   cudaStream_t s = ctx->stream;
-  // tuples: keys + values, double buffered for the sort
-  size_t cub_bytes = 0;
-  {
-    cub::DoubleBuffer<K> kb(nullptr, nullptr);
-    cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
-    cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, kb, vb, (int)vol, 0, bits, s);
-    size_t t1 = 0, t2 = 0;
-    NotSentinel<K> pred{(K)0};
-    auto flags = thrust::make_transform_iterator((const K*)nullptr, pred);
-    cub::DeviceSelect::If(nullptr, t1, (const K*)nullptr, (K*)nullptr,
-                          (unsigned long long*)nullptr, (int)vol, pred, s);
-    cub::DeviceSelect::Flagged(nullptr, t2, (const uint32_t*)nullptr, flags, (uint32_t*)nullptr,
-                               (unsigned long long*)nullptr, (int)vol, s);
-    if (t1 > cub_bytes) cub_bytes = t1;
-    if (t2 > cub_bytes) cub_bytes = t2;
-  }
+  // tuples: keys + values, double buffered for the sort (mk_sort.cuh)
+  const size_t sort_ws = mksort::workspace_bytes(vol);
   size_t off = 0;
   auto place = [&](size_t bytes) {
     size_t o = off;
@@ -336,7 +333,7 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   };
   const size_t o_k0 = place(sizeof(K) * vol), o_k1 = place(sizeof(K) * vol);
   const size_t o_v0 = place(sizeof(uint32_t) * vol), o_v1 = place(sizeof(uint32_t) * vol);
-  const size_t o_cub = place(cub_bytes + 256);
+  const size_t o_ws = place(sort_ws);
   int rc = ensure(ctx, &ctx->d_work, &ctx->d_work_bytes, off);
   if (rc) return rc;
   char* wb = static_cast<char*>(ctx->d_work);
@@ -490,12 +487,7 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   if (h[0] == vol) {
     CK(cudaMemcpyAsync(ctr + 5, &vol, sizeof(vol), cudaMemcpyHostToDevice, s));
   } else {
-    NotSentinel<K> pred{sentinel};
-    auto flags = thrust::make_transform_iterator((const K*)k0, pred);
-    size_t tb = cub_bytes;
-    CK(cub::DeviceSelect::If(wb + o_cub, tb, k0, k1, ctr + 5, (int)vol, pred, s));
-    tb = cub_bytes;
-    CK(cub::DeviceSelect::Flagged(wb + o_cub, tb, v0, flags, v1, ctr + 5, (int)vol, s));
+    CK((mksort::compact<K, uint32_t>(k0, v0, k1, v1, vol, sentinel, wb + o_ws, ctr + 5, s)));
     kc = k1;
     ko = k0;
     vc = v1;
@@ -510,20 +502,21 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   CK(cudaStreamSynchronize(s));
   if (force) h[4] = 1;
   const unsigned long long n = h[5];
-  cub::DoubleBuffer<K> kb(kc, ko);
-  cub::DoubleBuffer<uint32_t> vb(vc, vo);
+  K* ks = kc;
+  uint32_t* vs = vc;
   out->sorted = h[4] == 0;
   CK(cudaEventRecord(ctx->ev[2], s));
   if (h[4]) {
     unsigned long long reset[2] = {0ull, ~0ull};
     CK(cudaMemcpyAsync(ctr + 1, reset, sizeof(reset), cudaMemcpyHostToDevice, s));
-    if (n > 1) {
-      size_t tb = cub_bytes;
-      CK(cub::DeviceRadixSort::SortPairs(wb + o_cub, tb, kb, vb, (int)n, 0, bits, s));
-    }
+    mksort::SortInfo si{};
+    // MK_RACE_FORCE_SORT also forces every digit pass (measurement of the
+    // sort itself on keys that arrive ordered)
+    CK((mksort::sort_pairs<K, uint32_t>(kc, vc, ko, vo, n, bits, wb + o_ws, ctx->sms, s, &ks, &vs,
+                                       &si, force)));
+    out->sort_passes = si.passes_run;
     CK(cudaEventRecord(ctx->ev[2], s));
-    k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, kb.Current(), vb.Current(), ctr + 5, ctr + 1,
-                                                 ctr + 2, nullptr);
+    k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, ks, vs, ctr + 5, ctr + 1, ctr + 2, nullptr);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, s));
   }
@@ -538,9 +531,9 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
     const unsigned long long i = h[2];
     uint32_t va = 0, vb2 = 0;
     K key = 0;
-    CK(cudaMemcpy(&va, vb.Current() + i - 1, sizeof(va), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&vb2, vb.Current() + i, sizeof(vb2), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&key, kb.Current() + i, sizeof(key), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&va, vs + i - 1, sizeof(va), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&vb2, vs + i, sizeof(vb2), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&key, ks + i, sizeof(key), cudaMemcpyDeviceToHost));
     out->idx_a = va;
     out->idx_b = vb2;
     out->offset = (int64_t)((unsigned long long)key / R.nblocks) + R.off_lo;

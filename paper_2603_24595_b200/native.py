@@ -97,7 +97,8 @@ class RaceResult(ctypes.Structure):
                 ("first_key", ctypes.c_uint64), ("first_id", ctypes.c_uint64),
                 ("first_idx", ctypes.c_uint64), ("last_key", ctypes.c_uint64),
                 ("last_id", ctypes.c_uint64), ("last_idx", ctypes.c_uint64),
-                ("off_lo", ctypes.c_int64), ("nblocks", ctypes.c_uint64)]
+                ("off_lo", ctypes.c_int64), ("nblocks", ctypes.c_uint64),
+                ("sort_passes", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -124,14 +125,15 @@ class AccessResult(ctypes.Structure):
                 ("misaligned", ctypes.c_int32), ("slot_a", ctypes.c_uint64),
                 ("slot_b", ctypes.c_uint64), ("gen_ms", ctypes.c_double),
                 ("sort_ms", ctypes.c_double), ("scan_ms", ctypes.c_double),
-                ("fast", ctypes.c_int32), ("jit", ctypes.c_int32)]
+                ("fast", ctypes.c_int32), ("jit", ctypes.c_int32),
+                ("sort_passes", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
-assert ctypes.sizeof(AccessProg) == 120 and ctypes.sizeof(AccessResult) == 80
-assert ctypes.sizeof(RaceProg) == 160 and ctypes.sizeof(RaceResult) == 168
+assert ctypes.sizeof(AccessProg) == 120 and ctypes.sizeof(AccessResult) == 88
+assert ctypes.sizeof(RaceProg) == 160 and ctypes.sizeof(RaceResult) == 176
 
 
 def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
@@ -153,6 +155,11 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
                                   ctypes.POINTER(RaceResult)]
     lib.mk_access_sweep.argtypes = [ctypes.c_void_p, ctypes.POINTER(AccessInput),
                                     ctypes.POINTER(AccessResult)]
+    if hasattr(lib, "mk_sort_pairs_u64"):
+        lib.mk_sort_pairs_u64.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.POINTER(ctypes.c_double),
+                                          ctypes.POINTER(ctypes.c_int32)]
     if hasattr(lib, "mk_int_peak"):       # device library only (not the test emulator)
         lib.mk_int_peak.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
                                     ctypes.POINTER(ctypes.c_double)]
@@ -379,6 +386,21 @@ class Engine:
             msg = self.lib.mk_last_error(self.ctx)
             raise RuntimeError(f"mk_access_sweep failed ({rc}): {msg.decode() if msg else ''}")
         return out.as_dict()
+
+    def sort_pairs(self, keys: np.ndarray, vals: np.ndarray, bits: int = 64,
+                   force: bool = False) -> dict:
+        """The K2 HBM sort on host arrays (uint64, sorted in place):
+        mk_sort_pairs_u64; returns the device time and digit passes."""
+        assert keys.dtype == np.uint64 and vals.dtype == np.uint64 and keys.shape == vals.shape
+        keys = np.ascontiguousarray(keys)
+        vals = np.ascontiguousarray(vals)
+        ms, passes = ctypes.c_double(), ctypes.c_int32()
+        rc = self.lib.mk_sort_pairs_u64(self.ctx, keys.ctypes.data, vals.ctypes.data, keys.size,
+                                        bits, int(force), ctypes.byref(ms), ctypes.byref(passes))
+        if rc != 0:
+            msg = self.lib.mk_last_error(self.ctx)
+            raise RuntimeError(f"mk_sort_pairs_u64 failed ({rc}): {msg.decode() if msg else ''}")
+        return {"keys": keys, "vals": vals, "ms": ms.value, "passes": passes.value}
 
     def int_peak(self) -> dict:
         """Measured INT32 issue rate of this device (mk_int_peak): integer

@@ -86,7 +86,7 @@ void solve_problem(const mk_problem_set* set, int pid, int K, long long leaf_vol
       continue;
     }
     int64_t cnt = 0;
-    MkBoxVerdict v = mk_eval_box(P, b.lo.data(), b.hi.data(), R.data(), &cnt);
+    MkBoxVerdict v = mk_eval_box_t(P, b.lo.data(), b.hi.data(), R.data(), &cnt);
     st.insns_bb += cnt;
     if (v.any_false) {
       st.covered += vol0;
@@ -115,7 +115,7 @@ void solve_problem(const mk_problem_set* set, int pid, int K, long long leaf_vol
       for (long long idx = 0; idx < vol; ++idx) {
         mk_decode(b.lo.data(), b.hi.data(), nv, p.maxmask, (uint64_t)idx, x);
         st.points++;
-        if (mk_eval_point(P, x, C.data(), &ovf, &c2)) {
+        if (mk_eval_point_t(P, x, C.data(), &ovf, &c2)) {
           if (!has || mk_lex_better(x, best.data(), nv, p.maxmask)) {
             best.assign(x, x + nv);
             has = 1;

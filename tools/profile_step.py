@@ -14,10 +14,12 @@ import torch  # noqa: E402
 from goldens import load, queries  # noqa: E402
 from paper_2603_24595_b200.engine import SiteChecker, compile_all  # noqa: E402
 
-name = sys.argv[1] if len(sys.argv) > 1 else "rotary_embedding"
+name = sys.argv[1] if len(sys.argv) > 1 else "config3"
 torch.cuda.set_device(0)
 chk = SiteChecker(device=0, compile_workers=0)
-compiled = compile_all(queries(load(name)))
+from bench import entries, load_sites  # noqa: E402  (workload groups: config3, corpus)
+
+compiled = compile_all(load_sites(entries(name))[1])
 packed, _ = chk.pack([c for c, _ in compiled])
 res = chk.engine.upload(packed)
 lim = {"max_seconds": 600.0}
