@@ -60,6 +60,10 @@ MAX_VARS = 64        # free symbols per device problem (bit mask width)
 # host-side FBBT over the presolved rows; off: bound propagation is left to
 # the device's root contraction (mk_contract), measurement switch
 HOST_FBBT = os.environ.get("MK_HOST_FBBT", "1") != "0"
+# disjunctive contraction row groups (include/mk_b200.h mk_row.group), switch
+ROW_GROUPS = os.environ.get("MK_ROW_GROUPS", "1") != "0"
+# case split of a disjunction left after presolve (_split_disjunction), switch
+OR_SPLIT = os.environ.get("MK_OR_SPLIT", "1") != "0"
 MAX_REGS = 1024
 _AGG_WIDE = 4096
 _NEG = {"eq": "ne", "ne": "eq", "lt": "ge", "le": "gt", "gt": "le", "ge": "lt"}
@@ -120,6 +124,10 @@ class Group:
     reason: Optional[str]
     had_unsupported: bool
     problems: List[int] = field(default_factory=list)
+    # disjunct branches (_split_disjunction): (problem indices, eliminated
+    # symbol definitions, the component's symbols); the group's models are
+    # the union of the branches' models
+    alts: List[Tuple[List[int], Dict[str, Node], List[str]]] = field(default_factory=list)
 
 
 @dataclass
@@ -131,6 +139,27 @@ class CompiledQuery:
     defs: Dict[str, Node]          # eliminated symbols -> expr over free symbols
     free_default: Dict[str, int]   # symbols absent from every atom
     compile_s: float = 0.0         # host time spent compiling this query
+
+    @staticmethod
+    def _status_of(idxs: Sequence[int], results) -> str:
+        gs = "sat"
+        for pi in idxs:
+            st = results[pi][0]
+            if st == "unsat":
+                return "unsat"
+            if st != "sat":
+                gs = "unknown"
+        return gs
+
+    def _better(self, a: Dict[str, int], b: Dict[str, int], names: Sequence[str]) -> bool:
+        """a precedes b in the canonical witness order (engine/report.py:
+        177-203: ids max, everything else min) over the component's names."""
+        inside = set(names)
+        for n, d in self.order:
+            if n not in inside or n not in a or n not in b or a[n] == b[n]:
+                continue
+            return a[n] > b[n] if d == "max" else a[n] < b[n]
+        return False
 
     def assemble(self, results: Sequence[Tuple[str, Optional[List[int]]]]):
         """Combine per-problem device results into the reference verdict.
@@ -144,14 +173,12 @@ class CompiledQuery:
             if g.status == "unknown":
                 pending_unknown = True
                 continue
-            gs = "sat"
-            for pi in g.problems:
-                st = results[pi][0]
-                if st == "unsat":
-                    gs = "unsat"
-                    break
-                if st != "sat":
-                    gs = "unknown"
+            if g.alts:
+                sts = [self._status_of(idx, results) for idx, _, _ in g.alts]
+                gs = ("unsat" if all(x == "unsat" for x in sts) else
+                      "unknown" if any(x == "unknown" for x in sts) else "sat")
+            else:
+                gs = self._status_of(g.problems, results)
             if gs == "unsat":
                 if g.had_unsupported:
                     pending_unknown = True
@@ -162,11 +189,31 @@ class CompiledQuery:
         if pending_unknown:
             return "unknown", {}
         binding: Dict[str, int] = dict(self.free_default)
-        for p, (st, point) in zip(self.problems, results):
+        alt_members = {pi for g in self.groups for idx, _, _ in g.alts for pi in idx}
+        for i, (p, (st, point)) in enumerate(zip(self.problems, results)):
+            if i in alt_members:
+                continue
             for name, v in zip(p.var_names, point):
                 binding[name] = v
         for name, e in self.defs.items():
             binding[name] = ir.evaluate(e, binding)
+        for g in self.groups:
+            best = None
+            for idx, defs, names in g.alts:
+                if self._status_of(idx, results) != "sat":
+                    continue
+                b: Dict[str, int] = dict(self.free_default)
+                for pi in idx:
+                    for name, v in zip(self.problems[pi].var_names, results[pi][1]):
+                        b[name] = v
+                for name, e in defs.items():
+                    b[name] = ir.evaluate(e, b)
+                if best is None or self._better(b, best[0], names):
+                    best = (b, names)
+            if best is not None:
+                for n in best[1]:
+                    if n in best[0]:
+                        binding[n] = best[0][n]
         witness = {n: binding[n] for n in sorted(self.witness_names) if n in binding}
         return status, witness
 
@@ -640,6 +687,27 @@ class _Presolve:
         self.cuts: Set[Node] = set()
         self._lin_memo = _Lin(self.widths)
 
+    def fork(self, atoms: List[Node]) -> "_Presolve":
+        """A presolve of the same component continuing from this state with
+        ``atoms`` (the disjunct split, _compile_query)."""
+        q = _Presolve.__new__(_Presolve)
+        q.widths = dict(self.widths)
+        q.pos = dict(self.pos)
+        q.maximize = dict(self.maximize)
+        q.bounds = dict(self.bounds)
+        q.defs = dict(self.defs)
+        q.atoms = list(dict.fromkeys(atoms))
+        q.unsat = False
+        q.kcount = self.kcount
+        q.fm_rounds = 0
+        q.fbbt_passes = 0
+        q.agg_done = set(self.agg_done)
+        q._canon_memo = {}
+        q._norm_by_id = {}
+        q.cuts = set()         # a fresh cut budget for the branch's own rows
+        q._lin_memo = _Lin(q.widths)
+        return q
+
     # symbols of an IR node (memo-free; atoms are small)
     @staticmethod
     def _vars(e: Node) -> Set[str]:
@@ -835,6 +903,12 @@ class _Presolve:
         if self._try_aggregate(lin):
             return True
         if self._try_aggregate_ineq(lin):
+            return True
+        # 6b. linear relaxations of rows with bounded nonlinear terms (cuts)
+        if self._try_relax(lin):
+            return True
+        # 6c. opposite rows over one linear form that exclude each other
+        if self._try_parallel(lin):
             return True
         # 7. Fourier-Motzkin implied rows (sound cuts, never remove models)
         if self._try_fm(lin):
@@ -1267,6 +1341,75 @@ class _Presolve:
                     added = True
         return added
 
+    def _try_relax(self, lin: _Lin, max_new: int = 16) -> bool:
+        """For a row whose nonlinear (opaque) terms are bounded on the
+        current box, add the row with each such term replaced by the end of
+        its range that weakens the row: implied by the row, so the model
+        set is unchanged, and linear, so gcd aggregation, Fourier-Motzkin
+        and bound propagation can use it (paged attention's partition-local
+        logits index: 16*(4k + w - 32z) + (tx % 32) % 16 >= 512 relaxes to
+        4k + w - 32z >= 32)."""
+        ivl = _Ivl(self.bounds)
+        existing = set(self.atoms)
+        added = 0
+        for a in list(self.atoms):
+            if a[0] != "p" or a[1] != "le":
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None:
+                continue
+            terms, c = lf
+            opq = [(k, v) for k, v in terms.items() if not isinstance(k, str)]
+            sym = {k: v for k, v in terms.items() if isinstance(k, str)}
+            if not opq or not sym:
+                continue
+            shift = 0
+            for k, v in opq:
+                lo, hi = ivl(k)
+                if lo is None or hi is None:
+                    shift = None
+                    break
+                shift += min(v * lo, v * hi)
+            if shift is None:
+                continue
+            n = self._canon_cmp(lin, "le", lin_to_ir((sym, c + shift), self.widths),
+                                ("c", 0, "i64"))
+            if n == ir.FALSE:
+                self.unsat = True
+                return True
+            if n == ir.TRUE or n in existing or n in self.cuts:
+                continue
+            self.cuts.add(n)
+            existing.add(n)
+            self.atoms.append(n)
+            added += 1
+            if added >= max_new:
+                break
+        return added > 0
+
+    def _try_parallel(self, lin: _Lin) -> bool:
+        """f <= u and -f <= -l over the same symbols with l > u: no model
+        (two rows of one linear form -- a relaxation cut against a
+        Fourier-Motzkin row, say -- that bound propagation would only creep
+        towards one unit per sweep)."""
+        upper: Dict[Tuple, int] = {}
+        for a in self.atoms:
+            if a[0] != "p" or a[1] != "le":
+                continue
+            lf = self._lin_of_atom(lin, a)
+            if lf is None or not lf[0] or not all(isinstance(k, str) for k in lf[0]):
+                continue
+            key = tuple(sorted(lf[0].items()))
+            u = -lf[1]                       # sum(terms) <= -c
+            if key not in upper or u < upper[key]:
+                upper[key] = u
+        for key, u in upper.items():
+            neg = tuple(sorted((k, -v) for k, v in key))
+            if neg in upper and -upper[neg] > u:   # sum >= -u_neg > u
+                self.unsat = True
+                return True
+        return False
+
     def _try_fm(self, lin: _Lin, max_terms: int = 3, max_new: int = 16) -> bool:
         """Add Fourier-Motzkin combinations of pairs of linear rows that
         cancel one symbol.  Non-negative combinations of rows are implied by
@@ -1513,17 +1656,17 @@ class _Emitter:
         return out, nphys, atom_regs
 
 
-def _cmp_rows(lin: "_Lin", e: Node):
-    """A comparison over symbols as rows (rel, c0, terms): sum <= 0 (rel 0)
-    or sum == 0 (rel 1); ``ne`` is its two strict sides.  None when ``e``
-    is not a comparison of linear forms over symbols."""
+def _le_forms(lin: "_Lin", e: Node):
+    """A comparison as linear forms (rel, c0, terms) over symbols and opaque
+    terms: sum <= 0 (rel 0) or sum == 0 (rel 1); ``ne`` is its two strict
+    sides.  None when ``e`` is not a comparison of linear forms."""
     if e[0] != "p":
         return None
     try:
         terms, c0 = _lin_add(lin.lin(e[2]), lin.lin(e[3]), -1)
     except CompileError:
         return None
-    if not terms or not all(isinstance(k, str) for k in terms):
+    if not terms:
         return None
     neg = {k: -v for k, v in terms.items()}
     op = e[1]
@@ -1540,6 +1683,32 @@ def _cmp_rows(lin: "_Lin", e: Node):
     if op == "ne":
         return [(0, c0 + 1, terms), (0, -c0 + 1, neg)]
     return None
+
+
+def _relax(form, ivl: "_Ivl"):
+    """Contraction rows implied by one form on the root box: every opaque
+    (nonlinear) term is replaced by the end of its root-box interval that
+    makes the row weakest, so any model of the form -- a point of the root
+    box where it holds, without evaluation error -- satisfies the rows.  An
+    equality with opaque terms relaxes to its two inequalities.  Returns a
+    list of (rel, c0, symbol terms), [] when a needed interval is unbounded."""
+    rel, c0, terms = form
+    sym = {k: v for k, v in terms.items() if isinstance(k, str)}
+    opq = [(k, v) for k, v in terms.items() if not isinstance(k, str)]
+    if not opq:
+        return [(rel, c0, sym)]
+    lo_add = hi_add = 0
+    for k, v in opq:
+        lo, hi = ivl(k)
+        if lo is None or hi is None:
+            return []
+        x, y = v * lo, v * hi
+        lo_add += min(x, y)
+        hi_add += max(x, y)
+    if rel == 0:
+        return [(0, c0 + lo_add, sym)]
+    # sum == 0  ->  sym + c0 + lo_add <= 0  and  -(sym + c0 + hi_add) <= 0
+    return [(0, c0 + lo_add, sym), (0, -(c0 + hi_add), {k: -v for k, v in sym.items()})]
 
 
 def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
@@ -1573,25 +1742,54 @@ def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
     rows: List[Tuple[int, int, List[Tuple[int, int]], int]] = []
     lin = _Lin({})
     group = 0
+    seen_rows: Set[Tuple] = set()
+
+    def add_row(rel: int, c0: int, terms: Dict[str, int], grp: int) -> None:
+        key = (rel, c0, tuple(sorted(terms.items())), grp)
+        if grp == 0 and key in seen_rows:
+            return
+        seen_rows.add(key)
+        rows.append((rel, c0, [(index[k], v) for k, v in sorted(terms.items())], grp))
+
     for a in atoms:
-        if a[0] == "p" and a[1] in ("le", "eq") and a[3] == ("c", 0, "i64"):
-            terms, c0 = lin.lin(a[2])
-            if terms and all(isinstance(k, str) for k in terms):
-                rows.append((0 if a[1] == "le" else 1, c0,
-                             [(index[k], v) for k, v in sorted(terms.items())], 0))
+        forms = _le_forms(lin, a) if a[0] == "p" else None
+        if forms is not None and (a[1] != "ne" or not ROW_GROUPS):
+            # a conjunct: its rows (opaque terms relaxed to their root-box
+            # range) hold at every model
+            if a[1] == "ne":
                 continue
+            for f in forms:
+                for rel, c0, terms in _relax(f, ivl):
+                    if terms:
+                        add_row(rel, c0, terms, 0)
+                    elif c0 > 0:
+                        add_row(0, c0, {}, 0)         # no model: empty box
+            continue
+        if not ROW_GROUPS:
+            continue
         ops = a[2] if a[0] == "o" and a[1] == "or" else (a,) if a[0] == "p" and a[1] == "ne" else ()
         alts = []
         for o in ops:
-            got = _cmp_rows(lin, o)
+            got = _le_forms(lin, o)
             if got is None:
                 alts = []
                 break
-            alts.extend(got)
-        if len(alts) >= 2:
+            relaxed = []
+            for f in got:
+                r = _relax(f, ivl)
+                if len(r) != 1:          # unbounded, or an equality with opaque terms
+                    relaxed = None
+                    break
+                relaxed.append(r[0])
+            if relaxed is None:
+                alts = []
+                break
+            alts.extend(relaxed)
+        # an alternative that holds on the whole box makes the group useless
+        if len(alts) >= 2 and all(t or c0 > 0 for _, c0, t in alts):
             group += 1
             for rel, c0, terms in alts:
-                rows.append((rel, c0, [(index[k], v) for k, v in sorted(terms.items())], group))
+                add_row(rel, c0, terms, group)
     prob = Problem(var_names=var_names, lo=lo, hi=hi, maximize=maximize,
                    insns=code, consts=list(em.consts), nregs=nregs,
                    atom_regs=atom_regs, atom_masks=masks, rows=rows,
@@ -1712,6 +1910,87 @@ def _components(assertions: Sequence[Node]) -> List[List[Node]]:
     return [groups[r] for r in order]
 
 
+def _emit_component(ps: "_Presolve", problems: List[Problem]) -> List[int]:
+    """Independent device problems of one presolved component (its atoms
+    split over shared free symbols); appended to ``problems``, indices
+    returned."""
+    out: List[int] = []
+    free = [n for n in ps.bounds]
+    atom_vars = [set(ir.symbols_of(a)) for a in ps.atoms]
+    parent = {n: n for n in free}
+
+    def find(x: str) -> str:
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    for vs in atom_vars:
+        vs = list(vs)
+        for o in vs[1:]:
+            ra, rb = find(vs[0]), find(o)
+            if ra != rb:
+                parent[ra] = rb
+    buckets: Dict[str, List[int]] = {}
+    for i, vs in enumerate(atom_vars):
+        if vs:
+            buckets.setdefault(find(next(iter(vs))), []).append(i)
+    used: Set[str] = set()
+    for root, idxs in buckets.items():
+        names = sorted({n for i in idxs for n in atom_vars[i]}, key=lambda n: ps.pos[n])
+        used |= set(names)
+        lo = [ps.bounds[n][0] for n in names]
+        hi = [ps.bounds[n][1] for n in names]
+        if any(v is None for v in lo + hi):
+            raise CapacityError("unbounded free symbol after presolve")
+        mx = [ps.maximize.get(n, False) for n in names]
+        out.append(len(problems))
+        problems.append(_emit_problem(names, lo, hi, mx, [ps.atoms[i] for i in idxs]))
+    # free symbols constrained by bounds only: their optimum is a bound,
+    # still decided on the device as an atom-free problem
+    rest = sorted((n for n in free if n not in used), key=lambda n: ps.pos[n])
+    if rest:
+        lo = [ps.bounds[n][0] for n in rest]
+        hi = [ps.bounds[n][1] for n in rest]
+        if any(v is None for v in lo + hi):
+            raise CapacityError("unbounded free symbol after presolve")
+        mx = [ps.maximize.get(n, False) for n in rest]
+        out.append(len(problems))
+        problems.append(_emit_problem(rest, lo, hi, mx, []))
+    return out
+
+
+def _split_disjunction(ps: "_Presolve"):
+    """Case split on one disjunction left after presolve, as the reference
+    expands boolean paths (solver/linear.py:313-372): the component's models
+    are the union over the disjuncts of the models of (rest and disjunct).
+    Each branch is presolved on its own.  One surviving branch IS the
+    component (same model set, so the same canonical witness); two or more
+    come back as a list: the device searches each branch (its disjunct is a
+    linear row there, where the disjunction left only interval splitting)
+    and the component's witness is the best branch optimum in witness order
+    (CompiledQuery.assemble)."""
+    for a in ps.atoms:
+        if a[0] == "o" and a[1] == "or" and 2 <= len(a[2]) <= 4:
+            break
+    else:
+        return ps
+    rest = [x for x in ps.atoms if x is not a]
+    live = []
+    for d in a[2]:
+        f = ps.fork(rest + [d])
+        try:
+            f.run()
+        except CompileError:
+            return ps
+        if not f.unsat:
+            live.append(f)
+    if not live:
+        ps.unsat = True
+        return ps
+    return live[0] if len(live) == 1 else live
+
+
 def compile_query(assertions: Sequence[Node],
                   origin_of: Callable[[str], str]) -> CompiledQuery:
     """Compile one checker query (a list of IR assertions)."""
@@ -1768,7 +2047,9 @@ def _compile_query(assertions: Sequence[Node],
             groups.append(Group("unknown", str(exc), True))
             continue
         had = flags["unsupported"]
-        if ps.unsat:
+        if not ps.unsat and OR_SPLIT:
+            ps = _split_disjunction(ps)
+        if not isinstance(ps, list) and ps.unsat:
             if not had:
                 # one unsatisfiable component refutes the query whatever the
                 # others are (solver/builtin.py:737-740): nothing of it goes
@@ -1778,54 +2059,19 @@ def _compile_query(assertions: Sequence[Node],
                                      defs={}, free_default={})
             groups.append(Group("unknown", "float/unsupported atoms only", had))
             continue
+        if isinstance(ps, list):
+            # live disjunct branches: each its own problems and definitions;
+            # the component's models are their union (Group.alts)
+            grp = Group("pending", None, had)
+            for f in ps:
+                idx = _emit_component(f, problems)
+                grp.alts.append((idx, dict(f.defs), sorted(csyms)))
+            groups.append(grp)
+            continue
         for n, e in ps.defs.items():
             defs[n] = e
-        # post-presolve components over free symbols
-        free = [n for n in ps.bounds]
-        atom_vars = [set(ir.symbols_of(a)) for a in ps.atoms]
-        parent = {n: n for n in free}
-
-        def find(x: str) -> str:
-            while parent[x] != x:
-                parent[x] = parent[parent[x]]
-                x = parent[x]
-            return x
-
-        for vs in atom_vars:
-            vs = list(vs)
-            for o in vs[1:]:
-                ra, rb = find(vs[0]), find(o)
-                if ra != rb:
-                    parent[ra] = rb
-        buckets: Dict[str, List[int]] = {}
-        for i, vs in enumerate(atom_vars):
-            if vs:
-                buckets.setdefault(find(next(iter(vs))), []).append(i)
         grp = Group("pending", None, had)
-        used: Set[str] = set()
-        for root, idxs in buckets.items():
-            names = sorted({n for i in idxs for n in atom_vars[i]}, key=lambda n: ps.pos[n])
-            used |= set(names)
-            lo = [ps.bounds[n][0] for n in names]
-            hi = [ps.bounds[n][1] for n in names]
-            if any(v is None for v in lo + hi):
-                raise CapacityError("unbounded free symbol after presolve")
-            mx = [ps.maximize.get(n, False) for n in names]
-            prob = _emit_problem(names, lo, hi, mx, [ps.atoms[i] for i in idxs])
-            grp.problems.append(len(problems))
-            problems.append(prob)
-        # free symbols constrained by bounds only: their optimum is a bound,
-        # still decided on the device as an atom-free problem
-        rest = sorted((n for n in free if n not in used), key=lambda n: ps.pos[n])
-        if rest:
-            lo = [ps.bounds[n][0] for n in rest]
-            hi = [ps.bounds[n][1] for n in rest]
-            if any(v is None for v in lo + hi):
-                raise CapacityError("unbounded free symbol after presolve")
-            mx = [ps.maximize.get(n, False) for n in rest]
-            prob = _emit_problem(rest, lo, hi, mx, [])
-            grp.problems.append(len(problems))
-            problems.append(prob)
+        grp.problems.extend(_emit_component(ps, problems))
         groups.append(grp)
 
     if any(g.status == "unknown" for g in groups):

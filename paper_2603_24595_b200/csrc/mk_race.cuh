@@ -510,10 +510,11 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
     unsigned long long reset[2] = {0ull, ~0ull};
     CK(cudaMemcpyAsync(ctr + 1, reset, sizeof(reset), cudaMemcpyHostToDevice, s));
     mksort::SortInfo si{};
-    // MK_RACE_FORCE_SORT also forces every digit pass (measurement of the
-    // sort itself on keys that arrive ordered)
+    // MK_RACE_FORCE_SORT runs the sort path on keys the scan saw in order;
+    // the sort's own order check then skips every digit pass unless
+    // MK_SORT_ALL_PASSES forces them (measurement of the passes themselves)
     CK((mksort::sort_pairs<K, uint32_t>(kc, vc, ko, vo, n, bits, wb + o_ws, ctx->sms, s, &ks, &vs,
-                                       &si, force)));
+                                       &si, getenv("MK_SORT_ALL_PASSES") != nullptr)));
     out->sort_passes = si.passes_run;
     CK(cudaEventRecord(ctx->ev[2], s));
     k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, ks, vs, ctr + 5, ctr + 1, ctr + 2, nullptr);

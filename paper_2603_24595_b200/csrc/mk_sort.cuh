@@ -67,6 +67,24 @@ __device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long
 
 // -- pass 0: histograms of every digit pass + order check ---------------------------------
 
+// Per key and pass: the run heads among the warp's lanes (consecutive lanes
+// hold consecutive keys) add their run length, so ordered keys cost one
+// shared atomic per warp and digit instead of 32 conflicting ones.
+template <typename K>
+__device__ __forceinline__ void hist_add(unsigned* sh, K k, int p, unsigned active) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned d = (unsigned)((k >> (p * kRadixBits)) & (kRadix - 1));
+  const unsigned up = __shfl_up_sync(active, d, 1);
+  const bool head = lane == 0 || !((active >> (lane - 1)) & 1u) || up != d;
+  const unsigned heads = __ballot_sync(active, head);
+  if (head) {
+    // run = this head up to the next head (or the last active lane)
+    const unsigned after = heads & ~((2u << lane) - 1u);
+    const unsigned end = after ? (unsigned)(__ffs(after) - 1) : 32u - __clz(active);
+    atomicAdd(&sh[p * kRadix + d], end - lane);
+  }
+}
+
 template <typename K>
 __global__ void __launch_bounds__(kThreads)
     k_sort_hist(const K* __restrict__ keys, unsigned long long n, int passes,
@@ -75,22 +93,23 @@ __global__ void __launch_bounds__(kThreads)
   for (int i = threadIdx.x; i < passes * kRadix; i += kThreads) sh[i] = 0;
   __syncthreads();
   bool down = false;
-  const unsigned long long stride = (unsigned long long)gridDim.x * kThreads;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * kThreads + threadIdx.x; i < n;
-       i += stride) {
+  const unsigned lane = threadIdx.x & 31;
+  // warp-contiguous chunks of 32 keys, grid-stride over the chunks
+  const unsigned long long chunks = (n + 31) / 32;
+  const unsigned long long wstride = (unsigned long long)gridDim.x * kWarps;
+  for (unsigned long long c = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
+       c < chunks; c += wstride) {
+    const unsigned long long i = c * 32 + lane;
+    const bool ok = i < n;
+    const unsigned active = __ballot_sync(0xffffffffu, ok);
+    if (!ok) continue;
     const K k = keys[i];
-    if (i > 0 && k < keys[i - 1]) down = true;
-    // warp-aggregated counting: ordered keys share their high digits
-    // across a warp, so one leader adds the whole peer group
-    const unsigned active = __activemask();
+    const K prev = __shfl_up_sync(active, k, 1);
+    if (lane > 0 && k < prev) down = true;
+    if (lane == 0 && i > 0 && k < keys[i - 1]) down = true;
 #pragma unroll
-    for (int p = 0; p < KeyTraits<K>::kPasses; ++p) {
-      if (p < passes) {
-        const unsigned d = (unsigned)((k >> (p * kRadixBits)) & (kRadix - 1));
-        const unsigned peers = __match_any_sync(active, d);
-        if ((peers & lane_lt_mask()) == 0) atomicAdd(&sh[p * kRadix + d], (unsigned)__popc(peers));
-      }
-    }
+    for (int p = 0; p < KeyTraits<K>::kPasses; ++p)
+      if (p < passes) hist_add<K>(sh, k, p, active);
   }
   if (down) atomicOr(unsorted, 1u);
   __syncthreads();
@@ -136,7 +155,7 @@ struct PassSmem {
 };
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
     k_sort_pass(const K* __restrict__ kin, const V* __restrict__ vin, K* __restrict__ kout,
                 V* __restrict__ vout, unsigned long long n, int shift,
                 const unsigned long long* __restrict__ gbase, unsigned long long* lookback,
@@ -260,29 +279,27 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const unsigned tile = tile_s;
-  // blocked per thread: thread t owns tuples base + t*kItems .. +kItems (in order)
-  const unsigned long long base = (unsigned long long)tile * kTile + (unsigned long long)threadIdx.x * kItems;
+  // warp-striped: item j of lane l of warp w is tuple base + w*32*kItems + j*32 + l,
+  // so (j, lane) order is input order and every load / store is coalesced
+  const unsigned long long wbase =
+      (unsigned long long)tile * kTile + (unsigned long long)warp * 32 * kItems;
   K k[kItems];
   V v[kItems];
-  unsigned keep = 0;
+  unsigned keep[kItems];
+  unsigned mine = 0;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    const unsigned long long i = base + j;
+    const unsigned long long i = wbase + j * 32 + lane;
+    bool ok = false;
     if (i < n) {
       k[j] = kin[i];
       v[j] = vin[i];
-      if (k[j] != sentinel) keep |= 1u << j;
+      ok = k[j] != sentinel;
     }
+    keep[j] = __ballot_sync(0xffffffffu, ok);
+    mine += __popc(keep[j]);
   }
-  const unsigned mine = __popc(keep);
-  // exclusive scan over the block (warp shuffles, then warp sums)
-  unsigned incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned a = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += a;
-  }
-  if (lane == 31) wsum[warp] = incl;
+  if (lane == 0) wsum[warp] = mine;
   __syncthreads();
   unsigned wpre = 0, total = 0;
 #pragma unroll
@@ -290,7 +307,6 @@ __global__ void __launch_bounds__(kThreads)
     if (w < warp) wpre += wsum[w];
     total += wsum[w];
   }
-  const unsigned excl = wpre + incl - mine;
   if (threadIdx.x == 0) {
     unsigned long long* me = lookback + tile;
     const unsigned long long tag = epoch << 34;
@@ -314,14 +330,16 @@ __global__ void __launch_bounds__(kThreads)
     if (tile == ntiles - 1) *count_out = prefix + total;
   }
   __syncthreads();
-  unsigned long long dst = prefix_s + excl;
+  unsigned long long dst = prefix_s + wpre;
+  const unsigned lt = lane_lt_mask();
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    if (keep & (1u << j)) {
-      kout[dst] = k[j];
-      vout[dst] = v[j];
-      ++dst;
+    if ((keep[j] >> lane) & 1u) {
+      const unsigned long long o = dst + __popc(keep[j] & lt);
+      kout[o] = k[j];
+      vout[o] = v[j];
     }
+    dst += __popc(keep[j]);
   }
 }
 
@@ -389,7 +407,7 @@ inline cudaError_t sort_pairs(K* k0, V* v0, K* k1, V* v1, unsigned long long n, 
   Workspace w = carve(ws);
   cudaError_t e;
   if ((e = cudaMemsetAsync(w.hist, 0, 8 * 8 * kRadix + 64 + 64 + 64 * 4, s))) return e;
-  k_sort_hist<K><<<sms * 4, kThreads, 0, s>>>(k0, n, passes, w.hist, w.unsorted);
+  k_sort_hist<K><<<sms * 8, kThreads, 0, s>>>(k0, n, passes, w.hist, w.unsorted);
   k_sort_hist_scan<<<passes, kRadix, 0, s>>>(w.hist, passes, n, w.skip);
   int skip[8] = {0};
   unsigned unsorted = 0;
