@@ -557,6 +557,49 @@ def _analyze_line(chk, name):
                     "stage and branch screening vs the unmodified reference, one core"}
 
 
+def _search_line(chk, name, int_peak):
+    """The search kernels at scale: one workload whose step is a real
+    branch-and-prune (paged_attention_v1 at 32k context: millions of
+    boxes), resident and timed like the headline step; integer-issue
+    roofline on the algorithmic basis (bytecode instructions evaluated,
+    live counters) and on the SASS basis (ncu calibration)."""
+    from goldens import load, queries
+    from paper_2603_24595_b200.engine import compile_all
+
+    compiled = compile_all(queries(load(name)))
+    packed, _ = chk.pack([c for c, _ in compiled])
+    if not packed.problems:
+        return None
+    resident = chk.engine.upload(packed)
+    lim = dict(chk.limits)
+    lim["max_seconds"] = 600.0
+    resident.run(lim)
+    runs = [resident.run(lim) for _ in range(3)]
+    resident.free()
+    n = len(runs)
+    ms = sum(r["bb_ms"] + r["leaf_ms"] for r in runs) / n
+    step_ms = sum(r["device_ms"] for r in runs) / n
+    boxes = sum(r["boxes"] for r in runs) / n
+    points = sum(r["points"] for r in runs) / n
+    ops = sum(r["insns_bb"] + r["insns_leaf"] for r in runs) / n
+    alg = ops / (ms / 1e3) if ms > 0 else 0.0
+    cal = _calibration(name)
+    per_unit = cal.get("thread_inst_per_unit")
+    sass = (boxes + points) * per_unit / (ms / 1e3) if per_unit and ms > 0 else None
+    return {"workload": name, "description": CONFIG_NAMES.get(name),
+            "device_ms_per_step": step_ms, "boxes_per_step": boxes, "points_per_step": points,
+            "roofline": {"bound": "int32-issue", "achieved": alg / 1e9, "peak": int_peak / 1e9,
+                         "unit": "Gop/s", "frac": alg / int_peak if int_peak else None,
+                         "kernel": "k_search (+k_bb, k_leaf)", "kernel_ms_per_step": ms,
+                         "ops": "bytecode instructions evaluated (live device counters)",
+                         "sass_basis": {"achieved": sass / 1e9 if sass else None,
+                                        "frac": sass / int_peak if sass else None,
+                                        "per_unit": per_unit,
+                                        "source": f"profiles/ncu_{name}_summary.json",
+                                        "ncu_issue_active_pct":
+                                            cal.get("k_search_issue_active_pct")}}}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -694,6 +737,8 @@ def run_b200(args):
             side["k2_access_replay"] = _access_line(chk, args, peaks, src, int_peak)
         if args.analyze:
             side["time_to_verdict"] = _analyze_line(chk, args.analyze)
+        if args.search:
+            side["k1_search_at_scale"] = _search_line(chk, args.search, int_peak)
         if not args.no_cpu_baseline:
             side["cpu_baseline"] = _cpu_baseline(queries, inst, args.cpu_budget)
     if world > 1 and args.race_tokens > 0:
@@ -769,6 +814,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--analyze", default="rms_norm",
                     help="workload of the analyze() time-to-verdict line ('' to skip)")
+    ap.add_argument("--search", default="paged_attention_v1",
+                    help="workload of the k1_search_at_scale line ('' to skip)")
     ap.add_argument("--access-tokens", type=int, default=16384,
                     help="num_tokens of the oracle-rule access replay line (0: skip)")
     ap.add_argument("--race-tokens", type=int, default=262144,

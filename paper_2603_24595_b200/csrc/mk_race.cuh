@@ -146,23 +146,46 @@ __global__ void __launch_bounds__(RACE_THREADS) k_race_scan(RaceDev R, const K* 
   int64_t xa[SMALL_V], xb[SMALL_V];
   unsigned long long mine = 0, my_first = ~0ull;
   bool down = false;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const K a = keys[i - 1], b = keys[i];
-    if (b < a) down = true;
-    if (a != b) continue;
-    // identities are leading vars: decode the instance of the leading box
-    mk_decode(R.lo, R.hi, R.n_outer, R.prob->maxmask, (unsigned long long)vals[i - 1], xa);
-    mk_decode(R.lo, R.hi, R.n_outer, R.prob->maxmask, (unsigned long long)vals[i], xb);
-    bool same = true;
-    // shared: the key already holds the block, compare thread ids only
-    for (int a = R.shared ? 3 : 0; a < 6; ++a) {
-      const int v = R.id_var[a];
-      if (v >= 0 && xa[v] != xb[v]) same = false;
+  // warp-contiguous chunks of 8 x 32 tuples: eight independent key loads in
+  // flight per lane; each tuple's predecessor comes by shuffle
+  constexpr int J = 8;
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned long long nchunks = (n + 32 * J - 1) / (32 * J);
+  const unsigned long long wstride = (unsigned long long)gridDim.x * (blockDim.x / 32);
+  for (unsigned long long c = (unsigned long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+       c < nchunks; c += wstride) {
+    const unsigned long long base = c * 32 * J;
+    K kk[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const unsigned long long i = base + j * 32 + lane;
+      kk[j] = i < n ? keys[i] : (K)0;
     }
-    if (!same) {
-      ++mine;
-      if (i < my_first) my_first = i;
+    K carry = (lane == 0 && base > 0) ? keys[base - 1] : (K)0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const unsigned long long i = base + j * 32 + lane;
+      K prev = __shfl_up_sync(FULL, kk[j], 1);
+      const K last = __shfl_sync(FULL, kk[j], 31);
+      if (lane == 0) prev = carry;
+      carry = last;
+      if (i == 0 || i >= n) continue;
+      const K a = prev, b = kk[j];
+      if (b < a) down = true;
+      if (a != b) continue;
+      // identities are leading vars: decode the instance of the leading box
+      mk_decode(R.lo, R.hi, R.n_outer, R.prob->maxmask, (unsigned long long)vals[i - 1], xa);
+      mk_decode(R.lo, R.hi, R.n_outer, R.prob->maxmask, (unsigned long long)vals[i], xb);
+      bool same = true;
+      // shared: the key already holds the block, compare thread ids only
+      for (int a = R.shared ? 3 : 0; a < 6; ++a) {
+        const int v = R.id_var[a];
+        if (v >= 0 && xa[v] != xb[v]) same = false;
+      }
+      if (!same) {
+        ++mine;
+        if (i < my_first) my_first = i;
+      }
     }
   }
   for (int o = 16; o > 0; o >>= 1) {

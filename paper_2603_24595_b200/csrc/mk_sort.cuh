@@ -94,22 +94,38 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   bool down = false;
   const unsigned lane = threadIdx.x & 31;
-  // warp-contiguous chunks of 32 keys, grid-stride over the chunks
-  const unsigned long long chunks = (n + 31) / 32;
+  // warp-contiguous chunks of 8 x 32 keys, grid-stride over the chunks:
+  // eight independent loads in flight per lane
+  constexpr int J = 8;
+  const unsigned long long chunks = (n + 32 * J - 1) / (32 * J);
   const unsigned long long wstride = (unsigned long long)gridDim.x * kWarps;
   for (unsigned long long c = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
        c < chunks; c += wstride) {
-    const unsigned long long i = c * 32 + lane;
-    const bool ok = i < n;
-    const unsigned active = __ballot_sync(0xffffffffu, ok);
-    if (!ok) continue;
-    const K k = keys[i];
-    const K prev = __shfl_up_sync(active, k, 1);
-    if (lane > 0 && k < prev) down = true;
-    if (lane == 0 && i > 0 && k < keys[i - 1]) down = true;
+    const unsigned long long base = c * 32 * J;
+    K kk[J];
 #pragma unroll
-    for (int p = 0; p < KeyTraits<K>::kPasses; ++p)
-      if (p < passes) hist_add<K>(sh, k, p, active);
+    for (int j = 0; j < J; ++j) {
+      const unsigned long long i = base + j * 32 + lane;
+      kk[j] = i < n ? keys[i] : (K)0;
+    }
+    K carry = (lane == 0 && base > 0) ? keys[base - 1] : (K)0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const unsigned long long i0 = base + j * 32;
+      const bool ok = i0 + lane < n;
+      K prev = __shfl_up_sync(0xffffffffu, kk[j], 1);
+      const K last = __shfl_sync(0xffffffffu, kk[j], 31);
+      if (lane == 0) prev = carry;
+      carry = last;
+      if (ok && i0 + lane > 0 && kk[j] < prev) down = true;
+      if (i0 >= n) break;
+      const unsigned active = __ballot_sync(0xffffffffu, ok);
+      if (ok) {
+#pragma unroll
+        for (int p = 0; p < KeyTraits<K>::kPasses; ++p)
+          if (p < passes) hist_add<K>(sh, kk[j], p, active);
+      }
+    }
   }
   if (down) atomicOr(unsorted, 1u);
   __syncthreads();
