@@ -537,7 +537,8 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
     // the sort's own order check then skips every digit pass unless
     // MK_SORT_ALL_PASSES forces them (measurement of the passes themselves)
     CK((mksort::sort_pairs<K, uint32_t>(kc, vc, ko, vo, n, bits, wb + o_ws, ctx->sms, s, &ks, &vs,
-                                       &si, getenv("MK_SORT_ALL_PASSES") != nullptr)));
+                                       &si, getenv("MK_SORT_ALL_PASSES") != nullptr,
+                                       /*known_unsorted=*/!force)));
     out->sort_passes = si.passes_run;
     CK(cudaEventRecord(ctx->ev[2], s));
     k_race_scan<K><<<grid, RACE_THREADS, 0, s>>>(R, ks, vs, ctr + 5, ctr + 1, ctr + 2, nullptr);

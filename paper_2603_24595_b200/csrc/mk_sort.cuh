@@ -4,12 +4,14 @@
 // compaction, replacing cub::DeviceRadixSort / cub::DeviceSelect on the race
 // sweep (mk_race.cuh) and the oracle-rule access replay (mk_access.cuh).
 //
+//   k_sort_order    one read of the keys: keys that arrive non-decreasing
+//                   (a coalesced store's tuples) skip the sort entirely --
+//                   the stable sort is then the identity.
 //   k_sort_hist     ONE read of the keys: the digit histograms of every pass
 //                   at once (shared-memory counters per CTA, 4 x 8-bit digits
-//                   for u32 keys, up to 8 for u64) and a non-decreasing-order
-//                   check.  A pass whose digit is the same for every key
-//                   moves nothing and is skipped; already-ordered keys skip
-//                   the sort entirely (the stable sort is then the identity).
+//                   for u32 keys, up to 8 for u64; run heads of equal digits
+//                   across a warp add their run length).  A pass whose digit
+//                   is the same for every key moves nothing and is skipped.
 //   k_sort_pass     one onesweep pass per remaining digit (decoupled
 //                   look-back): tiles of 4096 tuples claim an in-order tile
 //                   id, rank their keys per digit with warp match/ballot
@@ -63,6 +65,32 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 
 __device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long long v) {
   asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+
+// Decoupled look-back by one whole warp (tile counts, one entry per tile):
+// the lanes read 32 predecessors at once, wait until all of them are
+// published, and stop at the nearest inclusive prefix.  Returns the
+// exclusive prefix of `tile` (every lane).
+__device__ __forceinline__ unsigned long long warp_lookback(const unsigned long long* lookback,
+                                                            unsigned tile,
+                                                            unsigned long long epoch) {
+  const unsigned lane = threadIdx.x & 31;
+  unsigned long long prefix = 0;
+  long long p = (long long)tile - 1;
+  while (p >= 0) {
+    const long long idx = p - (long long)lane;
+    unsigned long long e = idx >= 0 ? ld_volatile(lookback + idx) : ((epoch << 34) | kFlagIncl);
+    while (((e >> 34) != epoch || (e & (3ull << 32)) == 0)) e = ld_volatile(lookback + idx);
+    const unsigned incl = __ballot_sync(0xffffffffu, (e & kFlagIncl) != 0);
+    const unsigned upto = incl ? (unsigned)(__ffs(incl) - 1) : 31u;   // nearest inclusive lane
+    unsigned long long c = (lane <= upto && idx >= 0) ? (e & kCountMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    prefix += c;
+    if (incl) break;
+    p -= 32;
+  }
+  return prefix;
 }
 
 // -- pass 0: histograms of every digit pass + order check ---------------------------------
@@ -131,6 +159,39 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += kThreads)
     if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
+}
+
+// non-decreasing order check alone (one read of the keys, eight loads in
+// flight per lane): keys that arrive ordered need no histogram and no pass
+template <typename K>
+__global__ void __launch_bounds__(kThreads)
+    k_sort_order(const K* __restrict__ keys, unsigned long long n, unsigned* __restrict__ unsorted) {
+  constexpr int J = 8;
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned long long chunks = (n + 32 * J - 1) / (32 * J);
+  const unsigned long long wstride = (unsigned long long)gridDim.x * kWarps;
+  bool down = false;
+  for (unsigned long long c = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
+       c < chunks; c += wstride) {
+    const unsigned long long base = c * 32 * J;
+    K kk[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const unsigned long long i = base + j * 32 + lane;
+      kk[j] = i < n ? keys[i] : (K)0;
+    }
+    K carry = (lane == 0 && base > 0) ? keys[base - 1] : (K)0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const unsigned long long i = base + j * 32 + lane;
+      K prev = __shfl_up_sync(0xffffffffu, kk[j], 1);
+      const K last = __shfl_sync(0xffffffffu, kk[j], 31);
+      if (lane == 0) prev = carry;
+      carry = last;
+      if (i < n && i > 0 && kk[j] < prev) down = true;
+    }
+  }
+  if (__any_sync(0xffffffffu, down) && lane == 0) atomicOr(unsorted, 1u);
 }
 
 // exclusive prefix of each pass's histogram (in place); skip[p] = 1 when one
@@ -323,27 +384,22 @@ __global__ void __launch_bounds__(kThreads)
     if (w < warp) wpre += wsum[w];
     total += wsum[w];
   }
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     unsigned long long* me = lookback + tile;
     const unsigned long long tag = epoch << 34;
     unsigned long long prefix = 0;
     if (tile == 0) {
-      st_volatile(me, tag | kFlagIncl | total);
+      if (lane == 0) st_volatile(me, tag | kFlagIncl | total);
     } else {
-      st_volatile(me, tag | kFlagAgg | total);
-      long long p = (long long)tile - 1;
-      while (p >= 0) {
-        const unsigned long long e = ld_volatile(lookback + p);
-        if ((e >> 34) != epoch || (e & (3ull << 32)) == 0) continue;
-        prefix += e & kCountMask;
-        if (e & kFlagIncl) break;
-        --p;
-      }
-      st_volatile(me, tag | kFlagIncl | (prefix + total));
+      if (lane == 0) st_volatile(me, tag | kFlagAgg | total);
+      prefix = warp_lookback(lookback, tile, epoch);
+      if (lane == 0) st_volatile(me, tag | kFlagIncl | (prefix + total));
     }
-    prefix_s = prefix;
-    const unsigned long long ntiles = (n + kTile - 1) / kTile;
-    if (tile == ntiles - 1) *count_out = prefix + total;
+    if (lane == 0) {
+      prefix_s = prefix;
+      const unsigned long long ntiles = (n + kTile - 1) / kTile;
+      if (tile == ntiles - 1) *count_out = prefix + total;
+    }
   }
   __syncthreads();
   unsigned long long dst = prefix_s + wpre;
@@ -410,7 +466,8 @@ struct SortInfo {
 template <typename K, typename V>
 inline cudaError_t sort_pairs(K* k0, V* v0, K* k1, V* v1, unsigned long long n, int bits,
                               void* ws, int sms, cudaStream_t s, K** kres, V** vres,
-                              SortInfo* info, bool force_all = false) {
+                              SortInfo* info, bool force_all = false,
+                              bool known_unsorted = false) {
   static_assert(kThreads == kRadix, "one thread per digit in the pass kernel");
   *kres = k0;
   *vres = v0;
@@ -423,18 +480,23 @@ inline cudaError_t sort_pairs(K* k0, V* v0, K* k1, V* v1, unsigned long long n, 
   Workspace w = carve(ws);
   cudaError_t e;
   if ((e = cudaMemsetAsync(w.hist, 0, 8 * 8 * kRadix + 64 + 64 + 64 * 4, s))) return e;
+  if (!force_all && !known_unsorted) {
+    // ordered keys: the stable sort is the identity -- one read, no pass
+    unsigned unsorted = 0;
+    k_sort_order<K><<<sms * 8, kThreads, 0, s>>>(k0, n, w.unsorted);
+    if ((e = cudaMemcpyAsync(&unsorted, w.unsorted, sizeof(unsorted), cudaMemcpyDeviceToHost, s)))
+      return e;
+    if ((e = cudaStreamSynchronize(s))) return e;
+    if (!unsorted) {
+      if (info) info->already_sorted = 1;
+      return cudaSuccess;
+    }
+  }
   k_sort_hist<K><<<sms * 8, kThreads, 0, s>>>(k0, n, passes, w.hist, w.unsorted);
   k_sort_hist_scan<<<passes, kRadix, 0, s>>>(w.hist, passes, n, w.skip);
   int skip[8] = {0};
-  unsigned unsorted = 0;
   if ((e = cudaMemcpyAsync(skip, w.skip, sizeof(int) * passes, cudaMemcpyDeviceToHost, s))) return e;
-  if ((e = cudaMemcpyAsync(&unsorted, w.unsorted, sizeof(unsorted), cudaMemcpyDeviceToHost, s)))
-    return e;
   if ((e = cudaStreamSynchronize(s))) return e;
-  if (!unsorted && !force_all) {
-    if (info) info->already_sorted = 1;
-    return cudaSuccess;
-  }
   const size_t smem = pass_smem<K, V>();
   if ((e = cudaFuncSetAttribute(k_sort_pass<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem)))
