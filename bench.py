@@ -559,8 +559,8 @@ def _analyze_line(chk, name):
 
 def _search_line(chk, name, int_peak):
     """The search kernels at scale: one workload whose step is a real
-    branch-and-prune (paged_attention_v1 at 32k context: millions of
-    boxes), resident and timed like the headline step; integer-issue
+    branch-and-prune (moe_align, the Fig. 7 port: 852 problems, millions of
+    boxes and instances), resident and timed like the headline step; integer-issue
     roofline on the algorithmic basis (bytecode instructions evaluated,
     live counters) and on the SASS basis (ncu calibration)."""
     from goldens import load, queries
@@ -814,7 +814,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--analyze", default="rms_norm",
                     help="workload of the analyze() time-to-verdict line ('' to skip)")
-    ap.add_argument("--search", default="paged_attention_v1",
+    ap.add_argument("--search", default="moe_align",
                     help="workload of the k1_search_at_scale line ('' to skip)")
     ap.add_argument("--access-tokens", type=int, default=16384,
                     help="num_tokens of the oracle-rule access replay line (0: skip)")

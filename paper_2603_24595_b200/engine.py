@@ -120,7 +120,9 @@ class CompilePool:
             raise got
         return got
 
-    def compile(self, queries) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
+    def compile(self, queries, on_chunk=None) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
+        """Compile a batch; ``on_chunk(indices, results)`` (optional) is
+        called as each chunk of the batch completes, from a driver thread."""
         import threading
 
         items = [_portable(q) for q in queries]
@@ -142,8 +144,11 @@ class CompilePool:
                     idxs = chunks.pop(0)
                 try:
                     self._send(proc, [items[i] for i in idxs])
-                    for i, r in zip(idxs, self._recv(proc)):
+                    got = self._recv(proc)
+                    for i, r in zip(idxs, got):
                         out[i] = r
+                    if on_chunk is not None:
+                        on_chunk(idxs, got)
                 except BaseException as exc:  # surfaced to the caller below
                     with lock:
                         errors.append(exc)
@@ -247,10 +252,60 @@ class SiteChecker:
 
     def check_queries(self, queries: Sequence[Tuple[Sequence[ir.Node], Callable[[str], str]]]
                       ) -> List[QueryResult]:
+        if self.compile_workers > 1 and len(queries) >= self.POOL_MIN_BATCH:
+            return self._check_pipelined(queries)
         t0 = time.perf_counter()
         compiled = self.compile(queries)
         self.stats.compile_s += time.perf_counter() - t0
         return self.decide(compiled)
+
+    def _check_pipelined(self, queries) -> List[QueryResult]:
+        """Compile on the worker pool and decide on the device at the same
+        time: compiled chunks (longest queries first) go to a device thread
+        that decides whatever has arrived in one batch while the rest still
+        compiles (the engine call releases the GIL).  Results are the same
+        as compile-then-decide: queries are independent."""
+        import queue
+        import threading
+
+        if self._pool is None:
+            self._pool = CompilePool(self.compile_workers)
+        arrivals: "queue.Queue" = queue.Queue()
+        out: List[Optional[QueryResult]] = [None] * len(queries)
+        failure: List[BaseException] = []
+
+        def device_loop() -> None:
+            while True:
+                batch = [arrivals.get()]
+                while True:
+                    try:
+                        batch.append(arrivals.get_nowait())
+                    except queue.Empty:
+                        break
+                stop = any(b is None for b in batch)
+                flat = [pair for chunk in batch if chunk is not None for pair in chunk]
+                if flat and not failure:
+                    try:
+                        res = self.decide([r for _, r in flat])
+                        for (i, _), rr in zip(flat, res):
+                            out[i] = rr
+                    except BaseException as exc:  # surfaced to the caller below
+                        failure.append(exc)
+                if stop:
+                    return
+
+        th = threading.Thread(target=device_loop)
+        th.start()
+        t0 = time.perf_counter()
+        try:
+            self._pool.compile(queries, on_chunk=lambda idxs, rs: arrivals.put(list(zip(idxs, rs))))
+        finally:
+            self.stats.compile_s += time.perf_counter() - t0
+            arrivals.put(None)
+            th.join()
+        if failure:
+            raise failure[0]
+        return out  # type: ignore[return-value]
 
     def check(self, assertions: Sequence[ir.Node], origin_of: Callable[[str], str]) -> QueryResult:
         return self.check_queries([(assertions, origin_of)])[0]
