@@ -38,8 +38,16 @@ namespace mksort {
 
 constexpr int kThreads = 256;           // 8 warps
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;              // tuples per thread
-constexpr int kTile = kThreads * kItems;
+constexpr int kTileMin = kThreads * 16;  // smallest tile: sizes the look-back state
+
+// tuples per thread: 16 for every pair width (measured on the B200: 8 per
+// thread for 16-byte pairs -- half the staged tile, no spills -- sorted 6 %
+// slower, the look-back costs more per byte than the smaller tile saves)
+template <typename K, typename V>
+struct Tiling {
+  static constexpr int items = 16;
+  static constexpr int tile = kThreads * items;
+};
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
 constexpr unsigned long long kFlagAgg = 1ull << 32;
@@ -223,8 +231,8 @@ __global__ void k_sort_hist_scan(unsigned long long* hist, int passes, unsigned 
 
 template <typename K, typename V>
 struct PassSmem {
-  K keys[kTile];
-  V vals[kTile];
+  K keys[Tiling<K, V>::tile];
+  V vals[Tiling<K, V>::tile];
   unsigned wcnt[kWarps][kRadix];   // per-warp digit counts -> exclusive prefix over warps
   unsigned tstart[kRadix];         // digit start inside the tile (exclusive scan)
   unsigned long long gpos[kRadix]; // global start of the digit run of this tile
@@ -237,6 +245,8 @@ __global__ void __launch_bounds__(kThreads, 3)
                 V* __restrict__ vout, unsigned long long n, int shift,
                 const unsigned long long* __restrict__ gbase, unsigned long long* lookback,
                 unsigned* tile_ctr, unsigned long long epoch) {
+  constexpr int kItems = Tiling<K, V>::items;
+  constexpr int kTile = Tiling<K, V>::tile;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PassSmem<K, V>& S = *reinterpret_cast<PassSmem<K, V>*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -349,6 +359,8 @@ __global__ void __launch_bounds__(kThreads)
               V* __restrict__ vout, unsigned long long n, K sentinel,
               unsigned long long* lookback, unsigned* tile_ctr, unsigned long long epoch,
               unsigned long long* count_out) {
+  constexpr int kItems = Tiling<K, V>::items;
+  constexpr int kTile = Tiling<K, V>::tile;
   __shared__ unsigned wsum[kWarps];
   __shared__ unsigned tile_s;
   __shared__ unsigned long long prefix_s;
@@ -420,7 +432,7 @@ __global__ void __launch_bounds__(kThreads)
 // device workspace: histograms, skip flags, order flag, tile counters,
 // look-back state (one entry per tile and digit)
 inline size_t workspace_bytes(unsigned long long n) {
-  const unsigned long long tiles = (n + kTile - 1) / kTile + 1;
+  const unsigned long long tiles = (n + kTileMin - 1) / kTileMin + 1;
   return 8 * 8 * kRadix + 64 + 64 + 64 * 4 + tiles * kRadix * 8 + 256;
 }
 
@@ -501,7 +513,7 @@ inline cudaError_t sort_pairs(K* k0, V* v0, K* k1, V* v1, unsigned long long n, 
   if ((e = cudaFuncSetAttribute(k_sort_pass<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem)))
     return e;
-  const unsigned long long tiles = (n + kTile - 1) / kTile;
+  const unsigned long long tiles = (n + Tiling<K, V>::tile - 1) / Tiling<K, V>::tile;
   K* ki = k0;
   V* vi = v0;
   K* ko = k1;
@@ -532,7 +544,7 @@ inline cudaError_t compact(const K* kin, const V* vin, K* kout, V* vout, unsigne
   cudaError_t e;
   if ((e = cudaMemsetAsync(w.tile_ctr + 15, 0, sizeof(unsigned), s))) return e;
   if (n == 0) return cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s);
-  const unsigned long long tiles = (n + kTile - 1) / kTile;
+  const unsigned long long tiles = (n + Tiling<K, V>::tile - 1) / Tiling<K, V>::tile;
   k_compact<K, V><<<(unsigned)tiles, kThreads, 0, s>>>(kin, vin, kout, vout, n, sentinel,
                                                        w.lookback, w.tile_ctr + 15, next_epoch(),
                                                        d_count);

@@ -29,7 +29,7 @@ def _check(engine, keys, vals, bits, force=False):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n", [0, 1, 2, 31, TILE - 1, TILE, TILE + 1, 3 * TILE + 17, 1 << 20])
+@pytest.mark.parametrize("n", [0, 1, 2, 31, 2047, 2048, 2049, TILE - 1, TILE, TILE + 1, 3 * TILE + 17, 1 << 20])
 @pytest.mark.parametrize("bits", [8, 26, 31, 64])
 def test_random_keys(engine, n, bits):
     rng = np.random.default_rng(n * 131 + bits)

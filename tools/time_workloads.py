@@ -15,7 +15,8 @@ from paper_2603_24595_b200.engine import SiteChecker, compile_all  # noqa: E402
 
 
 def main(names):
-    chk = SiteChecker(device=0, compile_workers=0)
+    # MK_LIB: an alternative build of libmk_b200.so (measurement of build variants)
+    chk = SiteChecker(device=0, compile_workers=0, lib_path=os.environ.get("MK_LIB"))
     for name in names or workloads():
         doc = load(name)
         qs = queries(doc)
