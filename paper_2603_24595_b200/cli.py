@@ -6,6 +6,7 @@ reference specifies its CLI in SPEC.md:633-687 but does not ship it).
     python -m paper_2603_24595_b200 infer --log RUNS.jsonl --kernel NAME --out C.json
     python -m paper_2603_24595_b200 races --kernel K.mk [--wrapper W] [--context C.json]
         --launch BS=1,SL=32[,name=value...] [--device N]
+    python -m paper_2603_24595_b200 replay --kernel K.mk [--wrapper W] [--context C.json]
     python -m paper_2603_24595_b200 corpus DIR [DIR ...] [--device N]
 
 ``analyze`` runs the reference front end (parser, typechecker, executor DFS:
@@ -24,6 +25,11 @@ them at one concrete launch with the specification's oracle rule
 write-write race exists.  ``--launch`` pins launch-level symbols (BS, SL,
 scalar arguments...); the rest of the launch is the canonical model of the
 context's constraints.
+
+``replay`` analyzes and then replays every sat overflow / out-of-bounds /
+deref witness (paper_2603_24595_b200.witness): expression
+level and over every thread of the witness's launch; exit 1 when one is not
+confirmed.
 
 ``corpus`` analyzes several workload directories (kernel.mk + ctx.json each,
 BASELINE.json configs[4]) on one device context, one JSON line per entry.
@@ -63,13 +69,15 @@ def _load(kernel: str, context: Optional[str]):
     return unit, ctx
 
 
-def _analyze(unit, wrapper, ctx, budget, device, screening, recorders=None):
+def _analyze(unit, wrapper, ctx, budget, device, screening, recorders=None, created=None,
+             record_queries=False):
     from minikernel.engine import Budget, analyze
 
     from .detectors import install, shared_checker, uninstall
 
     chk = shared_checker(device)
-    prev = install(device=device, checker=chk, screening=screening, recorders=recorders)
+    prev = install(device=device, checker=chk, screening=screening, recorders=recorders,
+                   created=created, record_queries=record_queries)
     try:
         b = Budget(wall_s=budget) if budget else None
         return analyze(unit, wrapper, ctx=ctx, budget=b)
@@ -134,6 +142,35 @@ def cmd_races(a) -> int:
     return 1 if res.has_race else 0
 
 
+def cmd_replay(a) -> int:
+    """SPEC.md:664 replay: analyze, then replay every sat overflow /
+    out-of-bounds / deref witness (paper_2603_24595_b200.witness): expression
+    level and every thread of the witness launch on the device.  Exit 1 when
+    a witness is not confirmed."""
+    from .detectors import shared_checker
+    from .witness import replay_witness
+
+    unit, ctx = _load(a.kernel, a.context)
+    made: List[object] = []
+    rep = _analyze(unit, a.wrapper, ctx, a.budget, a.device, True, created=made,
+                   record_queries=True)
+    chk = shared_checker(a.device)
+    bad = 0
+    for f in rep.findings:
+        if f.status != "sat" or f.kind == "DataRace" or not f.witness:
+            continue
+        det = next((d for d in made if (f.kind, f.line, f.column) in d.sat_queries), None)
+        if det is None:
+            continue
+        q = det.sat_queries[(f.kind, f.line, f.column)]
+        r = replay_witness(chk.engine, q, det.table.origin_of, f.witness)
+        bad += r.status == "not-confirmed"
+        print(json.dumps({"kind": f.kind, "line": f.line, "column": f.column, "status": r.status,
+                          "violating_threads": r.violating_threads, "threads": r.threads,
+                          "note": r.note}))
+    return 1 if bad else 0
+
+
 def cmd_corpus(a) -> int:
     import os
 
@@ -172,6 +209,12 @@ def main(argv: Optional[List[str]] = None) -> int:
     p.add_argument("--budget", type=float)
     p.add_argument("--launch", default="")
     p.add_argument("--device", type=int, default=0)
+    p = sub.add_parser("replay")
+    p.add_argument("--kernel", required=True)
+    p.add_argument("--wrapper")
+    p.add_argument("--context")
+    p.add_argument("--budget", type=float)
+    p.add_argument("--device", type=int, default=0)
     p = sub.add_parser("corpus")
     p.add_argument("dirs", nargs="+")
     p.add_argument("--budget", type=float)
@@ -179,7 +222,7 @@ def main(argv: Optional[List[str]] = None) -> int:
     a = ap.parse_args(argv)
     try:
         return {"analyze": cmd_analyze, "infer": cmd_infer, "races": cmd_races,
-                "corpus": cmd_corpus}[a.cmd](a)
+                "replay": cmd_replay, "corpus": cmd_corpus}[a.cmd](a)
     except SystemExit:
         raise
     except Exception as exc:  # operational error

@@ -71,6 +71,10 @@ class GpuDetectors:
     # (paper_2603_24595_b200.replay); off by default
     record_accesses: bool = False
     accesses: List[object] = field(default_factory=list)
+    # (kind, line, col) -> IR assertions of the first sat query of the site,
+    # for witness replay (paper_2603_24595_b200.witness); off by default
+    record_queries: bool = False
+    sat_queries: Dict[Tuple[str, int, int], List[object]] = field(default_factory=dict)
 
     def __post_init__(self) -> None:
         if self.options is None:
@@ -78,6 +82,8 @@ class GpuDetectors:
             self.options = DetectorOptions()
         if self.checker is None:
             self.checker = shared_checker(self.device)
+        self._query_ir: Dict[Tuple[str, ...], List[object]] = {}
+        self._last_query = None
         E, R, S, T = _ref()
         self._E, self._R, self._S, self._T = E, R, S, T
         lo, hi = E.I32.bounds()
@@ -93,10 +99,15 @@ class GpuDetectors:
         key = tuple(E.render(a) for a in assertions)
         got = self._cache.get(key)
         if got is not None:
+            if self.record_queries:
+                self._last_query = self._query_ir.get(key)
             return got
         q = [ir.from_ref(a) for a in assertions]
         res = self.checker.check(q, self.table.origin_of)
         self._cache[key] = res
+        if self.record_queries:
+            self._query_ir[key] = q
+            self._last_query = q
         return res
 
     def _status(self, state, key) -> str:
@@ -111,6 +122,8 @@ class GpuDetectors:
               offset=None, flag_node=None) -> None:
         Finding = self._R.Finding
         if res.status == "sat":
+            if self.record_queries and key not in self.sat_queries and self._last_query:
+                self.sat_queries[key] = self._last_query
             status = self._status(state, key)
             if flag_node is not None:
                 state.flagged_io.append(flag_node)
@@ -312,7 +325,8 @@ class GpuDetectors:
 
 
 def install(device: int = 0, checker: Optional[SiteChecker] = None, screening: bool = False,
-            recorders: Optional[list] = None, created: Optional[list] = None):
+            recorders: Optional[list] = None, created: Optional[list] = None,
+            record_queries: bool = False):
     """Swap the checking stage of the reference executor for the B200 engine
     (engine/executor.py:33 resolves ``Detectors`` at construction time); with
     ``screening`` the executor's branch screening (engine/executor.py:489-492)
@@ -328,7 +342,8 @@ def install(device: int = 0, checker: Optional[SiteChecker] = None, screening: b
     class _Bound(GpuDetectors):
         def __init__(self, solver, table, kernel, options=None):
             super().__init__(solver, table, kernel, options, device=device, checker=checker,
-                             record_accesses=recorders is not None)
+                             record_accesses=recorders is not None,
+                             record_queries=record_queries)
             if recorders is not None:
                 recorders.append(self)
             if created is not None:

@@ -92,3 +92,15 @@ def test_corpus_one_line_per_entry():
     rows = [json.loads(x) for x in out.splitlines() if x.strip()]
     assert [os.path.basename(r["entry"]) for r in rows] == ["racy", "rms_norm"]
     assert rows[1]["findings"] == expected_findings(load("rms_norm"))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not HAVE_REF, reason="reference front end not available")
+def test_replay_confirms_the_narrowing_and_deref_witnesses():
+    for name, kind in (("silu_and_mul", "IntegerOverflow"), ("copy_blocks", "InvalidDeref")):
+        rc, out, err = _cli("replay", "--kernel", os.path.join(W, name, "kernel.mk"),
+                            "--context", os.path.join(W, name, "ctx.json"))
+        assert rc == 0, err
+        rows = [json.loads(line) for line in out.splitlines() if line.startswith("{")]
+        assert rows and all(r["status"] in ("confirmed", "confirmed-expression") for r in rows)
+        assert any(r["kind"] == kind and r["status"] == "confirmed" for r in rows)
