@@ -166,7 +166,7 @@ def cmd_replay(a) -> int:
         r = replay_witness(chk.engine, q, det.table.origin_of, f.witness)
         bad += r.status == "not-confirmed"
         print(json.dumps({"kind": f.kind, "line": f.line, "column": f.column, "status": r.status,
-                          "violating_threads": r.violating_threads, "threads": r.threads,
+                          "violating_threads": r.violating_threads, "candidate_threads": r.candidates,
                           "note": r.note}))
     return 1 if bad else 0
 

@@ -36,8 +36,9 @@ class Replay:
     status: str                 # "confirmed" | "confirmed-expression" | "not-confirmed"
     expression: bool            # the witness satisfies every assertion
     full_launch: Optional[bool]  # None: launch not swept
-    violating_threads: int = 0  # thread instances of the launch that violate the site
-    threads: int = 0            # thread instances enumerated
+    violating_threads: int = 0  # threads of the launch that violate the site
+    candidates: int = 0         # threads enumerated: the launch's threads that bound
+                                # propagation at the witness launch could not exclude
     note: str = ""
 
 

@@ -40,7 +40,7 @@ def test_small_launch_witnesses_confirmed_emulated():
         r = W.replay_witness(eng, a, o, s["witness"])
         assert r.status in ("confirmed", "confirmed-expression"), (name, s["line"], r)
         if r.status == "confirmed":
-            assert 1 <= r.violating_threads <= r.threads
+            assert 1 <= r.violating_threads <= r.candidates
             seen += 1
     assert seen >= 6
     eng.close()
