@@ -22,8 +22,10 @@
 //                   and one write of every tuple, plus 8 B per (tile, digit)
 //                   of look-back state.
 //   k_compact       order-preserving removal of sentinel tuples (guarded
-//                   accesses that did not execute), one read + one write,
-//                   decoupled look-back over tile counts.
+//                   accesses that did not execute), one read + one write:
+//                   each 4096-tuple tile arrives in shared memory by TMA bulk
+//                   copies (cp.async.bulk + mbarrier), per-item ballots, one
+//                   warp-parallel decoupled look-back over tile counts.
 //
 // Look-back entries carry an epoch tag, so the state array is never cleared:
 // entry = epoch << 34 | flag << 32 | count (flag 1: tile aggregate, 2:
@@ -73,6 +75,38 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 
 __device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long long v) {
   asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+
+// -- TMA bulk copies (cp.async.bulk) with an mbarrier ----------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// one bulk copy global -> shared of `bytes` (a multiple of 16, both ends
+// 16-byte aligned) completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n MK_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MK_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // Decoupled look-back by one whole warp (tile counts, one entry per tile):
@@ -250,12 +284,35 @@ __global__ void __launch_bounds__(kThreads, 3)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PassSmem<K, V>& S = *reinterpret_cast<PassSmem<K, V>*>(smem_raw);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) S.tile = atomicAdd(tile_ctr, 1u);
+  __shared__ __align__(8) unsigned long long bar;
+  if (threadIdx.x == 0) {
+    S.tile = atomicAdd(tile_ctr, 1u);
+    mbar_init(&bar, 1);
+  }
   for (int i = threadIdx.x; i < kWarps * kRadix; i += kThreads) (&S.wcnt[0][0])[i] = 0;
   __syncthreads();
   const unsigned tile = S.tile;
   const unsigned long long base = (unsigned long long)tile * kTile;
-  // warp-striped load: item j of lane l of warp w is tuple base + w*32*kItems + j*32 + l
+  // the tile arrives in the staging buffers by TMA bulk copies (16-byte
+  // granules; a ragged tail by plain loads); the buffers are only rewritten
+  // after every thread has read its items
+  {
+    const unsigned valid =
+        n - base < (unsigned long long)kTile ? (unsigned)(n - base) : (unsigned)kTile;
+    const unsigned nb = valid & ~3u;
+    if (threadIdx.x == 0 && nb) {
+      mbar_expect_tx(&bar, nb * (unsigned)(sizeof(K) + sizeof(V)));
+      bulk_g2s(S.keys, kin + base, nb * (unsigned)sizeof(K), &bar);
+      bulk_g2s(S.vals, vin + base, nb * (unsigned)sizeof(V), &bar);
+    }
+    for (unsigned i = nb + threadIdx.x; i < valid; i += kThreads) {
+      S.keys[i] = kin[base + i];
+      S.vals[i] = vin[base + i];
+    }
+    if (nb) mbar_wait(&bar, 0);
+    __syncthreads();
+  }
+  // warp-striped: item j of lane l of warp w is tuple base + w*32*kItems + j*32 + l
   K k[kItems];
   V v[kItems];
   unsigned rank[kItems];
@@ -264,8 +321,8 @@ __global__ void __launch_bounds__(kThreads, 3)
   for (int j = 0; j < kItems; ++j) {
     const unsigned long long i = wbase + j * 32 + lane;
     if (i < n) {
-      k[j] = kin[i];
-      v[j] = vin[i];
+      k[j] = S.keys[i - base];
+      v[j] = S.vals[i - base];
     }
   }
   // stable rank inside the warp, items in (j, lane) order
@@ -361,28 +418,50 @@ __global__ void __launch_bounds__(kThreads)
               unsigned long long* count_out) {
   constexpr int kItems = Tiling<K, V>::items;
   constexpr int kTile = Tiling<K, V>::tile;
+  extern __shared__ __align__(128) unsigned char csm[];   // keys[kTile], vals[kTile]
+  K* skeys = reinterpret_cast<K*>(csm);
+  V* svals = reinterpret_cast<V*>(csm + sizeof(K) * kTile);
   __shared__ unsigned wsum[kWarps];
   __shared__ unsigned tile_s;
   __shared__ unsigned long long prefix_s;
+  __shared__ __align__(8) unsigned long long bar;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
+  if (threadIdx.x == 0) {
+    tile_s = atomicAdd(tile_ctr, 1u);
+    mbar_init(&bar, 1);
+  }
   __syncthreads();
   const unsigned tile = tile_s;
-  // warp-striped: item j of lane l of warp w is tuple base + w*32*kItems + j*32 + l,
-  // so (j, lane) order is input order and every load / store is coalesced
-  const unsigned long long wbase =
-      (unsigned long long)tile * kTile + (unsigned long long)warp * 32 * kItems;
+  const unsigned long long base = (unsigned long long)tile * kTile;
+  const unsigned valid = n - base < (unsigned long long)kTile ? (unsigned)(n - base) : (unsigned)kTile;
+  // the tile's keys and values land in shared memory by two TMA bulk copies
+  // (multiples of 4 tuples: 16-byte granules); a ragged tail by plain loads
+  const unsigned nb = valid & ~3u;
+  if (threadIdx.x == 0 && nb) {
+    mbar_expect_tx(&bar, nb * (unsigned)(sizeof(K) + sizeof(V)));
+    bulk_g2s(skeys, kin + base, nb * (unsigned)sizeof(K), &bar);
+    bulk_g2s(svals, vin + base, nb * (unsigned)sizeof(V), &bar);
+  }
+  for (unsigned i = nb + threadIdx.x; i < valid; i += kThreads) {
+    skeys[i] = kin[base + i];
+    svals[i] = vin[base + i];
+  }
+  if (nb) mbar_wait(&bar, 0);
+  __syncthreads();
+  // warp-striped: item j of lane l of warp w is tuple w*32*kItems + j*32 + l of the
+  // tile, so (j, lane) order is input order and every store is coalesced
+  const unsigned wloc = (unsigned)warp * 32 * kItems;
   K k[kItems];
   V v[kItems];
   unsigned keep[kItems];
   unsigned mine = 0;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
-    const unsigned long long i = wbase + j * 32 + lane;
+    const unsigned i = wloc + j * 32 + lane;
     bool ok = false;
-    if (i < n) {
-      k[j] = kin[i];
-      v[j] = vin[i];
+    if (i < valid) {
+      k[j] = skeys[i];
+      v[j] = svals[i];
       ok = k[j] != sentinel;
     }
     keep[j] = __ballot_sync(0xffffffffu, ok);
@@ -545,7 +624,11 @@ inline cudaError_t compact(const K* kin, const V* vin, K* kout, V* vout, unsigne
   if ((e = cudaMemsetAsync(w.tile_ctr + 15, 0, sizeof(unsigned), s))) return e;
   if (n == 0) return cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s);
   const unsigned long long tiles = (n + Tiling<K, V>::tile - 1) / Tiling<K, V>::tile;
-  k_compact<K, V><<<(unsigned)tiles, kThreads, 0, s>>>(kin, vin, kout, vout, n, sentinel,
+  const size_t smem = (sizeof(K) + sizeof(V)) * (size_t)Tiling<K, V>::tile;
+  if ((e = cudaFuncSetAttribute(k_compact<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem)))
+    return e;
+  k_compact<K, V><<<(unsigned)tiles, kThreads, smem, s>>>(kin, vin, kout, vout, n, sentinel,
                                                        w.lookback, w.tile_ctr + 15, next_epoch(),
                                                        d_count);
   return cudaGetLastError();
