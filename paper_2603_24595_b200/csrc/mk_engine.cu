@@ -297,6 +297,34 @@ __global__ void k_roots(DevSet D, int nprob, void* stack, int keep_incumbents) {
   D.inc[pid].key = ~0ull;
 }
 
+// Root bound propagation, one thread per problem, before any search: the
+// linear rows (and row groups) contract the root box in the stack to their
+// fixpoint (up to `sweeps` FBBT sweeps, exact int128); a root with no model
+// is marked empty (lo > hi in its first symbol) and every consumer drops
+// it.  This is the device half of the presolve's bound propagation (the host
+// half can be switched off: compiler.HOST_FBBT).
+__global__ void k_root_contract(DevSet D, int nprob, void* stack, int sweeps) {
+  const int pid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pid >= nprob) return;
+  const mk_problem p = D.probs[pid];
+  if (p.nrows == 0 || p.nvars == 0) return;
+  Box* b = box_at(stack, D.box_bytes, pid);
+  mk_i128* blo = box_lo(b);
+  mk_i128* bhi = blo + D.stride;
+  i128 lo[MK_MAXV], hi[MK_MAXV];
+  for (int i = 0; i < p.nvars; ++i) {
+    lo[i] = ldv<i128>(blo[i]);
+    hi[i] = ldv<i128>(bhi[i]);
+  }
+  const MkProb P = mk_prob_view(D.probs, pid, D.insns, D.consts, D.atom_regs, D.atom_masks,
+                                D.rows, D.terms);
+  if (!mk_contract<i128>(P, lo, hi, sweeps)) lo[0] = hi[0] + 1;
+  for (int i = 0; i < p.nvars; ++i) {
+    blo[i] = Store<i128>::put(lo[i]);
+    bhi[i] = Store<i128>::put(hi[i]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // per-box step
 
@@ -331,6 +359,8 @@ __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo,
   a.m2 = 1;
   V c[CAPV];
   st.boxes++;
+  for (int v = 0; v < nv; ++v)
+    if (lo[v] > hi[v]) return a;  // an empty root (k_root_contract)
   mk_corner(lo, hi, nv, p.maxmask, c);
   const double vol0 = mk_volume_f(lo, hi, nv);
   if (inc_dominates<V>(D, pid, p, c)) {
@@ -1161,6 +1191,19 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   k_roots<<<(nprob + 127) / 128, 128, 0, s>>>(D, nprob, stack, keep_incumbents ? 1 : 0);
   ++launches;
   CK(cudaGetLastError());
+  {
+    // off by default: measured on the B200 with the host presolve's bound
+    // tightening on, a contracted root changes the split order and slows some
+    // searches (fused_add_rms_norm 0.8 -> 4.2 ms); with the host tightening
+    // off it does not recover the host-presolved speed
+    int sweeps = 0;
+    if (const char* e = getenv("MK_ROOT_SWEEPS")) sweeps = atoi(e);
+    if (sweeps > 0) {
+      k_root_contract<<<(nprob + 63) / 64, 64, 0, s>>>(D, nprob, stack, sweeps);
+      ++launches;
+      CK(cudaGetLastError());
+    }
+  }
   long long top = nprob;
   int* h_counts = static_cast<int*>(ctx->h_pinned);
   double dive_ms = 0.0;
