@@ -1071,7 +1071,12 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   int64_t max_rounds = lim && lim->max_rounds > 0 ? lim->max_rounds : 200000;
   int64_t max_boxes = lim && lim->max_boxes > 0 ? lim->max_boxes : (int64_t)4e9;
   double max_seconds = lim && lim->max_seconds > 0 ? lim->max_seconds : 30.0;
-  int K = lim && lim->split_k > 1 ? lim->split_k : 16;
+  // split arity, measured on the B200 (profiles/r02_split_k_*.jsonl): the
+  // whole golden corpus sums to 117 ms of resident steps at 16, 86 at 8, 80
+  // at 12; the config3 headline set takes 135 ms at 16, 80 at 12, 39 at 8
+  int K = 8;
+  if (const char* e = getenv("MK_SPLIT_K")) K = atoi(e) > 1 ? atoi(e) : K;
+  if (lim && lim->split_k > 1) K = lim->split_k;
   int chunk = lim && lim->chunk > 0 ? lim->chunk : 65536;
   long long leaf_volume = lim && lim->leaf_volume > 0 ? lim->leaf_volume : 4096;
   // incumbent dive: steps of width 1 from every root before the search
