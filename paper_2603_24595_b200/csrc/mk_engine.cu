@@ -613,6 +613,7 @@ struct SearchArgs {
   int max_steps;     // steps per task (0: unbounded)
   int dive;          // incumbent dive: no spills, dumps or pending marks
   const int* stop;   // dive: the main search has finished (polled per step)
+  int adapt_k;       // widen the splits of a shallow stack (MK_ADAPT_K)
 };
 
 // TASK_DUMPED: redistribution (every task has been handed out), the unit
@@ -687,7 +688,11 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
     a.sv = -1;
     if (lane < n) {
       load_box<V, V>(box_at(stack, A.box_bytes, (size_t)(base + lane)), nv, D.stride, lo, hi);
-      a = process_box<V, CAPV, CAPR, SH>(D, pid, p, lo, hi, K, A.leaf_volume, st, wide);
+      // a shallow stack splits wider so the next step fills the warp:
+      // n boxes popped -> up to 32 / n pieces each (A.adapt_k)
+      int Ke = K;
+      if (A.adapt_k && wide && n * K < 32) Ke = (int)(32 / n) < MAX_CHILDREN ? (int)(32 / n) : MAX_CHILDREN;
+      a = process_box<V, CAPV, CAPR, SH>(D, pid, p, lo, hi, Ke, A.leaf_volume, st, wide);
     }
     const int nch = a.kind == ACT_SPLIT ? a.m * a.m2 : 0;
     int incl = nch;
@@ -1076,6 +1081,10 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   // at 12; the config3 headline set takes 135 ms at 16, 80 at 12, 39 at 8
   int K = 8;
   if (const char* e = getenv("MK_SPLIT_K")) K = atoi(e) > 1 ? atoi(e) : K;
+  // widen the splits of shallow stacks (measured: config3 40 -> 32 ms,
+  // racy 8.7 -> 4.6 ms, the rest within noise; profiles/r02_adapt_k.jsonl)
+  int adapt_k = 1;
+  if (const char* e = getenv("MK_ADAPT_K")) adapt_k = atoi(e);
   if (lim && lim->split_k > 1) K = lim->split_k;
   int chunk = lim && lim->chunk > 0 ? lim->chunk : 65536;
   long long leaf_volume = lim && lim->leaf_volume > 0 ? lim->leaf_volume : 4096;
@@ -1270,6 +1279,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
       k_stamp<<<1, 1, 0, cs>>>(reinterpret_cast<unsigned long long*>(cls[c].ctl + 4));
       ++launches;
       SearchArgs A;
+      A.adapt_k = adapt_k;
       A.tasks = cls[c].tasks;
       A.ntasks = (int)cls[c].ntasks;
       A.ctl = cls[c].ctl;
@@ -1358,6 +1368,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
         k_stamp<<<1, 1, 0, ds>>>(reinterpret_cast<unsigned long long*>(dctl + 4));
         ++launches;
         SearchArgs A;
+        A.adapt_k = 0;   // a dive pops one box per step by design
         A.tasks = dst[c];
         A.ntasks = (int)nt[c];
         A.ctl = dctl;
