@@ -14,17 +14,22 @@ Default workload: BASELINE.json configs[2] at its stated domain (SURVEY.md
 (workloads/paged_attention_*_long_*).  ``--workload corpus`` is configs[4]
 (every golden workload); any single workload name works too.
 
-Instances.  A site's instances are the points of its compiled domain (thread
-identities x loop indices x havoc loads x user-controlled launch
-assignments) that the B200 search certifies: the root-box volumes of the
-site's device problems.  A site the host site compiler refutes during
-presolve has no device problem and counts 0 instances (it is reported in
-``decided``).  Both arms use the same per-site counts, so every ratio of
-values is a ratio of times.
+Instances.  A site's instances are the points of its domain after
+structural lowering (thread identities x loop indices x havoc loads x
+user-controlled launch assignments): the root-box volumes of its light
+compile's device problems (its full compile's when the light one cannot
+bound it; bench.site_instances).  Both arms use the same per-site counts,
+so every ratio of values is a ratio of times.
 
-value   device-certified instances / device time of the step: the compiled
-        problem set resident in HBM (mk_set_eval), CUDA events on the engine
-        streams, L2 flushed between steps (256 MiB write).  Max over ranks.
+Two tiers (SiteChecker.check_queries): every site is first compiled light
+(structural presolve only) and searched on the device within a short
+budget; the sites the device does not decide there go through the full
+host presolve and the device.  ``decided`` reports where each verdict came
+from.
+
+value   instances / device time of the step: both tiers' problem sets
+        resident in HBM (mk_set_eval), CUDA events on the engine streams, L2
+        flushed between steps (256 MiB write).  Max over ranks.
 e2e     the same instances / wall time of the public API a user calls
         (SiteChecker.check_queries; N>1: shard.check_sites): host compile on
         the worker pool, pack, H2D, search, D2H, witness assembly, every step.
@@ -101,26 +106,25 @@ def load_sites(names):
     return docs, qs, recs
 
 
-def site_accounting(compiled):
-    """Per site: certified instances (device problems' root-box volumes) and
-    where its verdict is decided."""
-    inst, where = [], []
-    for cq, err in compiled:
-        if cq is None:
-            inst.append(0)
-            where.append("host_unknown")
-            continue
-        v = 0
-        for p in cq.problems:
-            v += p.volume()
-        inst.append(v)
-        if any(g.status == "unsat" for g in cq.groups):
-            where.append("host_unsat")
-        elif not cq.problems:
-            where.append("host_unknown")
-        else:
-            where.append("device")
-    return inst, where
+def site_instances(queries, light=None, full=None):
+    """Per site: its instances = the root-box volume of the device problems
+    of its *light* compile (the query's domain after structural lowering:
+    thread ids x loop indices x havoc loads x launch assignments, before any
+    bound reasoning), or of its full compile when the light one cannot bound
+    it.  Deterministic (no device involved), so both arms count the same
+    instances and every ratio of values is a ratio of times."""
+    from paper_2603_24595_b200.engine import compile_all
+
+    light = light if light is not None else compile_all(queries, light=True)
+    need = [i for i, (cq, _) in enumerate(light) if cq is None or not cq.problems]
+    if full is None:
+        got = compile_all([queries[i] for i in need])
+        full = dict(zip(need, got))
+    inst = []
+    for i, (cq, _) in enumerate(light):
+        src = cq if (cq is not None and cq.problems) else full.get(i, (None, None))[0]
+        inst.append(sum(p.volume() for p in src.problems) if src is not None else 0)
+    return inst
 
 
 def _free_port():
@@ -246,7 +250,7 @@ def run_reference(args):
 
     names = entries(args.workload)
     _, queries, _ = load_sites(names)
-    inst, _ = site_accounting(compile_all(queries))
+    inst = site_instances(queries)
     cores = os.cpu_count() or 1
     pool = mp.get_context("fork").Pool(cores)
     n = len(queries)
@@ -644,32 +648,66 @@ def run_b200(args):
     t0 = time.perf_counter()
     compiled = compile_all(queries)
     compile_serial_ms = 1e3 * (time.perf_counter() - t0)
-    inst, where = site_accounting(compiled)
+    light = compile_all(queries, light=True)
+    inst = site_instances(queries, light, dict(enumerate(compiled)))
     mine = (shard.deal([float(1 + len(a)) for a, _ in queries], world)[rank]
             if world > 1 else list(range(len(queries))))
-    my_compiled = [compiled[i] for i in mine]
-    my_inst = float(sum(inst[i] for i in mine))
     total_instances = float(sum(inst))
+
+    # the public API's two tiers (SiteChecker.check_queries), made resident:
+    # tier 1 = the light problems of every site that compiles light, within
+    # the first-tier budget; tier 2 = the full problems of the sites tier 1
+    # did not decide.  The parity gate below fixes the tier split.
+    lmine = [i for i in mine if light[i][0] is not None]
+    packed1, offs1 = chk.pack([light[i][0] for i in lmine])
+    t1_budget = chk.tier1_budget(len(lmine))
+    res1 = chk.decide([light[i] for i in lmine], packed1, offs1, budget_s=t1_budget)
+    tier1 = {i: r for i, r in zip(lmine, res1) if r.status in ("sat", "unsat")}
+    rest = [i for i in mine if i not in tier1]
+    packed2, offs2 = chk.pack([compiled[i][0] for i in rest])
+    res2 = chk.decide([compiled[i] for i in rest], packed2, offs2)
+    results = dict(tier1)
+    results.update(zip(rest, res2))
 
     # parity gate: the benchmarked results must be the reference's (sites
     # the reference only timed out on are pinned by z3, tests/goldens.py)
-    packed, offsets = chk.pack([c for c, _ in my_compiled])
-    results = chk.decide(my_compiled, packed, offsets)
-    bad = mismatches({"sites": [recs[i] for i in mine]}, results)
+    bad = mismatches({"sites": [recs[i] for i in mine]}, [results[i] for i in mine])
     if bad:
         raise SystemExit(f"parity failure on sites {bad[:10]}")
-    sat_dev = sum(1 for i, r in zip(mine, results) if r.status == "sat" and where[i] == "device")
 
-    resident = chk.engine.upload(packed) if packed.problems else None
+    def where(i):
+        if i in tier1:
+            return "tier1_device" if light[i][0].problems else "tier1_host_light"
+        cq = compiled[i][0]
+        if cq is None or (not cq.problems and not any(g.status == "unsat" for g in cq.groups)):
+            return "host_unknown"
+        return "host_unsat" if any(g.status == "unsat" for g in cq.groups) else "tier2_device"
+
+    places = {i: where(i) for i in mine}
+    sat_dev = sum(1 for i in mine if results[i].status == "sat"
+                  and places[i] in ("tier1_device", "tier2_device"))
+    resident1 = chk.engine.upload(packed1) if packed1.problems else None
+    resident2 = chk.engine.upload(packed2) if packed2.problems else None
+    lim1 = dict(chk.limits)
+    lim1["max_seconds"] = t1_budget
     limits = dict(chk.limits)
-    limits["max_seconds"] = min(chk.limits["max_seconds"] * max(len(mine), 1), 3600.0)
+    limits["max_seconds"] = min(chk.limits["max_seconds"] * max(len(rest), 1), 3600.0)
     peak = chk.engine.int_peak()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     empty = {"device_ms": 0.0, "bb_ms": 0.0, "leaf_ms": 0.0, "boxes": 0, "points": 0,
              "insns_bb": 0, "insns_leaf": 0, "launches": 0, "covered": 0.0}
+    def step():
+        out = dict(empty)
+        for rs, lim in ((resident1, lim1), (resident2, limits)):
+            if rs is None:
+                continue
+            st = rs.run(lim)
+            for k in empty:
+                out[k] += st[k]
+        return out
+
     for _ in range(args.warmup):
-        if resident:
-            resident.run(limits)
+        step()
     clocks = Clocks(local).start()
     if world > 1:
         dist.barrier()
@@ -678,7 +716,7 @@ def run_b200(args):
     for _ in range(args.steps):
         flush.random_(0, 255)
         torch.cuda.synchronize()
-        st = resident.run(limits) if resident else dict(empty)
+        st = step()
         dev_ms.append(st["device_ms"])
         launches += int(st["launches"])
         for k in empty:
@@ -707,8 +745,8 @@ def run_b200(args):
         e2e_call()
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(sum(e2e_t) / len(e2e_t))
-    h2d = sum_over_ranks(packed.host_bytes())
-    d2h = sum_over_ranks(resident.d2h_bytes() if resident else 0)
+    h2d = sum_over_ranks(packed1.host_bytes() + packed2.host_bytes())
+    d2h = sum_over_ranks(sum(r.d2h_bytes() for r in (resident1, resident2) if r))
 
     # roofline of k_search (+ its pre-split / leaf kernels): integer issue
     search_ms = (acc["bb_ms"] + acc["leaf_ms"]) / n
@@ -721,12 +759,20 @@ def run_b200(args):
     sass = units * per_unit / (search_ms / 1e3) if per_unit and search_ms > 0 else None
     sms = torch.cuda.get_device_properties(local).multi_processor_count
 
+    def count(kind):
+        return int(sum_over_ranks(sum(1 for w in places.values() if w == kind)))
+
     decided = {"sites": len(queries),
-               "device": sum(1 for w in where if w == "device"),
-               "host_presolve_unsat": sum(1 for w in where if w == "host_unsat"),
-               "host_reference_giveup_unknown": sum(1 for w in where if w == "host_unknown"),
+               "device": count("tier1_device") + count("tier2_device"),
+               "device_tier1_light": count("tier1_device"),
+               "device_tier2_full": count("tier2_device"),
+               "host_light_constant_folding": count("tier1_host_light"),
+               "host_presolve_unsat": count("host_unsat"),
+               "host_reference_giveup_unknown": count("host_unknown"),
                "device_sat_witnesses": int(sum_over_ranks(sat_dev)),
-               "device_problems": int(sum_over_ranks(len(packed.problems)))}
+               "device_problems": int(sum_over_ranks(len(packed1.problems) + len(packed2.problems))),
+               "tiers": "tier 1: light compile (structural presolve only) + device within "
+                        f"{t1_budget * 1e3:.0f} ms; tier 2: full presolve + device for the rest"}
 
     side = {}
     if rank == 0 and world == 1:
@@ -756,8 +802,9 @@ def run_b200(args):
             "config": {"workload": args.workload, "description": CONFIG_NAMES.get(args.workload),
                        "entries": names, "sites": len(queries),
                        "instances_per_step": total_instances,
-                       "instances": "device-certified root-box volumes of the sites' compiled "
-                                    "problems (presolve-refuted sites count 0)",
+                       "instances": "root-box volumes of the sites' device problems after "
+                                    "structural lowering (light compile; full when the light one "
+                                    "cannot bound the site)",
                        "l2": "flushed between steps (256 MiB write)",
                        "parallelism": "1 GPU" if world == 1 else
                        f"{world} ranks, sites dealt longest-first (no data-path collective; "
@@ -795,8 +842,9 @@ def run_b200(args):
         }
         out.update(side)
         print(json.dumps(out))
-    if resident:
-        resident.free()
+    for r in (resident1, resident2):
+        if r:
+            r.free()
     chk.close()
     if world > 1:
         dist.destroy_process_group()

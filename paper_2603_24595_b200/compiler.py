@@ -665,7 +665,13 @@ def _replace_node(e: Node, old: Node, new: Node) -> Node:
 
 class _Presolve:
     def __init__(self, atoms: List[Node], widths: Dict[str, str],
-                 pos: Dict[str, float], maximize: Dict[str, bool]) -> None:
+                 pos: Dict[str, float], maximize: Dict[str, bool], light: bool = False) -> None:
+        # light: structural steps only (normalisation, unary bounds, folding,
+        # elimination, lattices); every step that reasons with the symbols'
+        # ranges (bound tightening, dead disjuncts, quotients, radix split,
+        # aggregation, relaxation / opposite rows, Fourier-Motzkin) is left to
+        # the device search -- the first tier of SiteChecker.check_queries
+        self.light = light
         self.widths = widths
         self.pos = pos
         self.maximize = maximize
@@ -691,6 +697,7 @@ class _Presolve:
         """A presolve of the same component continuing from this state with
         ``atoms`` (the disjunct split, _compile_query)."""
         q = _Presolve.__new__(_Presolve)
+        q.light = self.light
         q.widths = dict(self.widths)
         q.pos = dict(self.pos)
         q.maximize = dict(self.maximize)
@@ -836,7 +843,7 @@ class _Presolve:
         # linear forms are pure in the node (widths only grow: new lattice
         # symbols), so one memo serves every pass of this presolve
         lin = self._lin_memo
-        ivl0 = _Ivl(self.bounds)
+        ivl0 = None if self.light else _Ivl(self.bounds)
         # 1. normalise, split conjunctions, drop truths
         new_atoms: List[Node] = []
         for a in self._split_and(self.atoms):
@@ -888,7 +895,7 @@ class _Presolve:
             return True
         # 3b. mixed-radix split with a symbolic radix (before elimination
         # rewrites the digit equality into bounds)
-        if self._try_radix(lin):
+        if not self.light and self._try_radix(lin):
             return True
         # 4. unit-coefficient equality elimination (order preserving)
         if self._try_eliminate(lin):
@@ -896,6 +903,8 @@ class _Presolve:
         # 5. lattice substitution for emod(.., c) == r
         if self._try_lattice(lin):
             return True
+        if self.light:
+            return False
         # 5b. quotient variables for divisions by positive constants
         if self._try_quotient(lin):
             return True
@@ -1992,14 +2001,15 @@ def _split_disjunction(ps: "_Presolve"):
 
 
 def compile_query(assertions: Sequence[Node],
-                  origin_of: Callable[[str], str]) -> CompiledQuery:
-    """Compile one checker query (a list of IR assertions)."""
+                  origin_of: Callable[[str], str], light: bool = False) -> CompiledQuery:
+    """Compile one checker query (a list of IR assertions); ``light``: the
+    structural presolve only (_Presolve.light)."""
     with ir.compile_scope():
-        return _compile_query(assertions, origin_of)
+        return _compile_query(assertions, origin_of, light)
 
 
 def _compile_query(assertions: Sequence[Node],
-                   origin_of: Callable[[str], str]) -> CompiledQuery:
+                   origin_of: Callable[[str], str], light: bool = False) -> CompiledQuery:
     widths: Dict[str, str] = {}
     for a in assertions:
         ir.symbols_of(a, widths)
@@ -2040,14 +2050,14 @@ def _compile_query(assertions: Sequence[Node],
             groups.append(Group("unknown", str(exc), True))
             continue
         int_widths = {n: w for n, w in csyms.items() if not ir.is_float(w)}
-        ps = _Presolve(atoms, dict(int_widths), dict(pos), dict(maximize))
+        ps = _Presolve(atoms, dict(int_widths), dict(pos), dict(maximize), light)
         try:
             ps.run()
         except CompileError as exc:
             groups.append(Group("unknown", str(exc), True))
             continue
         had = flags["unsupported"]
-        if not ps.unsat and OR_SPLIT:
+        if not ps.unsat and OR_SPLIT and not light:
             ps = _split_disjunction(ps)
         if not isinstance(ps, list) and ps.unsat:
             if not had:

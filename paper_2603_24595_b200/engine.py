@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 from typing import Callable, Dict, List, Optional, Sequence, Tuple
 
 from . import ir
-from .compiler import CompileError, CompiledQuery, compile_query
+from .compiler import CapacityError, CompileError, CompiledQuery, compile_query
 from .native import Engine, PackedSet
 from .order import OriginLookup
 
@@ -35,25 +35,38 @@ class BatchStats:
     queries: int = 0
     problems: int = 0
     compile_s: float = 0.0
+    tier1_decided: int = 0         # queries decided by the light first tier
+    tier2_queries: int = 0         # queries that went through the full presolve
     device_s: float = 0.0
     assemble_s: float = 0.0
     device: Dict[str, float] = field(default_factory=dict)
 
 
+LIGHT_FAILED = "light compile: left to the full presolve"
+
+
 def _compile_one(item) -> Tuple[Optional[CompiledQuery], Optional[str]]:
-    assertions, origin_of = item
+    """(assertions, origin lookup[, light]) -> (compiled query, error).  A
+    light compile that hits an engine limit (typically a symbol only the full
+    presolve bounds) is not an error: the query goes to the second tier."""
+    assertions, origin_of = item[0], item[1]
+    light = len(item) > 2 and bool(item[2])
     t0 = time.perf_counter()
     try:
-        cq = compile_query(assertions, origin_of)
+        cq = compile_query(assertions, origin_of, light)
         cq.compile_s = time.perf_counter() - t0
         return cq, None
     except CompileError as exc:
-        return None, str(exc)
+        return None, (LIGHT_FAILED if light else str(exc))
+    except CapacityError:
+        if light:
+            return None, LIGHT_FAILED
+        raise
 
 
-def compile_all(queries: Sequence[Tuple[Sequence[ir.Node], Callable[[str], str]]]
-                ) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
-    return [_compile_one(q) for q in queries]
+def compile_all(queries: Sequence[Tuple[Sequence[ir.Node], Callable[[str], str]]],
+                light: bool = False) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
+    return [_compile_one((q[0], q[1], light)) for q in queries]
 
 
 def _portable(query):
@@ -120,12 +133,13 @@ class CompilePool:
             raise got
         return got
 
-    def compile(self, queries, on_chunk=None) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
+    def compile(self, queries, on_chunk=None, light: bool = False
+                ) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
         """Compile a batch; ``on_chunk(indices, results)`` (optional) is
         called as each chunk of the batch completes, from a driver thread."""
         import threading
 
-        items = [_portable(q) for q in queries]
+        items = [_portable(q) + (light,) for q in queries]
         # longest first (cost ~ assertion count): the big queries start in the
         # first wave and the small ones fill the gaps, so the batch's critical
         # path is close to its largest query
@@ -197,6 +211,8 @@ class SiteChecker:
         # 0 / 1: compile inline; None: default_workers()
         self.compile_workers = default_workers() if compile_workers is None else compile_workers
         self._pool: Optional[CompilePool] = None
+        # light first tier on the device before the full presolve
+        self.two_tier = os.environ.get("MK_TWO_TIER", "1") != "0"
 
     def close(self) -> None:
         if self._pool is not None:
@@ -204,12 +220,13 @@ class SiteChecker:
             self._pool = None
         self.engine.close()
 
-    def compile(self, queries) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
+    def compile(self, queries, light: bool = False
+                ) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
         if self.compile_workers > 1 and len(queries) >= self.POOL_MIN_BATCH:
             if self._pool is None:
                 self._pool = CompilePool(self.compile_workers)
-            return self._pool.compile(queries)
-        return compile_all(queries)
+            return self._pool.compile(queries, light=light)
+        return compile_all(queries, light)
 
     def pack(self, compiled: Sequence[Optional[CompiledQuery]]) -> Tuple[PackedSet, List[int]]:
         problems, offsets = [], []
@@ -220,16 +237,18 @@ class SiteChecker:
         return PackedSet(problems), offsets
 
     def decide(self, compiled: Sequence[Tuple[Optional[CompiledQuery], Optional[str]]],
-               packed: Optional[PackedSet] = None, offsets: Optional[List[int]] = None
-               ) -> List[QueryResult]:
+               packed: Optional[PackedSet] = None, offsets: Optional[List[int]] = None,
+               budget_s: Optional[float] = None) -> List[QueryResult]:
         cqs = [c for c, _ in compiled]
         if packed is None:
             packed, offsets = self.pack(cqs)
         t0 = time.perf_counter()
         # the reference grants every query its own timeout (engine/state.py:38);
-        # a batch gets the sum, capped
+        # a batch gets the sum, capped; ``budget_s``: an absolute budget for
+        # the batch (the first tier)
         lim = dict(self.limits)
-        lim["max_seconds"] = min(self.limits["max_seconds"] * max(len(compiled), 1), 3600.0)
+        lim["max_seconds"] = (budget_s if budget_s is not None else
+                              min(self.limits["max_seconds"] * max(len(compiled), 1), 3600.0))
         results = self.engine.solve_packed(packed, lim) if packed.problems else []
         t1 = time.perf_counter()
         out: List[QueryResult] = []
@@ -250,8 +269,46 @@ class SiteChecker:
                 self.stats.device[k] = self.stats.device.get(k, 0) + v
         return out
 
+    # first tier: device budget for the whole light batch (seconds): per query,
+    # clamped (measured on the B200: the light tier decides 65 % of the golden
+    # corpus's sites within 20 ms per batch)
+    TIER1_S = (0.002, 0.005, 0.02)   # per query, minimum, maximum
+
+    def tier1_budget(self, n: int) -> float:
+        per, lo, hi = self.TIER1_S
+        return min(max(per * n, lo), hi)
+
     def check_queries(self, queries: Sequence[Tuple[Sequence[ir.Node], Callable[[str], str]]]
                       ) -> List[QueryResult]:
+        """Two tiers.  (1) Every query compiled *light* (structural presolve
+        only) and searched on the device within a short budget: whatever the
+        device decides (sat with its canonical witness, or unsat) is final --
+        the model set and the witness order are the same as after the full
+        presolve.  (2) The rest -- queries the light compile cannot bound or
+        the budget did not finish -- through the full presolve and the
+        device with the reference's per-query budget.  ``two_tier = False``
+        runs (2) alone."""
+        if not self.two_tier or not queries:
+            return self._check_full(queries)
+        t0 = time.perf_counter()
+        light = self.compile(queries, light=True)
+        self.stats.compile_s += time.perf_counter() - t0
+        ok = [i for i, (cq, _) in enumerate(light) if cq is not None]
+        out: List[Optional[QueryResult]] = [None] * len(queries)
+        if ok:
+            res = self.decide([light[i] for i in ok], budget_s=self.tier1_budget(len(ok)))
+            for i, r in zip(ok, res):
+                if r.status in ("sat", "unsat"):
+                    out[i] = r
+                    self.stats.tier1_decided += 1
+        redo = [i for i, r in enumerate(out) if r is None]
+        if redo:
+            for i, r in zip(redo, self._check_full([queries[i] for i in redo])):
+                out[i] = r
+        self.stats.tier2_queries += len(redo)
+        return out  # type: ignore[return-value]
+
+    def _check_full(self, queries) -> List[QueryResult]:
         if self.compile_workers > 1 and len(queries) >= self.POOL_MIN_BATCH:
             return self._check_pipelined(queries)
         t0 = time.perf_counter()
