@@ -100,6 +100,9 @@ class CompilePool:
         pkg_root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         env = dict(os.environ)
         env["PYTHONPATH"] = pkg_root + os.pathsep + env.get("PYTHONPATH", "")
+        import threading
+
+        self._lock = threading.Lock()
         self.workers = workers
         self.procs = [subprocess.Popen([sys.executable, "-m", __package__ + ".compile_worker"],
                                        stdin=subprocess.PIPE, stdout=subprocess.PIPE, env=env)
@@ -136,7 +139,12 @@ class CompilePool:
     def compile(self, queries, on_chunk=None, light: bool = False
                 ) -> List[Tuple[Optional[CompiledQuery], Optional[str]]]:
         """Compile a batch; ``on_chunk(indices, results)`` (optional) is
-        called as each chunk of the batch completes, from a driver thread."""
+        called as each chunk of the batch completes, from a driver thread.
+        Concurrent calls (the two-tier checker's overlap) take turns."""
+        with self._lock:
+            return self._compile(queries, on_chunk, light)
+
+    def _compile(self, queries, on_chunk, light):
         import threading
 
         items = [_portable(q) + (light,) for q in queries]
@@ -213,6 +221,9 @@ class SiteChecker:
         self._pool: Optional[CompilePool] = None
         # light first tier on the device before the full presolve
         self.two_tier = os.environ.get("MK_TWO_TIER", "1") != "0"
+        import threading
+
+        self._device_lock = threading.Lock()
 
     def close(self) -> None:
         if self._pool is not None:
@@ -249,7 +260,8 @@ class SiteChecker:
         lim = dict(self.limits)
         lim["max_seconds"] = (budget_s if budget_s is not None else
                               min(self.limits["max_seconds"] * max(len(compiled), 1), 3600.0))
-        results = self.engine.solve_packed(packed, lim) if packed.problems else []
+        with self._device_lock:   # one engine call at a time per context
+            results = self.engine.solve_packed(packed, lim) if packed.problems else []
         t1 = time.perf_counter()
         out: List[QueryResult] = []
         for (cq, err), off in zip(compiled, offsets):
@@ -272,7 +284,7 @@ class SiteChecker:
     # first tier: device budget for the whole light batch (seconds): per query,
     # clamped (measured on the B200: the light tier decides 65 % of the golden
     # corpus's sites within 20 ms per batch)
-    TIER1_S = (0.002, 0.005, 0.02)   # per query, minimum, maximum
+    TIER1_S = (0.001, 0.002, 0.02)   # per query, minimum, maximum
 
     def tier1_budget(self, n: int) -> float:
         per, lo, hi = self.TIER1_S
@@ -290,22 +302,50 @@ class SiteChecker:
         runs (2) alone."""
         if not self.two_tier or not queries:
             return self._check_full(queries)
+        import threading
+
         t0 = time.perf_counter()
         light = self.compile(queries, light=True)
         self.stats.compile_s += time.perf_counter() - t0
         ok = [i for i, (cq, _) in enumerate(light) if cq is not None]
+        failed = [i for i, (cq, _) in enumerate(light) if cq is None]
         out: List[Optional[QueryResult]] = [None] * len(queries)
+        # the queries the light compile could not bound are certainly second
+        # tier: their full presolve starts now, on the worker pool, while the
+        # device runs the first tier (engine calls take turns)
+        early: List[object] = []
+
+        def second_tier_early() -> None:
+            try:
+                early.append(self._check_full([queries[i] for i in failed]))
+            except BaseException as exc:  # surfaced below
+                early.append(exc)
+
+        th = None
+        if failed and self.compile_workers > 1:
+            th = threading.Thread(target=second_tier_early)
+            th.start()
+        elif failed:
+            second_tier_early()
         if ok:
             res = self.decide([light[i] for i in ok], budget_s=self.tier1_budget(len(ok)))
             for i, r in zip(ok, res):
                 if r.status in ("sat", "unsat"):
                     out[i] = r
                     self.stats.tier1_decided += 1
-        redo = [i for i, r in enumerate(out) if r is None]
+        redo = [i for i in ok if out[i] is None]
         if redo:
             for i, r in zip(redo, self._check_full([queries[i] for i in redo])):
                 out[i] = r
-        self.stats.tier2_queries += len(redo)
+        if th is not None:
+            th.join()
+        if failed:
+            got = early[0]
+            if isinstance(got, BaseException):
+                raise got
+            for i, r in zip(failed, got):
+                out[i] = r
+        self.stats.tier2_queries += len(redo) + len(failed)
         return out  # type: ignore[return-value]
 
     def _check_full(self, queries) -> List[QueryResult]:
