@@ -185,6 +185,53 @@ class CompilePool:
             raise errors[0]
         return out
 
+    def stream(self, jobs, on_done) -> None:
+        """Serve compile jobs until a ``None`` job arrives: ``jobs`` is a
+        queue.PriorityQueue of (priority, seq, index, item) -- item as for
+        _compile_one -- and ``on_done(indices, results)`` is called per
+        finished chunk (from a driver thread; it may enqueue more jobs).
+        Blocks until every worker has drained; re-raises a worker failure."""
+        import queue as _q
+        import threading
+
+        with self._lock:
+            errors: List[BaseException] = []
+            stop = threading.Event()
+
+            def drive(proc) -> None:
+                while not stop.is_set():
+                    job = jobs.get()
+                    if job[3] is None:
+                        jobs.put(job)          # the sentinel stays for the others
+                        return
+                    batch = [job]
+                    while len(batch) < 4:
+                        try:
+                            nxt = jobs.get_nowait()
+                        except _q.Empty:
+                            break
+                        if nxt[3] is None:
+                            jobs.put(nxt)
+                            break
+                        batch.append(nxt)
+                    try:
+                        self._send(proc, [b[3] for b in batch])
+                        got = self._recv(proc)
+                        on_done([b[2] for b in batch], got)
+                    except BaseException as exc:  # surfaced to the caller below
+                        errors.append(exc)
+                        stop.set()
+                        jobs.put((-1, -1, -1, None))
+                        return
+
+            threads = [threading.Thread(target=drive, args=(p,)) for p in self.procs]
+            for t in threads:
+                t.start()
+            for t in threads:
+                t.join()
+            if errors:
+                raise errors[0]
+
     def close(self) -> None:
         for p in self.procs:
             try:
@@ -302,50 +349,110 @@ class SiteChecker:
         runs (2) alone."""
         if not self.two_tier or not queries:
             return self._check_full(queries)
-        import threading
-
-        t0 = time.perf_counter()
-        light = self.compile(queries, light=True)
-        self.stats.compile_s += time.perf_counter() - t0
+        if self.compile_workers > 1 and len(queries) >= self.POOL_MIN_BATCH:
+            return self._check_streaming(queries)
+        light = compile_all(queries, light=True)
         ok = [i for i, (cq, _) in enumerate(light) if cq is not None]
-        failed = [i for i, (cq, _) in enumerate(light) if cq is None]
         out: List[Optional[QueryResult]] = [None] * len(queries)
-        # the queries the light compile could not bound are certainly second
-        # tier: their full presolve starts now, on the worker pool, while the
-        # device runs the first tier (engine calls take turns)
-        early: List[object] = []
-
-        def second_tier_early() -> None:
-            try:
-                early.append(self._check_full([queries[i] for i in failed]))
-            except BaseException as exc:  # surfaced below
-                early.append(exc)
-
-        th = None
-        if failed and self.compile_workers > 1:
-            th = threading.Thread(target=second_tier_early)
-            th.start()
-        elif failed:
-            second_tier_early()
         if ok:
             res = self.decide([light[i] for i in ok], budget_s=self.tier1_budget(len(ok)))
             for i, r in zip(ok, res):
                 if r.status in ("sat", "unsat"):
                     out[i] = r
                     self.stats.tier1_decided += 1
-        redo = [i for i in ok if out[i] is None]
+        redo = [i for i, r in enumerate(out) if r is None]
         if redo:
             for i, r in zip(redo, self._check_full([queries[i] for i in redo])):
                 out[i] = r
-        if th is not None:
+        self.stats.tier2_queries += len(redo)
+        return out  # type: ignore[return-value]
+
+    def _check_streaming(self, queries) -> List[QueryResult]:
+        """The two tiers as one stream over the worker pool and the device:
+        light compiles flow to the device's first tier as they finish; a
+        query the light compile cannot bound, or the first tier does not
+        decide, goes back to the pool for its full presolve (ahead of the
+        remaining light compiles) and then to the device's second tier.  The
+        device thread decides whatever has arrived in one batch per tier."""
+        import itertools
+        import queue
+        import threading
+
+        if self._pool is None:
+            self._pool = CompilePool(self.compile_workers)
+        n = len(queries)
+        items = [_portable(q) for q in queries]
+        jobs: "queue.PriorityQueue" = queue.PriorityQueue()
+        seq = itertools.count()
+        for i in sorted(range(n), key=lambda i: -len(items[i][0])):
+            jobs.put((1, next(seq), i, items[i] + (True,)))       # light first
+        ready: "queue.Queue" = queue.Queue()
+        out: List[Optional[QueryResult]] = [None] * n
+        failure: List[BaseException] = []
+
+        def on_done(idxs, results) -> None:
+            for i, r in zip(idxs, results):
+                ready.put((i, r))
+
+        def full_job(i) -> None:
+            jobs.put((0, next(seq), i, items[i] + (False,)))      # ahead of light jobs
+
+        def device_loop() -> None:
+            done = 0
+            light_seen = set()
+            while done < n and not failure:
+                batch = [ready.get()]
+                while True:
+                    try:
+                        batch.append(ready.get_nowait())
+                    except queue.Empty:
+                        break
+                if any(b is None for b in batch):
+                    return
+                tier1, tier2 = [], []
+                for i, (cq, err) in batch:
+                    if i not in light_seen:
+                        light_seen.add(i)
+                        if cq is None:
+                            full_job(i)            # the light compile cannot bound it
+                        else:
+                            tier1.append((i, (cq, err)))
+                    else:
+                        tier2.append((i, (cq, err)))
+                try:
+                    if tier1:
+                        res = self.decide([c for _, c in tier1],
+                                          budget_s=self.tier1_budget(len(tier1)))
+                        for (i, _), r in zip(tier1, res):
+                            if r.status in ("sat", "unsat"):
+                                out[i] = r
+                                done += 1
+                                self.stats.tier1_decided += 1
+                            else:
+                                full_job(i)
+                    if tier2:
+                        res = self.decide([c for _, c in tier2])
+                        for (i, _), r in zip(tier2, res):
+                            out[i] = r
+                            done += 1
+                            self.stats.tier2_queries += 1
+                except BaseException as exc:  # surfaced to the caller below
+                    failure.append(exc)
+            jobs.put((2, next(seq), -1, None))                     # stop the pool
+
+        th = threading.Thread(target=device_loop)
+        th.start()
+        t0 = time.perf_counter()
+        try:
+            self._pool.stream(jobs, on_done)
+        except BaseException as exc:
+            failure.append(exc)
+            ready.put(None)
+        finally:
+            self.stats.compile_s += time.perf_counter() - t0
             th.join()
-        if failed:
-            got = early[0]
-            if isinstance(got, BaseException):
-                raise got
-            for i, r in zip(failed, got):
-                out[i] = r
-        self.stats.tier2_queries += len(redo) + len(failed)
+        if failure:
+            raise failure[0]
         return out  # type: ignore[return-value]
 
     def _check_full(self, queries) -> List[QueryResult]:
