@@ -271,6 +271,7 @@ class SiteChecker:
         import threading
 
         self._device_lock = threading.Lock()
+        self._warm = False
 
     def close(self) -> None:
         if self._pool is not None:
@@ -308,6 +309,13 @@ class SiteChecker:
         lim["max_seconds"] = (budget_s if budget_s is not None else
                               min(self.limits["max_seconds"] * max(len(compiled), 1), 3600.0))
         with self._device_lock:   # one engine call at a time per context
+            if budget_s is not None and not self._warm and packed.problems:
+                # the first engine call of a context allocates its work
+                # buffers (GiBs of box stacks); a short first-tier budget
+                # must not pay for that: one untimed call first
+                self.engine.solve_packed(packed, lim)
+            if packed.problems:
+                self._warm = True
             results = self.engine.solve_packed(packed, lim) if packed.problems else []
         t1 = time.perf_counter()
         out: List[QueryResult] = []
