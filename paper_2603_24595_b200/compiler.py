@@ -1002,7 +1002,20 @@ class _Presolve:
             self.widths[kname] = "i64"
             self.pos[kname] = self.pos[v] - 0.25
             self.maximize[kname] = self.maximize.get(v, False) ^ (av < 0)
-            self.bounds[kname] = (None, None)
+            # the lattice coordinate's range implied by v's range and the rest
+            # of the index (kk = (av*v + k0 + R - r) / m): exact interval
+            # arithmetic, so the light presolve (no tightening passes) still
+            # hands the device a bounded box
+            kb: Tuple[Optional[int], Optional[int]] = (None, None)
+            vlo, vhi = self.bounds.get(v, (None, None))
+            others_lf = ({t: x for t, x in terms.items() if t != v}, k0 - r)
+            olo, ohi = _Ivl(self.bounds)(lin_to_ir(others_lf, self.widths)) \
+                if others_lf[0] else (others_lf[1], others_lf[1])
+            if None not in (vlo, vhi, olo, ohi):
+                nlo = min(av * vlo, av * vhi) + olo
+                nhi = max(av * vlo, av * vhi) + ohi
+                kb = (-((-nlo) // m), nhi // m)
+            self.bounds[kname] = kb
             rest = {t: -x * av for t, x in terms.items() if t != v}
             rest[kname] = m * av
             expr = lin_to_ir((rest, (r - k0) * av), self.widths)
