@@ -53,7 +53,10 @@ def main(budget_s, names):
             if any(g.status == "unsat" for g in cq.groups):
                 host += 1
                 continue
-            if r.status == "unknown" and not any(g.status == "unknown" for g in cq.groups):
+            if r.status == "unknown":
+                # not decided by the light tier (budget, or a float / give-up
+                # component whose verdict the full presolve settles): the
+                # product sends it to the second tier
                 und += 1
                 continue
             dev += 1
