@@ -35,7 +35,9 @@ from .engine import QueryResult, SiteChecker
 
 Query = Tuple[Sequence[ir.Node], Callable[[str], str]]
 
-_STATUS = {"unsat": 0, "sat": 1, "unknown": 2}
+# "giveup": undecided for a reason other than the budget (an overflow or
+# engine limit) -- unknown in the result, never searched again
+_STATUS = {"unsat": 0, "sat": 1, "unknown": 2, "giveup": 3}
 _STATUS_NAME = {v: k for k, v in _STATUS.items()}
 _MASK64 = (1 << 64) - 1
 
@@ -154,7 +156,7 @@ def combine_slabs(problems: Sequence[Problem],
     out = []
     for k, p in enumerate(problems):
         rs = [r[k] for r in per_rank]
-        if any(s == "unknown" for s, _ in rs):
+        if any(s in ("unknown", "giveup") for s, _ in rs):
             out.append(("unknown", None))
             continue
         best = None
@@ -203,10 +205,43 @@ def _all_gather_records(rec: List[int], device, group=None) -> List[List[int]]:
     return [[int(x) for x in o.cpu().tolist()] for o in outs]
 
 
+def slab_rounds(total_s: float, first_s: float = 0.25) -> List[float]:
+    """Budget of each exchange round of ``check_slabbed``: doubling slices
+    from ``first_s`` whose sum is ``total_s`` (the same schedule on every
+    rank, so every rank enters the same number of collectives)."""
+    out: List[float] = []
+    left, cur = float(total_s), float(first_s)
+    while left > 1e-9:
+        t = min(cur, left)
+        out.append(t)
+        left -= t
+        cur *= 2.0
+    return out or [float(total_s)]
+
+
+def dominated(p: Problem, rank: int, statuses: Sequence[str]) -> bool:
+    """Slab ``rank`` of ``p`` cannot hold the combined answer once another
+    slab has a model: slabs are ordered best first along the first symbol
+    with two values (every earlier symbol is fixed), so every point of a
+    lower slab precedes every point of this one in witness order; for a
+    feasibility-only problem any model decides."""
+    if p.any_model:
+        return any(s == "sat" for r, s in enumerate(statuses) if r != rank)
+    return any(s == "sat" for s in statuses[:rank])
+
+
 def check_slabbed(checker: SiteChecker, queries: Sequence[Query], group=None,
-                  device=None) -> List[QueryResult]:
+                  device=None, first_round_s: float = 0.25) -> List[QueryResult]:
     """Decide one site set with every problem's root box split across the
-    ranks of ``group``; every rank returns the same results."""
+    ranks of ``group``; every rank returns the same results.
+
+    The search runs in rounds of doubling budget (``slab_rounds``).  After
+    each round the ranks exchange their per-problem results (one all-gather
+    of fixed-width records): a slab still undecided on one rank stops as soon
+    as a better-ordered slab has a model (``dominated``), i.e. the incumbents
+    are shared at round boundaries; only the slabs still open are searched
+    again, with twice the budget.  Without budget cut-offs the result is the
+    exact combination (``combine_slabs``) of every slab's optimum."""
     rank, world = _world(group)
     compiled = checker.compile(queries)
     problems: List[Problem] = []
@@ -216,23 +251,50 @@ def check_slabbed(checker: SiteChecker, queries: Sequence[Query], group=None,
         if cq is not None:
             problems.extend(cq.problems)
     mine = [slab(p, rank, world) for p in problems]
-    run = [p for p in mine if p is not None]
-    lim = dict(checker.limits)
-    lim["max_seconds"] = min(checker.limits["max_seconds"] * max(len(queries), 1), 3600.0)
-    solved = checker.engine.solve(run, lim) if run else []
-    it = iter(solved)
-    local = [next(it) if p is not None else ("unsat", None) for p in mine]
-    if world > 1:
-        if device is None:
-            # NCCL only moves device tensors; gloo (the CPU tests) host ones
-            import torch
+    local: List[Tuple[str, Optional[List[int]]]] = [
+        ("unsat", None) if m is None else ("unknown", None) for m in mine]
+    live = [k for k, m in enumerate(mine) if m is not None]
+    total = min(checker.limits["max_seconds"] * max(len(queries), 1), 3600.0)
+    if world > 1 and device is None:
+        # NCCL only moves device tensors; gloo (the CPU tests) host ones
+        import torch
 
-            nccl = _dist().get_backend(group) == "nccl"
-            device = f"cuda:{torch.cuda.current_device()}" if nccl else "cpu"
-        recs = _all_gather_records(_encode(problems, local), device, group)
-        per_rank = [_decode(problems, r) for r in recs]
-    else:
-        per_rank = [local]
+        nccl = _dist().get_backend(group) == "nccl"
+        device = f"cuda:{torch.cuda.current_device()}" if nccl else "cpu"
+    per_rank = [local]
+    self_rounds = 0
+    for budget in slab_rounds(total, first_round_s):
+        if live:
+            lim = dict(checker.limits)
+            lim["max_seconds"] = budget
+            solved = checker.engine.solve([mine[k] for k in live], lim)
+            # a call that ended well inside its budget did not cut anything
+            # off: its unknowns are give-ups, not worth a longer round
+            cut = checker.engine.last_stats.get("seconds", budget) >= 0.5 * budget
+            for k, r in zip(live, solved):
+                local[k] = r if (r[0] != "unknown" or cut) else ("giveup", None)
+        self_rounds += 1
+        if world > 1:
+            recs = _all_gather_records(_encode(problems, local), device, group)
+            per_rank = [_decode(problems, r) for r in recs]
+        else:
+            per_rank = [local]
+        # open = undecided here and not dominated by another slab's model
+        # (computed from the gathered records: the same on every rank)
+        open_any = False
+        for k, p in enumerate(problems):
+            sts = [pr[k][0] for pr in per_rank]
+            for r in range(world):
+                if sts[r] == "unknown" and dominated(p, r, sts):
+                    sts[r] = "unsat"          # nothing here beats the better slab
+                    per_rank[r][k] = ("unsat", None)
+            if "unknown" in sts:
+                open_any = True
+        local[:] = per_rank[rank]
+        live = [k for k in live if local[k][0] == "unknown"]
+        if not open_any:
+            break
+    checker.last_slab_rounds = self_rounds
     results = combine_slabs(problems, per_rank)
     out: List[QueryResult] = []
     for (cq, err), off in zip(compiled, offsets):

@@ -103,6 +103,85 @@ def test_combine_is_lexicographic_and_conservative():
     assert combine_slabs([p], [unknown, sat_hi]) == [("unknown", None)]
 
 
+def test_slab_rounds_and_domination():
+    from paper_2603_24595_b200.compiler import Problem
+    from paper_2603_24595_b200.shard import dominated, slab_rounds
+
+    r = slab_rounds(30.0, 0.25)
+    assert abs(sum(r) - 30.0) < 1e-9 and r[:3] == [0.25, 0.5, 1.0]
+    assert slab_rounds(0.1, 0.25) == [0.1]
+    p = Problem(var_names=["a"], lo=[0], hi=[9], maximize=[False])
+    # a model in a better-ordered slab closes the later ones, not the earlier
+    assert dominated(p, 1, ["sat", "unknown", "unknown"])
+    assert dominated(p, 2, ["unsat", "sat", "unknown"])
+    assert not dominated(p, 0, ["unknown", "sat", "unknown"])
+    q = Problem(var_names=["a"], lo=[0], hi=[9], maximize=[False], any_model=True)
+    assert dominated(q, 0, ["unknown", "sat"])      # feasibility: any model decides
+
+
+class _StubEngine:
+    """Rank 0's slab has a model at once; rank 1's slab never finishes in
+    budget (every round ends on the clock)."""
+
+    def __init__(self, rank):
+        self.rank, self.calls, self.last_stats = rank, 0, {}
+
+    def solve(self, problems, lim):
+        self.calls += 1
+        self.last_stats = {"seconds": lim["max_seconds"]}
+        if self.rank == 0:
+            return [("sat", [p.lo[0]]) for p in problems]
+        return [("unknown", None) for _ in problems]
+
+
+class _StubChecker:
+    def __init__(self, rank):
+        from paper_2603_24595_b200.compiler import CompiledQuery, Group, Problem
+
+        self.limits = {"max_seconds": 30.0}
+        self.engine = _StubEngine(rank)
+        p = Problem(var_names=["a"], lo=[0], hi=[99], maximize=[False])
+        self.cq = CompiledQuery(witness_names=["a"], order=[("a", "min")],
+                                groups=[Group("pending", None, False, problems=[0])],
+                                problems=[p], defs={}, free_default={})
+
+    def compile(self, queries):
+        return [(self.cq, None) for _ in queries]
+
+
+def _incumbent_worker(rank, world, port, out_dir):
+    import json
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from paper_2603_24595_b200 import shard
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        chk = _StubChecker(rank)
+        res = shard.check_slabbed(chk, [None])
+        with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
+            json.dump({"calls": chk.engine.calls, "rounds": chk.last_slab_rounds,
+                       "res": [(r.status, r.witness) for r in res]}, fh)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_incumbent_exchange_stops_dominated_slab(tmp_path):
+    """Rank 1's undecided slab stops after the first exchange: rank 0's
+    model precedes every point of it, so the answer is rank 0's model."""
+    import json
+
+    import torch.multiprocessing as mp
+
+    mp.spawn(_incumbent_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    outs = [json.load(open(os.path.join(tmp_path, f"rank{r}.json"))) for r in range(2)]
+    assert outs[0]["res"] == outs[1]["res"] == [["sat", {"a": 0}]]
+    assert outs[1]["calls"] == 1 and outs[0]["rounds"] == outs[1]["rounds"] == 1
+
+
 def test_deal_balances_and_covers():
     from paper_2603_24595_b200.shard import deal
 
