@@ -30,10 +30,17 @@
 #define MK_HD __host__ __device__ __forceinline__
 #define MK_HDM __host__ __device__ __forceinline__ static
 #define MK_HDF __host__ __device__ __forceinline__   /* non-static member functions */
+#define MK_HDN __host__ __device__ __noinline__      /* rare, large: one copy, called */
+/* runtime-bounded loops stay rolled: unrolled copies of the 64-bit
+   division / multiply sequences made the search kernel's code exceed the
+   instruction caches (ncu: no_inst the top stall) */
+#define MK_NOUNROLL _Pragma("unroll 1")
 #else
+#define MK_NOUNROLL
 #define MK_HD static inline
 #define MK_HDM static inline
 #define MK_HDF inline
+#define MK_HDN static __attribute__((noinline))
 #endif
 
 typedef __int128 i128;
@@ -230,6 +237,80 @@ MK_HD void mk_iv_div_part(V xlo, V xhi, V d1, V d2, V* lo, V* hi) {
   mk_corners(mk_tdiv(xlo, d1), mk_tdiv(xlo, d2), mk_tdiv(xhi, d1), mk_tdiv(xhi, d2), lo, hi);
 }
 
+// interval division / remainder (both operands OK): not inlined -- each
+// corner is a 64- or 128-bit division sequence, and inlining it into every
+// evaluator copy made the search kernel's code too large for the instruction
+// caches
+template <typename V>
+MK_HDN MkIvT<V> mk_iv_divmod(int op, MkIvT<V> a, MkIvT<V> b, bool err) {
+  typedef MkNum<V> N;
+  const V INF = N::inf();
+  MkIvT<V> r;
+  r.lo = 0;
+  r.hi = 0;
+  r.fl = 0;
+  {
+    bool has0 = b.lo <= 0 && b.hi >= 0;
+    if (has0) err = true;
+    if (b.lo == 0 && b.hi == 0) {  // every point divides by zero
+      r.fl = MK_FL_ERR;
+      return r;
+    }
+    if (op == MK_OP_DIV) {
+      bool first = true;
+      if (b.hi >= 1) {  // positive divisor part
+        V l, h;
+        mk_iv_div_part<V>(a.lo, a.hi, mk_max<V>(b.lo, 1), b.hi, &l, &h);
+        r.lo = l; r.hi = h; first = false;
+      }
+      if (b.lo <= -1) {
+        V l, h;
+        mk_iv_div_part<V>(a.lo, a.hi, b.lo, mk_min<V>(b.hi, -1), &l, &h);
+        if (first) { r.lo = l; r.hi = h; }
+        else { r.lo = mk_min(r.lo, l); r.hi = mk_max(r.hi, h); }
+      }
+      if (N::kWide && (a.lo == -INF || a.hi == INF)) {
+        // unbounded numerator: be explicit about the sign reach
+        if (a.lo == -INF) { if (b.hi >= 1) r.lo = -INF; if (b.lo <= -1) r.hi = INF; }
+        if (a.hi == INF) { if (b.hi >= 1) r.hi = INF; if (b.lo <= -1) r.lo = -INF; }
+      }
+    } else {
+      V m;  // max |divisor| - 1
+      if (N::isinf(b.lo) || N::isinf(b.hi)) m = INF;
+      else m = mk_max<V>(b.lo < 0 ? -b.lo : b.lo, b.hi < 0 ? -b.hi : b.hi) - 1;
+      bool xfin = !N::isinf(a.lo) && !N::isinf(a.hi);
+      bool dsing = mk_exact1(b);
+      if (op == MK_OP_MOD) {
+        if (xfin && dsing && a.lo == a.hi) {
+          r.lo = r.hi = a.lo % b.lo;
+        } else if (xfin && dsing && ((a.lo >= 0 && a.lo / b.lo == a.hi / b.lo) ||
+                                     (a.hi <= 0 && a.lo / b.lo == a.hi / b.lo))) {
+          r.lo = a.lo % b.lo;
+          r.hi = a.hi % b.lo;
+          if (r.lo > r.hi) { V t = r.lo; r.lo = r.hi; r.hi = t; }
+        } else {
+          r.lo = (a.lo >= 0) ? 0 : ((a.lo == -INF) ? -m : mk_max<V>(a.lo, -m));
+          r.hi = (a.hi <= 0) ? 0 : ((a.hi == INF) ? m : mk_min<V>(a.hi, m));
+        }
+      } else {
+        if (xfin && dsing) {
+          V M = b.lo < 0 ? -b.lo : b.lo;
+          if (mk_floordiv(a.lo, M) == mk_floordiv(a.hi, M)) {
+            r.lo = mk_emod_c(a.lo, M);
+            r.hi = mk_emod_c(a.hi, M);
+          } else {
+            r.lo = 0; r.hi = m;
+          }
+        } else {
+          r.lo = 0; r.hi = m;
+        }
+      }
+    }
+  }
+  r.fl = MK_FL_OK | (err ? MK_FL_ERR : 0);
+  return r;
+}
+
 template <typename V>
 MK_HD MkIvT<V> mk_iv_binop(int op, const MkIvT<V>& a, const MkIvT<V>& b) {
   typedef MkNum<V> N;
@@ -280,65 +361,8 @@ MK_HD MkIvT<V> mk_iv_binop(int op, const MkIvT<V>& a, const MkIvT<V>& b) {
     }
     case MK_OP_DIV:
     case MK_OP_MOD:
-    case MK_OP_EMOD: {
-      bool has0 = b.lo <= 0 && b.hi >= 0;
-      if (has0) err = true;
-      if (b.lo == 0 && b.hi == 0) {  // every point divides by zero
-        r.fl = MK_FL_ERR;
-        return r;
-      }
-      if (op == MK_OP_DIV) {
-        bool first = true;
-        if (b.hi >= 1) {  // positive divisor part
-          V l, h;
-          mk_iv_div_part<V>(a.lo, a.hi, mk_max<V>(b.lo, 1), b.hi, &l, &h);
-          r.lo = l; r.hi = h; first = false;
-        }
-        if (b.lo <= -1) {
-          V l, h;
-          mk_iv_div_part<V>(a.lo, a.hi, b.lo, mk_min<V>(b.hi, -1), &l, &h);
-          if (first) { r.lo = l; r.hi = h; }
-          else { r.lo = mk_min(r.lo, l); r.hi = mk_max(r.hi, h); }
-        }
-        if (N::kWide && (a.lo == -INF || a.hi == INF)) {
-          // unbounded numerator: be explicit about the sign reach
-          if (a.lo == -INF) { if (b.hi >= 1) r.lo = -INF; if (b.lo <= -1) r.hi = INF; }
-          if (a.hi == INF) { if (b.hi >= 1) r.hi = INF; if (b.lo <= -1) r.lo = -INF; }
-        }
-      } else {
-        V m;  // max |divisor| - 1
-        if (N::isinf(b.lo) || N::isinf(b.hi)) m = INF;
-        else m = mk_max<V>(b.lo < 0 ? -b.lo : b.lo, b.hi < 0 ? -b.hi : b.hi) - 1;
-        bool xfin = !N::isinf(a.lo) && !N::isinf(a.hi);
-        bool dsing = mk_exact1(b);
-        if (op == MK_OP_MOD) {
-          if (xfin && dsing && a.lo == a.hi) {
-            r.lo = r.hi = a.lo % b.lo;
-          } else if (xfin && dsing && ((a.lo >= 0 && a.lo / b.lo == a.hi / b.lo) ||
-                                       (a.hi <= 0 && a.lo / b.lo == a.hi / b.lo))) {
-            r.lo = a.lo % b.lo;
-            r.hi = a.hi % b.lo;
-            if (r.lo > r.hi) { V t = r.lo; r.lo = r.hi; r.hi = t; }
-          } else {
-            r.lo = (a.lo >= 0) ? 0 : ((a.lo == -INF) ? -m : mk_max<V>(a.lo, -m));
-            r.hi = (a.hi <= 0) ? 0 : ((a.hi == INF) ? m : mk_min<V>(a.hi, m));
-          }
-        } else {
-          if (xfin && dsing) {
-            V M = b.lo < 0 ? -b.lo : b.lo;
-            if (mk_floordiv(a.lo, M) == mk_floordiv(a.hi, M)) {
-              r.lo = mk_emod_c(a.lo, M);
-              r.hi = mk_emod_c(a.hi, M);
-            } else {
-              r.lo = 0; r.hi = m;
-            }
-          } else {
-            r.lo = 0; r.hi = m;
-          }
-        }
-      }
-      break;
-    }
+    case MK_OP_EMOD:
+      return mk_iv_divmod<V>(op, a, b, err);
     case MK_OP_EQ:
     case MK_OP_NE: {
       bool t = !(mk_sure_lt(a, b) || mk_sure_lt(b, a));
@@ -479,6 +503,7 @@ MK_HD MkBoxVerdict mk_eval_box_impl(const MkProb& P, Regs R, int64_t* insn_count
   v.all_true = true;
   v.overflow = false;
   v.und_mask = 0;
+  MK_NOUNROLL
   for (int k = 0; k < n; ++k) {
     const mk_insn in = P.insns[k];
     switch (in.op) {
@@ -525,11 +550,13 @@ MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const V* vlo, const V* vhi, MkIv
   typedef MkNum<V> N;
   const int nv = P.p->nvars;
   const int nc = P.p->nconst;
+  MK_NOUNROLL
   for (int i = 0; i < nv; ++i) {
     R[i].lo = vlo[i];
     R[i].hi = vhi[i];
     R[i].fl = MK_FL_OK;
   }
+  MK_NOUNROLL
   for (int i = 0; i < nc; ++i) {
     V c = N::ld(P.consts[i]);
     R[nv + i].lo = c;
@@ -563,6 +590,7 @@ MK_HD void mk_row_range(const mk_row& row, const mk_row_term* T, const V* lo, co
   fmin = N::ld(row.c0);
   fmax = fmin;
   nmin_inf = nmax_inf = 0;
+  MK_NOUNROLL
   for (int k = 0; k < row.nterms; ++k) {
     V c = N::ld(T[k].coef);
     int v = T[k].var;
@@ -591,6 +619,7 @@ MK_HD bool mk_row_tighten(const mk_row& row, const mk_row_term* T, V* lo, V* hi,
                           V fmax, int nmin_inf, int nmax_inf, bool& changed) {
   typedef MkNum<V> N;
   const V INF = N::inf();
+  MK_NOUNROLL
   for (int k = 0; k < row.nterms; ++k) {
     V c = N::ld(T[k].coef);
     int v = T[k].var;
@@ -635,8 +664,10 @@ MK_HD bool mk_row_tighten(const mk_row& row, const mk_row_term* T, V* lo, V* hi,
 template <typename V>
 MK_HD bool mk_contract(const MkProb& P, V* lo, V* hi, int sweeps) {
   const int nr = P.p->nrows;
+  MK_NOUNROLL
   for (int s = 0; s < sweeps; ++s) {
     bool changed = false;
+    MK_NOUNROLL
     for (int r = 0; r < nr;) {
       const mk_row row = P.rows[r];
       V fmin, fmax;
@@ -654,6 +685,7 @@ MK_HD bool mk_contract(const MkProb& P, V* lo, V* hi, int sweeps) {
       int e = r + 1;
       while (e < nr && P.rows[e].group == row.group) ++e;
       int live = -1, nlive = 0;
+      MK_NOUNROLL
       for (int q = r; q < e && nlive < 2; ++q) {
         const mk_row rq = P.rows[q];
         mk_row_range<V>(rq, P.terms + rq.term_off, lo, hi, fmin, fmax, nmin_inf, nmax_inf);
@@ -716,6 +748,7 @@ MK_HD bool mk_eval_point_impl(const MkProb& P, Regs R, bool* overflow, int64_t* 
   typedef MkNum<V> N;
   const int n = P.p->ninsn;
   bool ovf = false;
+  MK_NOUNROLL
   for (int k = 0; k < n; ++k) {
     const mk_insn in = P.insns[k];
     const MkCvT<V> a = R.get(in.a), b = R.get(in.b);
@@ -788,7 +821,9 @@ MK_HD bool mk_eval_point(const MkProb& P, const V* x, MkCvT<V>* R, bool* overflo
   typedef MkNum<V> N;
   const int nv = P.p->nvars;
   const int nc = P.p->nconst;
+  MK_NOUNROLL
   for (int i = 0; i < nv; ++i) { R[i].v = x[i]; R[i].err = 0; }
+  MK_NOUNROLL
   for (int i = 0; i < nc; ++i) { R[nv + i].v = N::ld(P.consts[i]); R[nv + i].err = 0; }
   return mk_eval_point_impl<V>(P, MkCvFile<V>{R}, overflow, insn_count);
 }
@@ -805,6 +840,7 @@ MK_HD bool mk_eval_point_t(const MkProb& P, const V* x, MkCvT<V>* T, bool* overf
 // lexicographic comparison in witness order: true when x is strictly better
 template <typename V>
 MK_HD bool mk_lex_better(const V* x, const V* y, int nv, uint64_t maxmask) {
+  MK_NOUNROLL
   for (int i = 0; i < nv; ++i) {
     if (x[i] == y[i]) continue;
     bool mx = (maxmask >> i) & 1;
@@ -816,6 +852,7 @@ MK_HD bool mk_lex_better(const V* x, const V* y, int nv, uint64_t maxmask) {
 // the best corner of a box (its lexicographic lower bound)
 template <typename V>
 MK_HD void mk_corner(const V* lo, const V* hi, int nv, uint64_t maxmask, V* out) {
+  MK_NOUNROLL
   for (int i = 0; i < nv; ++i) out[i] = ((maxmask >> i) & 1) ? hi[i] : lo[i];
 }
 
@@ -824,6 +861,7 @@ template <typename V>
 MK_HD int64_t mk_volume(const V* lo, const V* hi, int nv) {
   const u128 cap = ((u128)1) << 62;
   u128 v = 1;
+  MK_NOUNROLL
   for (int i = 0; i < nv; ++i) {
     u128 s = (u128)(hi[i] - lo[i]) + 1;
     if (s >= cap) return (int64_t)cap;
@@ -835,6 +873,7 @@ MK_HD int64_t mk_volume(const V* lo, const V* hi, int nv) {
 template <typename V>
 MK_HD double mk_volume_f(const V* lo, const V* hi, int nv) {
   double v = 1.0;
+  MK_NOUNROLL
   for (int i = 0; i < nv; ++i) v *= (double)(hi[i] - lo[i] + 1);
   return v;
 }
@@ -842,6 +881,7 @@ MK_HD double mk_volume_f(const V* lo, const V* hi, int nv) {
 // decode point #idx of a box in lexicographic order (index order == witness order)
 template <typename V>
 MK_HD void mk_decode(const V* lo, const V* hi, int nv, uint64_t maxmask, uint64_t idx, V* x) {
+  MK_NOUNROLL
   for (int i = nv - 1; i >= 0; --i) {
     uint64_t s = (uint64_t)(hi[i] - lo[i] + 1);
     uint64_t d = idx % s;
@@ -861,6 +901,7 @@ MK_HD int mk_pick_split(const V* lo, const V* hi, int nv, uint64_t und_mask,
                         bool have_incumbent) {
   int best = -1;
   V bw = 0;
+  MK_NOUNROLL
   for (int i = 0; i < nv; ++i) {
     if (!((und_mask >> i) & 1) || lo[i] >= hi[i]) continue;
     if (have_incumbent) return i;

@@ -127,11 +127,25 @@ struct LaneStats {
 __device__ __forceinline__ bool is_narrow(const mk_problem& p) {
   return (p.flags & MK_PF_NARROW) != 0;
 }
+// specialised k_search code paths for small problems (8 symbols: 64-entry
+// local register files; 24 registers: the register file in shared memory).
+// Off: one generic path per class is faster on every corpus set measured on
+// the B200 (config3 40.7 -> 36.2 ms, paged_attention_v2 long 32.2 -> 29.6,
+// moe_align 18.4 -> 17.3; profiles/r02_code_paths.jsonl) -- the three inlined
+// copies made k_search<int64_t> 46 k SASS instructions, and 40 % of its
+// stall samples were instruction fetch (no_inst) -- and a budgeted run
+// keeps its budget (the small path overran a 0.5 s budget by 0.49 s)
+#ifndef MK_SMALL_PATH
+#define MK_SMALL_PATH 0
+#endif
+#ifndef MK_SHREG_PATH
+#define MK_SHREG_PATH 0
+#endif
 __device__ __forceinline__ bool is_small(const mk_problem& p) {
-  return p.nvars <= SMALL_V && p.nregs <= SMALL_R;
+  return MK_SMALL_PATH && p.nvars <= SMALL_V && p.nregs <= SMALL_R;
 }
 __device__ __forceinline__ bool is_shreg(const mk_problem& p) {
-  return is_narrow(p) && p.nvars <= SMALL_V && p.nregs <= SH_R;
+  return MK_SHREG_PATH && is_narrow(p) && p.nvars <= SMALL_V && p.nregs <= SH_R;
 }
 
 __device__ __forceinline__ Box* box_at(void* base, size_t box_bytes, size_t i) {
