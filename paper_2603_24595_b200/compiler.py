@@ -813,11 +813,16 @@ class _Presolve:
         return False
 
     def _substitute(self, name: str, e: Node) -> None:
-        m = {name: e}
-        self.atoms = [ir.substitute(a, m) for a in self.atoms]
+        self._substitute_many({name: e})
+
+    def _substitute_many(self, m: Dict[str, Node]) -> None:
+        """Replace every symbol of ``m`` at once; the replacements must not
+        mention each other's symbols (constants, say)."""
+        memo: Dict[Node, Node] = {}
+        self.atoms = [ir.substitute(a, m, memo) for a in self.atoms]
         for k in list(self.defs):
-            self.defs[k] = ir.substitute(self.defs[k], m)
-        self.defs[name] = e
+            self.defs[k] = ir.substitute(self.defs[k], m, memo)
+        self.defs.update(m)
 
     def _eliminate(self, name: str, e: Node) -> None:
         lo, hi = self.bounds.pop(name, (None, None))
@@ -887,9 +892,9 @@ class _Presolve:
         fixed = [(n, b[0]) for n, b in self.bounds.items()
                  if b[0] is not None and b[0] == b[1]]
         if fixed:
-            for n, v in fixed:
+            for n, _ in fixed:
                 del self.bounds[n]
-                self._substitute(n, ("c", v, "i64"))
+            self._substitute_many({n: ("c", v, "i64") for n, v in fixed})
             return True
         if changed:
             return True

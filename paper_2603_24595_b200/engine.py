@@ -37,6 +37,10 @@ class BatchStats:
     compile_s: float = 0.0
     tier1_decided: int = 0         # queries decided by the light first tier
     tier2_queries: int = 0         # queries that went through the full presolve
+    tier1_batches: int = 0         # device calls of the first tier
+    tier1_s: float = 0.0           # wall time of those calls
+    tier2_batches: int = 0
+    tier2_s: float = 0.0
     device_s: float = 0.0
     assemble_s: float = 0.0
     device: Dict[str, float] = field(default_factory=dict)
@@ -204,13 +208,17 @@ class CompilePool:
                     if job[3] is None:
                         jobs.put(job)          # the sentinel stays for the others
                         return
+                    # several jobs per round trip only while the queue is
+                    # long and only for the same priority class: a full
+                    # presolve (up to ~200 ms) sits on its site's critical
+                    # path and is never queued behind another one
                     batch = [job]
-                    while len(batch) < 4:
+                    while len(batch) < 4 and jobs.qsize() > 2 * len(self.procs):
                         try:
                             nxt = jobs.get_nowait()
                         except _q.Empty:
                             break
-                        if nxt[3] is None:
+                        if nxt[3] is None or nxt[0] != job[0] or job[0] == 0:
                             jobs.put(nxt)
                             break
                         batch.append(nxt)
@@ -268,6 +276,8 @@ class SiteChecker:
         self._pool: Optional[CompilePool] = None
         # light first tier on the device before the full presolve
         self.two_tier = os.environ.get("MK_TWO_TIER", "1") != "0"
+        # (t_ms, event, ...) records of the streaming pipeline when a list
+        self.trace: Optional[list] = None
         import threading
 
         self._device_lock = threading.Lock()
@@ -398,7 +408,15 @@ class SiteChecker:
         out: List[Optional[QueryResult]] = [None] * n
         failure: List[BaseException] = []
 
+        t00 = time.perf_counter()
+        trace = self.trace
+
+        def ev(*what) -> None:
+            if trace is not None:
+                trace.append((round((time.perf_counter() - t00) * 1e3, 2),) + what)
+
         def on_done(idxs, results) -> None:
+            ev("compiled", list(idxs))
             for i, r in zip(idxs, results):
                 ready.put((i, r))
 
@@ -429,8 +447,12 @@ class SiteChecker:
                         tier2.append((i, (cq, err)))
                 try:
                     if tier1:
+                        ev("tier1", [i for i, _ in tier1])
+                        t1 = time.perf_counter()
                         res = self.decide([c for _, c in tier1],
                                           budget_s=self.tier1_budget(len(tier1)))
+                        self.stats.tier1_batches += 1
+                        self.stats.tier1_s += time.perf_counter() - t1
                         for (i, _), r in zip(tier1, res):
                             if r.status in ("sat", "unsat"):
                                 out[i] = r
@@ -439,13 +461,18 @@ class SiteChecker:
                             else:
                                 full_job(i)
                     if tier2:
+                        ev("tier2", [i for i, _ in tier2])
+                        t2 = time.perf_counter()
                         res = self.decide([c for _, c in tier2])
+                        self.stats.tier2_batches += 1
+                        self.stats.tier2_s += time.perf_counter() - t2
                         for (i, _), r in zip(tier2, res):
                             out[i] = r
                             done += 1
                             self.stats.tier2_queries += 1
                 except BaseException as exc:  # surfaced to the caller below
                     failure.append(exc)
+                ev("device_idle", done)
             jobs.put((2, next(seq), -1, None))                     # stop the pool
 
         th = threading.Thread(target=device_loop)

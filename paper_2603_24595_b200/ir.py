@@ -221,10 +221,14 @@ def contains(e: Node, needle: Node) -> bool:
     return any(contains(c, needle) for c in children(e))
 
 
-def substitute(e: Node, mapping: Mapping[str, Node]) -> Node:
+def substitute(e: Node, mapping: Mapping[str, Node],
+               memo: Optional[Dict[Node, Node]] = None) -> Node:
+    """``e`` with every symbol of ``mapping`` replaced; ``memo`` may be shared
+    by calls with the same mapping (shared subtrees are rewritten once)."""
     if not mapping:
         return e
-    memo: Dict[Node, Node] = {}
+    if memo is None:
+        memo = {}
 
     def go(n: Node) -> Node:
         got = memo.get(n)

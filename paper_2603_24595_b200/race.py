@@ -142,10 +142,11 @@ class _BoundsOnly(_Presolve):
         super().__init__(*a, **kw)
         self.fixed: Dict[str, int] = {}
 
-    def _substitute(self, name, e):
-        if e[0] == "c":
-            self.fixed[name] = e[1]
-        super()._substitute(name, e)
+    def _substitute_many(self, m):
+        for name, e in m.items():
+            if e[0] == "c":
+                self.fixed[name] = e[1]
+        super()._substitute_many(m)
 
     def _try_eliminate(self, lin):
         return False
