@@ -44,11 +44,29 @@
 
 namespace {
 
+// specialised k_search code paths for small problems (8 symbols: 64-entry
+// local register files; 24 registers: the register file in shared memory).
+// Off: one generic path per class is faster on every corpus set measured on
+// the B200 (config3 40.7 -> 36.2 ms, paged_attention_v2 long 32.2 -> 29.6,
+// moe_align 18.4 -> 17.3; profiles/r02_code_paths.jsonl) -- the three inlined
+// copies made k_search<int64_t> 46 k SASS instructions, and 40 % of its
+// stall samples were instruction fetch (no_inst) -- and a budgeted run
+// keeps its budget (the small path overran a 0.5 s budget by 0.49 s)
+#ifndef MK_SMALL_PATH
+#define MK_SMALL_PATH 0
+#endif
+#ifndef MK_SHREG_PATH
+#define MK_SHREG_PATH 0
+#endif
+
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SMALL_V = 8;    // free symbols of a "small" problem
 constexpr int SMALL_R = 64;   // registers of a "small" problem
 constexpr int SH_R = 24;      // registers of a narrow problem evaluated from shared memory
-constexpr int SH_BYTES = 2 * SH_R * 128 * (int)sizeof(int64_t);  // per 128-thread CTA
+// per 128-thread CTA; none without the shared-register path, which leaves
+// the whole 256 KB of the SM's L1 / shared storage to the L1 (the generic
+// path's register files are local memory)
+constexpr int SH_BYTES = MK_SHREG_PATH ? 2 * SH_R * 128 * (int)sizeof(int64_t) : 0;
 constexpr int DIVE_CAP = 1024;  // boxes per speculative-dive stack
 
 // dynamic shared memory of k_search<int64_t>: lo / hi interval register files
@@ -127,20 +145,6 @@ struct LaneStats {
 __device__ __forceinline__ bool is_narrow(const mk_problem& p) {
   return (p.flags & MK_PF_NARROW) != 0;
 }
-// specialised k_search code paths for small problems (8 symbols: 64-entry
-// local register files; 24 registers: the register file in shared memory).
-// Off: one generic path per class is faster on every corpus set measured on
-// the B200 (config3 40.7 -> 36.2 ms, paged_attention_v2 long 32.2 -> 29.6,
-// moe_align 18.4 -> 17.3; profiles/r02_code_paths.jsonl) -- the three inlined
-// copies made k_search<int64_t> 46 k SASS instructions, and 40 % of its
-// stall samples were instruction fetch (no_inst) -- and a budgeted run
-// keeps its budget (the small path overran a 0.5 s budget by 0.49 s)
-#ifndef MK_SMALL_PATH
-#define MK_SMALL_PATH 0
-#endif
-#ifndef MK_SHREG_PATH
-#define MK_SHREG_PATH 0
-#endif
 __device__ __forceinline__ bool is_small(const mk_problem& p) {
   return MK_SMALL_PATH && p.nvars <= SMALL_V && p.nregs <= SMALL_R;
 }
@@ -962,6 +966,12 @@ extern "C" int mk_ctx_create(int device, mk_ctx** out) {
   {
     int sms = 0, per_wide = 0, per_narrow = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    // the search kernels keep their register files in local memory: all of
+    // the SM's unified L1 / shared storage as L1
+    cudaFuncSetAttribute(k_search<i128>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         SH_BYTES ? -1 : 0);
+    cudaFuncSetAttribute(k_search<int64_t>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         SH_BYTES ? -1 : 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_wide, k_search<i128>, SEARCH_THREADS, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_narrow, k_search<int64_t>, SEARCH_THREADS,
                                                   SH_BYTES);
