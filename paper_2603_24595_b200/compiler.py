@@ -65,6 +65,7 @@ ROW_GROUPS = os.environ.get("MK_ROW_GROUPS", "1") != "0"
 # case split of a disjunction left after presolve (_split_disjunction), switch
 OR_SPLIT = os.environ.get("MK_OR_SPLIT", "1") != "0"
 MAX_REGS = 1024
+MAX_TEMPS = 64       # temporaries of a search problem (mk_core.cuh MK_MAXT: flag bit masks)
 _AGG_WIDE = 4096
 _NEG = {"eq": "ne", "ne": "eq", "lt": "ge", "le": "gt", "gt": "le", "ge": "lt"}
 _FLIP = {"lt": "gt", "le": "ge", "gt": "lt", "ge": "le", "eq": "eq", "ne": "ne"}
@@ -1755,6 +1756,9 @@ def _emit_problem(var_names: List[str], lo: List[int], hi: List[int],
     for i, a in enumerate(atoms):
         em.atom(a, i)
     code, nregs, _ = em.finish([])
+    if nregs - len(var_names) - len(em.consts) > MAX_TEMPS:
+        raise CapacityError(f"search problem needs {nregs - len(var_names) - len(em.consts)} "
+                            f"temporaries (> {MAX_TEMPS})")
     atom_regs = [0] * len(atoms)
     masks = []
     for a in atoms:

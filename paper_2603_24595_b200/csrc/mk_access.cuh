@@ -264,7 +264,7 @@ extern "C" int mk_access_sweep(mk_ctx* ctx, const mk_access_input* in, mk_access
     if (p.nregs > maxr) maxr = p.nregs;
   }
   if (slots > 2147483647ull) return fail(ctx, MK_EINVAL, "access sweep exceeds 2^31 tuples");
-  int rc = upload_set(ctx, &set, &ctx->scratch);
+  int rc = upload_set(ctx, &set, &ctx->scratch, false);
   if (rc) return rc;
   mk_dset* ds = &ctx->scratch;
   char* base = static_cast<char*>(ds->d);

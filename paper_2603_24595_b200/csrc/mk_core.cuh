@@ -54,6 +54,7 @@ typedef unsigned __int128 u128;
 #define MK_MAXR 256   /* registers per problem evaluated by the kernels */
 #endif
 #define MK_MAXV 64    /* free symbols per problem */
+#define MK_MAXT 64    /* temporaries per problem in the search kernels (flag bit masks) */
 
 MK_HD i128 mk_ld(const mk_i128& v) {
   return (i128)(((u128)(uint64_t)v.hi << 64) | (u128)v.lo);
@@ -471,16 +472,34 @@ struct MkIvFile {
   MK_HDF void set(int r, const MkIvT<V>& x) { R[r] = x; }
 };
 
+// an interval temporary without its flags: one 16-byte (int64) load / store
+template <typename V>
+struct alignas(16) MkPair {
+  V lo, hi;
+};
+
+// temporaries only (registers nvars + nconst ...): variables are read from
+// the box, constants from the table; the temporaries' OK / ERR flags are bit
+// masks held in registers (at most MK_MAXT temporaries), so the register
+// file in local memory is {lo, hi} pairs only
 template <typename V>
 struct MkIvTemps {
   const MkProb* P;
   const V* lo;
   const V* hi;
-  MkIvT<V>* T;
+  MkPair<V>* T;
   int nv, base;
+  uint64_t ok = 0, er = 0;
   MK_HDF MkIvT<V> get(int r) const {
-    if (r >= base) return T[r - base];
     MkIvT<V> o;
+    if (r >= base) {
+      const int k = r - base;
+      const MkPair<V> t = T[k];
+      o.lo = t.lo;
+      o.hi = t.hi;
+      o.fl = (uint8_t)((((ok >> k) & 1) ? MK_FL_OK : 0) | (((er >> k) & 1) ? MK_FL_ERR : 0));
+      return o;
+    }
     o.fl = MK_FL_OK;
     if (r < nv) {
       o.lo = lo[r];
@@ -492,7 +511,16 @@ struct MkIvTemps {
     }
     return o;
   }
-  MK_HDF void set(int r, const MkIvT<V>& x) { T[r - base] = x; }
+  MK_HDF void set(int r, const MkIvT<V>& x) {
+    const int k = r - base;
+    MkPair<V> t;
+    t.lo = x.lo;
+    t.hi = x.hi;
+    T[k] = t;
+    const uint64_t bit = 1ull << k;
+    ok = (x.fl & MK_FL_OK) ? (ok | bit) : (ok & ~bit);
+    er = (x.fl & MK_FL_ERR) ? (er | bit) : (er & ~bit);
+  }
 };
 
 template <typename V, typename Regs>
@@ -568,10 +596,11 @@ MK_HD MkBoxVerdict mk_eval_box(const MkProb& P, const V* vlo, const V* vhi, MkIv
 
 // temporaries only in T (registers nvars + nconst ... nregs - 1)
 template <typename V>
-MK_HD MkBoxVerdict mk_eval_box_t(const MkProb& P, const V* vlo, const V* vhi, MkIvT<V>* T,
+MK_HD MkBoxVerdict mk_eval_box_t(const MkProb& P, const V* vlo, const V* vhi, MkPair<V>* T,
                                  int64_t* insn_count) {
   const int nv = P.p->nvars;
-  return mk_eval_box_impl<V>(P, MkIvTemps<V>{&P, vlo, vhi, T, nv, nv + P.p->nconst}, insn_count);
+  return mk_eval_box_impl<V>(P, MkIvTemps<V>{&P, vlo, vhi, T, nv, nv + P.p->nconst},
+                             insn_count);
 }
 
 // ---------------------------------------------------------------------------
@@ -727,20 +756,33 @@ struct MkCvFile {
   MK_HDF void set(int r, const MkCvT<V>& x) { R[r] = x; }
 };
 
+// temporaries only, values in T and the error flags as a bit mask in a
+// register (at most MK_MAXT temporaries)
 template <typename V>
 struct MkCvTemps {
   const MkProb* P;
   const V* x;
-  MkCvT<V>* T;
+  V* T;
   int nv, base;
+  uint64_t er = 0;
   MK_HDF MkCvT<V> get(int r) const {
-    if (r >= base) return T[r - base];
     MkCvT<V> o;
+    if (r >= base) {
+      const int k = r - base;
+      o.v = T[k];
+      o.err = (uint8_t)((er >> k) & 1);
+      return o;
+    }
     o.err = 0;
     o.v = r < nv ? x[r] : MkNum<V>::ld(P->consts[r - nv]);
     return o;
   }
-  MK_HDF void set(int r, const MkCvT<V>& v) { T[r - base] = v; }
+  MK_HDF void set(int r, const MkCvT<V>& v) {
+    const int k = r - base;
+    T[k] = v.v;
+    const uint64_t bit = 1ull << k;
+    er = v.err ? (er | bit) : (er & ~bit);
+  }
 };
 
 template <typename V, typename Regs>
@@ -830,7 +872,7 @@ MK_HD bool mk_eval_point(const MkProb& P, const V* x, MkCvT<V>* R, bool* overflo
 
 // temporaries only in T (the k_search leaf enumeration)
 template <typename V>
-MK_HD bool mk_eval_point_t(const MkProb& P, const V* x, MkCvT<V>* T, bool* overflow,
+MK_HD bool mk_eval_point_t(const MkProb& P, const V* x, V* T, bool* overflow,
                            int64_t* insn_count) {
   const int nv = P.p->nvars;
   return mk_eval_point_impl<V>(P, MkCvTemps<V>{&P, x, T, nv, nv + P.p->nconst}, overflow,

@@ -394,7 +394,7 @@ __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo,
   if constexpr (SH != 0) {
     v = sh_eval_box(P, lo, hi, mk_dyn_sh, mk_dyn_sh + SH_R * blockDim.x, &cnt);
   } else {
-    MkIvT<V> R[CAPR];   // temporaries only: variables and constants are read in place
+    MkPair<V> R[CAPR < MK_MAXT ? CAPR : MK_MAXT];   // temporaries only (flags in registers)
     v = mk_eval_box_t(P, lo, hi, R, &cnt);
   }
   st.insns_bb += (unsigned long long)cnt;
@@ -540,7 +540,7 @@ __device__ void warp_enumerate(const DevSet& D, int pid, const mk_problem& p, co
   }
   if (skip) return;
   const MkProb P = view(D, pid);
-  MkCvT<V> R[SH ? 1 : CAPR];
+  V R[SH ? 1 : (CAPR < MK_MAXT ? CAPR : MK_MAXT)];   // temporaries only (flags in a register)
   int64_t cnt = 0;
   bool ovf = false;
   unsigned long long found = ~0ull;
@@ -1025,13 +1025,17 @@ static int ensure(mk_ctx* ctx, void** buf, size_t* cap, size_t need) {
   return MK_OK;
 }
 
-static int upload_set(mk_ctx* ctx, const mk_problem_set* set, mk_dset* ds) {
+// search = false: a race / access program (its evaluators keep the whole
+// register file, no temporaries limit)
+static int upload_set(mk_ctx* ctx, const mk_problem_set* set, mk_dset* ds, bool search = true) {
   const int nprob = set->nprob;
   int S = 1;
   for (int i = 0; i < nprob; ++i) {
     const mk_problem& p = set->probs[i];
-    if (p.nvars > MK_MAXV || p.nregs > MK_MAXR)
-      return fail(ctx, MK_EINVAL, "problem exceeds MK_MAXV symbols or MK_MAXR registers");
+    if (p.nvars > MK_MAXV || p.nregs > MK_MAXR ||
+        (search && p.nregs - p.nvars - p.nconst > MK_MAXT))
+      return fail(ctx, MK_EINVAL,
+                  "problem exceeds MK_MAXV symbols, MK_MAXR registers or MK_MAXT temporaries");
     if (p.nvars > S) S = p.nvars;
   }
   size_t off = 0;

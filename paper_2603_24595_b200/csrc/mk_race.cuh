@@ -607,7 +607,7 @@ extern "C" int mk_race_sweep(mk_ctx* ctx, const mk_race_prog* prog, mk_race_resu
   }
   if (volf > 2147483647.0L) return fail(ctx, MK_EINVAL, "race sweep box exceeds 2^31 instances");
   if (volf * innerf > 9.0e18L) return fail(ctx, MK_EINVAL, "race sweep box exceeds 2^63 points");
-  int rc = upload_set(ctx, &set, &ctx->scratch);
+  int rc = upload_set(ctx, &set, &ctx->scratch, false);
   if (rc) return rc;
   mk_dset* ds = &ctx->scratch;
   char* base = static_cast<char*>(ds->d);

@@ -53,8 +53,8 @@ void solve_problem(const mk_problem_set* set, int pid, int K, long long leaf_vol
   const mk_problem& p = set->probs[pid];
   MkProb P = mk_prob_view(set->probs, pid, set->insns, set->consts, set->atom_regs,
                           set->atom_masks, set->rows, set->row_terms);
-  std::vector<MkIvT<V>> R(MK_MAXR);
-  std::vector<MkCvT<V>> C(MK_MAXR);
+  std::vector<MkPair<V>> R(MK_MAXT);
+  std::vector<V> C(MK_MAXT);
   const int nv = p.nvars;
   std::vector<EBox<V>> stack;
   EBox<V> root;
