@@ -38,7 +38,6 @@ from __future__ import annotations
 import math
 import os
 from dataclasses import dataclass, field
-from fractions import Fraction
 from typing import Callable, Dict, List, Optional, Sequence, Set, Tuple
 
 from . import ir, refmirror
@@ -882,7 +881,7 @@ class _Presolve:
                     elif c > 0:
                         self._set_bound(k, None, (-const) // c)
                     else:
-                        self._set_bound(k, math.ceil(Fraction(-const, c)), None)
+                        self._set_bound(k, -(const // c), None)
                     changed = True
                     if self.unsat:
                         return False
@@ -1233,14 +1232,14 @@ class _Presolve:
                 ub = (-c) // f
                 ent[1] = ub if ent[1] is None else min(ent[1], ub)
             else:
-                lb = math.ceil(Fraction(-c, f))
+                lb = -(c // f)
                 ent[0] = lb if ent[0] is None else max(ent[0], lb)
             if a[1] == "eq":
                 if f > 0:
-                    lb = math.ceil(Fraction(-c, f))
+                    lb = -(c // f)
                     ent[0] = lb if ent[0] is None else max(ent[0], lb)
                 else:
-                    ub = math.floor(Fraction(-c, f))
+                    ub = (-c) // f
                     ent[1] = ub if ent[1] is None else min(ent[1], ub)
         return out
 
@@ -1507,34 +1506,48 @@ class _Presolve:
                     continue
                 terms, c = lf
                 parts = []
+                # activity range of the row: finite sums plus the number of
+                # unbounded contributions, so each term's residual range is
+                # the total less its own contribution (linear in the terms)
+                smin = smax = c
+                nmin = nmax = 0
                 for k, v in terms.items():
                     lo, hi = self.bounds.get(k, (None, None)) if isinstance(k, str) else ivl(k)
-                    parts.append((k, v, lo, hi))
-                for j, (k, v, _, _) in enumerate(parts):
+                    mn, mx = (lo, hi) if v > 0 else (hi, lo)
+                    mn = None if mn is None else v * mn
+                    mx = None if mx is None else v * mx
+                    if mn is None:
+                        nmin += 1
+                    else:
+                        smin += mn
+                    if mx is None:
+                        nmax += 1
+                    else:
+                        smax += mx
+                    parts.append((k, v, mn, mx))
+                for k, v, mn, mx in parts:
                     if not isinstance(k, str):
                         continue
-                    rlo, rhi = c, c
-                    for i, (k2, v2, lo, hi) in enumerate(parts):
-                        if i == j:
-                            continue
-                        if v2 > 0:
-                            rlo = None if rlo is None or lo is None else rlo + v2 * lo
-                            rhi = None if rhi is None or hi is None else rhi + v2 * hi
-                        else:
-                            rlo = None if rlo is None or hi is None else rlo + v2 * hi
-                            rhi = None if rhi is None or lo is None else rhi + v2 * lo
+                    if mn is None:
+                        rlo = smin if nmin == 1 else None
+                    else:
+                        rlo = smin - mn if nmin == 0 else None
+                    if mx is None:
+                        rhi = smax if nmax == 1 else None
+                    else:
+                        rhi = smax - mx if nmax == 0 else None
                     # v*x + rest <= 0  (and >= 0 for eq)
                     nlo = nhi = None
                     if rlo is not None:
                         if v > 0:
                             nhi = (-rlo) // v
                         else:
-                            nlo = math.ceil(Fraction(-rlo, v))
+                            nlo = -(rlo // v)            # ceil(-rlo / v)
                     if a[1] == "eq" and rhi is not None:
                         if v > 0:
-                            nlo = math.ceil(Fraction(-rhi, v))
+                            nlo = -(rhi // v)            # ceil(-rhi / v)
                         else:
-                            nhi = math.floor(Fraction(-rhi, v))
+                            nhi = (-rhi) // v            # floor(-rhi / v)
                     if self._set_bound(k, nlo, nhi):
                         changed = True
                         if self.unsat:
