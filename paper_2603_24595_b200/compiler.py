@@ -1418,15 +1418,19 @@ class _Presolve:
         """f <= u and -f <= -l over the same symbols with l > u: no model
         (two rows of one linear form -- a relaxation cut against a
         Fourier-Motzkin row, say -- that bound propagation would only creep
-        towards one unit per sweep)."""
+        towards one unit per sweep).  Opaque terms (a product of symbols,
+        say) count as one more coordinate: a term is a function of the
+        symbols, so at any model both rows hold with the same value of it
+        (a point where it raises is no model)."""
         upper: Dict[Tuple, int] = {}
         for a in self.atoms:
             if a[0] != "p" or a[1] != "le":
                 continue
             lf = self._lin_of_atom(lin, a)
-            if lf is None or not lf[0] or not all(isinstance(k, str) for k in lf[0]):
+            if lf is None or not lf[0]:
                 continue
-            key = tuple(sorted(lf[0].items()))
+            key = tuple(sorted(((k if isinstance(k, str) else ir.render(k)), v)
+                               for k, v in lf[0].items()))
             u = -lf[1]                       # sum(terms) <= -c
             if key not in upper or u < upper[key]:
                 upper[key] = u
@@ -1465,6 +1469,11 @@ class _Presolve:
         # only wide symbols are eliminated: narrow ones are cheap to enumerate
         symbols = sorted({k for t, _ in rows for k in t if isinstance(k, str) and wide(k)},
                          key=lambda n: self.pos.get(n, 0))
+        # opaque terms (products of symbols, quotients) are eliminated too,
+        # after the symbols: a term is one value at any model, so rows that
+        # bound it from both sides imply their combination without it
+        symbols += sorted({k for t, _ in rows for k in t if not isinstance(k, str)},
+                          key=ir.render)
         if len(self.cuts) >= 48:
             return False
         for v in symbols:
