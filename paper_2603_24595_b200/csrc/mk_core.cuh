@@ -144,15 +144,6 @@ MK_HD V mk_min(V a, V b) { return a < b ? a : b; }
 template <typename V>
 MK_HD V mk_max(V a, V b) { return a > b ? a : b; }
 
-// truncating division; b != 0.  infinite numerator stays infinite, an infinite
-// divisor drives a finite numerator to 0 (the limit; sound at interval corners)
-template <typename V>
-MK_HD V mk_tdiv(V a, V b) {
-  typedef MkNum<V> N;
-  if (N::isinf(a)) return ((a < 0) != (b < 0)) ? -N::inf() : N::inf();
-  if (N::isinf(b)) return 0;
-  return a / b;
-}
 // truncating quotient, one division: a 32-bit division when both operands
 // fit (the common case for the contraction rows' bounds and coefficients;
 // a 64-bit division is a ~70-instruction sequence on the GPU)
@@ -161,6 +152,16 @@ MK_HD int64_t mk_tquot(int64_t a, int64_t b) {
   if (a == (int64_t)(int32_t)a && b == (int64_t)(int32_t)b && !(a == INT32_MIN && b == -1))
     return (int64_t)((int32_t)a / (int32_t)b);
   return a / b;
+}
+
+// truncating division; b != 0.  infinite numerator stays infinite, an infinite
+// divisor drives a finite numerator to 0 (the limit; sound at interval corners)
+template <typename V>
+MK_HD V mk_tdiv(V a, V b) {
+  typedef MkNum<V> N;
+  if (N::isinf(a)) return ((a < 0) != (b < 0)) ? -N::inf() : N::inf();
+  if (N::isinf(b)) return 0;
+  return mk_tquot(a, b);
 }
 template <typename V>
 MK_HD V mk_floordiv(V a, V b) {
@@ -177,7 +178,7 @@ MK_HD V mk_ceildiv(V a, V b) {
 template <typename V>
 MK_HD V mk_emod_c(V a, V b) {  // exact, b != 0, finite
   V m = b < 0 ? -b : b;
-  V r = a % m;
+  V r = a - mk_tquot(a, m) * m;
   if (r < 0) r += m;
   return r;
 }
@@ -839,10 +840,10 @@ MK_HD bool mk_eval_point_impl(const MkProb& P, Regs R, bool* overflow, int64_t* 
             case MK_OP_SHL: r.v = N::shl(a.v, (int)b.v); break;
             case MK_OP_SHR: r.v = N::shr(a.v, (int)b.v); break;
             case MK_OP_DIV:
-              if (b.v == 0) r.err = 1; else r.v = a.v / b.v;
+              if (b.v == 0) r.err = 1; else r.v = mk_tquot(a.v, b.v);
               break;
             case MK_OP_MOD:
-              if (b.v == 0) r.err = 1; else r.v = a.v % b.v;
+              if (b.v == 0) r.err = 1; else r.v = a.v - mk_tquot(a.v, b.v) * b.v;
               break;
             case MK_OP_EMOD:
               if (b.v == 0) r.err = 1; else r.v = mk_emod_c(a.v, b.v);
