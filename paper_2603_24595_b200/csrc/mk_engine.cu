@@ -632,6 +632,7 @@ struct SearchArgs {
   int dive;          // incumbent dive: no spills, dumps or pending marks
   const int* stop;   // dive: the main search has finished (polled per step)
   int adapt_k;       // widen the splits of a shallow stack (MK_ADAPT_K)
+  int group;         // tasks taken per grab; a run of one problem's tasks shares a stack
 };
 
 // TASK_DUMPED: redistribution (every task has been handed out), the unit
@@ -666,12 +667,12 @@ __device__ bool dump_stack(const SearchArgs& A, const DevSet& D, char* stack, lo
 template <typename V, int CAPV, int CAPR, int SH = 0>
 __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const mk_problem& p,
                            char* stack, char* leaves, unsigned long long t_start,
-                           LaneStats& st) {
+                           LaneStats& st, long long top0 = 1) {
   const int lane = threadIdx.x & 31;
   const int nv = p.nvars;
   const int K = A.K;
   const unsigned long long deadline_ns = t_start + A.budget_ns;
-  long long top = 1;
+  long long top = top0;
   int steps = 0;
   while (top > 0) {
     long long room = A.cap - top;
@@ -803,40 +804,70 @@ __global__ void __launch_bounds__(SEARCH_THREADS, MinBlocks<V>::value)
   const size_t words = A.box_bytes / sizeof(int4);
   LaneStats st;
   st.zero();
+  const int G = A.group > 1 ? A.group : 1;
   for (;;) {
     int task = 0;
-    if (lane == 0) task = atomicAdd(A.ctl, 1);
+    if (lane == 0) task = atomicAdd(A.ctl, G);
     task = __shfl_sync(FULL, task, 0);
     if (task >= A.ntasks) {
       if (lane == 0) atomicAdd(A.ctl + 1, 1);  // idle from now on
       break;
     }
-    // tasks are taken best-first: the top of the task stack
-    const Box* tb = box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - 1 - task));
-    {
-      const int4* src = reinterpret_cast<const int4*>(tb);
-      int4* dst = reinterpret_cast<int4*>(stack);
-      for (size_t w = lane; w < words; w += 32) dst[w] = src[w];
+    const int tend = task + G < A.ntasks ? task + G : A.ntasks;
+    bool dumped = false;
+    // tasks are taken best-first (the top of the task stack); a run of
+    // consecutive tasks of one problem is searched as one stack -- task box
+    // ntasks-1-t for task t, so the run's boxes are contiguous, worst first,
+    // exactly the stack order -- which fills the warp's lanes from the
+    // first step instead of one root box per unit
+    for (int t = task; t < tend;) {
+      const Box* tb = box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - 1 - t));
+      const int pid = tb->prob;
+      int len = 1;
+      while (t + len < tend &&
+             box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - 1 - t - len))->prob == pid)
+        ++len;
+      if (dumped) {
+        // this unit's launch ended: the rest of its grab goes to the dump
+        if (pid >= 0) {
+          const int4* src = reinterpret_cast<const int4*>(
+              box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - t - len)));
+          int4* dst = reinterpret_cast<int4*>(stack);
+          for (size_t w = lane; w < words * (size_t)len; w += 32) dst[w] = src[w];
+          __syncwarp();
+          if (!dump_stack(A, D, stack, len) && lane == 0) atomicExch(&D.inc[pid].err, 1);
+          __syncwarp();
+        }
+        t += len;
+        continue;
+      }
+      {
+        const int4* src = reinterpret_cast<const int4*>(
+            box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - t - len)));
+        int4* dst = reinterpret_cast<int4*>(stack);
+        for (size_t w = lane; w < words * (size_t)len; w += 32) dst[w] = src[w];
+      }
+      __syncwarp();
+      t += len;
+      if (pid < 0) continue;  // holes left by a dump that did not fit
+      const mk_problem p = D.probs[pid];
+      if (globaltimer_ns() > t_start + A.budget_ns) {
+        if (lane == 0 && !A.dive) A.pending[pid] = 1;
+        continue;
+      }
+      int r;
+      if constexpr (!MkNum<V>::kWide) {
+        if (is_shreg(p)) r = search_task<V, SMALL_V, SH_R, 1>(A, D, pid, p, stack, leaves, t_start, st, len);
+        else if (is_small(p)) r = search_task<V, SMALL_V, SMALL_R>(A, D, pid, p, stack, leaves, t_start, st, len);
+        else r = search_task<V, MK_MAXV, MK_MAXR>(A, D, pid, p, stack, leaves, t_start, st, len);
+      } else {
+        if (is_small(p)) r = search_task<V, SMALL_V, SMALL_R>(A, D, pid, p, stack, leaves, t_start, st, len);
+        else r = search_task<V, MK_MAXV, MK_MAXR>(A, D, pid, p, stack, leaves, t_start, st, len);
+      }
+      if (r == TASK_ABORT && lane == 0 && !A.dive) A.pending[pid] = 1;
+      if (r == TASK_DUMPED) dumped = true;  // the launch ends for the unit; the host redistributes
     }
-    __syncwarp();
-    const int pid = tb->prob;
-    if (pid < 0) continue;  // hole left by a dump that did not fit
-    const mk_problem p = D.probs[pid];
-    if (globaltimer_ns() > t_start + A.budget_ns) {
-      if (lane == 0 && !A.dive) A.pending[pid] = 1;
-      continue;
-    }
-    int r;
-    if constexpr (!MkNum<V>::kWide) {
-      if (is_shreg(p)) r = search_task<V, SMALL_V, SH_R, 1>(A, D, pid, p, stack, leaves, t_start, st);
-      else if (is_small(p)) r = search_task<V, SMALL_V, SMALL_R>(A, D, pid, p, stack, leaves, t_start, st);
-      else r = search_task<V, MK_MAXV, MK_MAXR>(A, D, pid, p, stack, leaves, t_start, st);
-    } else {
-      if (is_small(p)) r = search_task<V, SMALL_V, SMALL_R>(A, D, pid, p, stack, leaves, t_start, st);
-      else r = search_task<V, MK_MAXV, MK_MAXR>(A, D, pid, p, stack, leaves, t_start, st);
-    }
-    if (r == TASK_ABORT && lane == 0 && !A.dive) A.pending[pid] = 1;
-    if (r == TASK_DUMPED) break;  // this launch ends for the unit; the host redistributes
+    if (dumped) break;
   }
   st.flush_warp(A.st);
 }
@@ -1113,6 +1144,9 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   // racy 8.7 -> 4.6 ms, the rest within noise; profiles/r02_adapt_k.jsonl)
   int adapt_k = 1;
   if (const char* e = getenv("MK_ADAPT_K")) adapt_k = atoi(e);
+  // most tasks a unit grabs at once (k_search; 1 = one root per grab)
+  long long group_cap = 16;   // measured: profiles/r02_task_group.jsonl
+  if (const char* e = getenv("MK_TASK_GROUP")) group_cap = atoi(e) > 0 ? atoi(e) : 1;
   if (lim && lim->split_k > 1) K = lim->split_k;
   int chunk = lim && lim->chunk > 0 ? lim->chunk : 65536;
   long long leaf_volume = lim && lim->leaf_volume > 0 ? lim->leaf_volume : 4096;
@@ -1339,6 +1373,13 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
       int grid = ctx->ctas[c] - dive_ctas[c];
       if (grid < ctx->sms) grid = ctx->sms;
       A.units = grid * WARPS_PER_CTA;
+      // tasks per grab: with many more tasks than units, a unit takes a few
+      // at once (runs of one problem share its stack); never in a dive
+      {
+        long long g = dive ? 1 : A.ntasks / (2LL * A.units);
+        if (g > group_cap) g = group_cap;
+        A.group = g < 1 ? 1 : (int)g;
+      }
       if (c == 0) k_search<i128><<<grid, SEARCH_THREADS, 0, cs>>>(D, A);
       else k_search<int64_t><<<grid, SEARCH_THREADS, SH_BYTES, cs>>>(D, A);
       ++launches;
@@ -1397,6 +1438,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
         ++launches;
         SearchArgs A;
         A.adapt_k = 0;   // a dive pops one box per step by design
+        A.group = 1;
         A.tasks = dst[c];
         A.ntasks = (int)nt[c];
         A.ctl = dctl;

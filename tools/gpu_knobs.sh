@@ -1,6 +1,7 @@
 # GPU box: resident full-presolve step device time per search knob setting
-# (MK_SPLIT_K split arity, MK_ADAPT_K shallow-stack widening), read by the
-# engine at every call
+# (MK_SPLIT_K split arity, MK_ADAPT_K shallow-stack widening, MK_TASK_GROUP
+# tasks per grab), read by the engine at every call.  KNOBS="NAME=v1,v2 ..."
+# picks the settings swept (default: split arity x widening)
 mkdir -p gpurun_out
 python - > gpurun_out/knobs.jsonl 2>&1 <<'PY'
 import json, os, sys
@@ -12,13 +13,15 @@ sets = {}
 for g in ["config3", "moe_align", "paged_attention_v2_long_b16", "paged_attention_v1", "racy"]:
     packed, _ = chk.pack([c for c, _ in compile_all(load_sites(entries(g))[1]) if c is not None])
     sets[g] = chk.engine.upload(packed)
-for k in ["6", "8", "12", "16"]:
-    for ad in ["0", "1"]:
-        os.environ["MK_SPLIT_K"] = k
-        os.environ["MK_ADAPT_K"] = ad
-        for g, rs in sets.items():
-            runs = [rs.run({"max_seconds": 600.0}) for _ in range(5)]
-            print(json.dumps({"K": k, "adapt": ad, "group": g,
-                              "ms": sorted(round(r["device_ms"], 2) for r in runs),
-                              "boxes": runs[-1]["boxes"], "steps": runs[-1]["steps"]}), flush=True)
+import itertools
+spec = os.environ.get("KNOBS", "MK_SPLIT_K=6,8,12,16 MK_ADAPT_K=0,1").split()
+names = [x.split("=")[0] for x in spec]
+for vals in itertools.product(*[x.split("=")[1].split(",") for x in spec]):
+    for n, v in zip(names, vals):
+        os.environ[n] = v
+    for g, rs in sets.items():
+        runs = [rs.run({"max_seconds": 600.0}) for _ in range(5)]
+        print(json.dumps({**dict(zip(names, vals)), "group": g,
+                          "ms": sorted(round(r["device_ms"], 2) for r in runs),
+                          "boxes": runs[-1]["boxes"], "steps": runs[-1]["steps"]}), flush=True)
 PY
