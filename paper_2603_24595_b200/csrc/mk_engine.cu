@@ -460,6 +460,12 @@ __device__ __forceinline__ void load_box(const Box* in, int nv, int stride, V* l
   }
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---------------------------------------------------------------------------
 // pre-split round kernel: one thread per box
 
@@ -579,12 +585,21 @@ __device__ void leaf_block(const DevSet& D, const Box* in, LaneStats& st) {
 }
 
 // pre-split leaves: one warp per leaf box
+// a leaf is enumerated only inside the run's wall budget (device stamp +
+// budget); one left over marks its problem undecided
 __global__ void __launch_bounds__(128) k_leaf(DevSet D, const void* leaves, int nleaf,
-                                              DevStats* dst) {
+                                              DevStats* dst, const unsigned long long* stamp,
+                                              unsigned long long budget_ns, int* pending) {
   const int w = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   LaneStats st;
   st.zero();
-  if (w < nleaf) {
+  bool late = false;
+  if (w < nleaf && (threadIdx.x & 31) == 0) late = globaltimer_ns() > *stamp + budget_ns;
+  late = __shfl_sync(FULL, late, 0);
+  if (w < nleaf && late) {
+    if ((threadIdx.x & 31) == 0)
+      pending[box_at(const_cast<void*>(leaves), D.box_bytes, w)->prob] = 1;
+  } else if (w < nleaf) {
     const Box* in = box_at(const_cast<void*>(leaves), D.box_bytes, w);
     const mk_problem p = D.probs[in->prob];
     if (is_narrow(p)) {
@@ -597,11 +612,6 @@ __global__ void __launch_bounds__(128) k_leaf(DevSet D, const void* leaves, int 
   st.flush_warp(dst);
 }
 
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 __global__ void k_stamp(unsigned long long* out) { *out = globaltimer_ns(); }
 
@@ -644,6 +654,23 @@ enum { TASK_DONE = 0, TASK_ABORT = 1, TASK_DUMPED = 2 };
 // CAS retry storm when every unit dumps at once); a reservation that runs past
 // the buffer end marks its in-range slots empty (prob = -1) so the next
 // launch skips them, and the host clamps the count to the capacity.
+// warp-wide copy of n int4 words with 4 loads in flight per lane (stack
+// spills and dumps move megabytes; one dependent load per iteration made a
+// spill a multi-millisecond step)
+__device__ __forceinline__ void warp_copy16(int4* __restrict__ dst, const int4* __restrict__ src,
+                                            size_t n) {
+  const int lane = threadIdx.x & 31;
+  size_t w = lane;
+  for (; w + 96 < n; w += 128) {
+    const int4 a = src[w], b = src[w + 32], c = src[w + 64], d = src[w + 96];
+    dst[w] = a;
+    dst[w + 32] = b;
+    dst[w + 64] = c;
+    dst[w + 96] = d;
+  }
+  for (; w < n; w += 32) dst[w] = src[w];
+}
+
 __device__ bool dump_stack(const SearchArgs& A, const DevSet& D, char* stack, long long top) {
   const int lane = threadIdx.x & 31;
   unsigned long long off = 0;
@@ -659,8 +686,7 @@ __device__ bool dump_stack(const SearchArgs& A, const DevSet& D, char* stack, lo
   const size_t words = A.box_bytes / sizeof(int4);
   const int4* src = reinterpret_cast<const int4*>(stack);
   int4* dst = reinterpret_cast<int4*>(static_cast<char*>(A.dump) + (size_t)off * A.box_bytes);
-  const size_t total = (size_t)top * words;
-  for (size_t w = lane; w < total; w += 32) dst[w] = src[w];
+  warp_copy16(dst, src, (size_t)top * words);
   return true;
 }
 
@@ -682,6 +708,12 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
     if (fit < n) n = fit;
     if (n < 1 && A.dive) return TASK_DONE;
     if (n < 1) {
+      // past the deadline a full stack is not spilled: the task is undecided
+      {
+        int lt = 0;
+        if (lane == 0) lt = globaltimer_ns() > deadline_ns;
+        if (__shfl_sync(FULL, lt, 0)) return TASK_ABORT;
+      }
       // stack full: the bottom (worst) half goes to the next launch's task
       // list, the unit keeps searching its best half
       const long long spill = top - top / 2;
@@ -692,8 +724,8 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
       const size_t words = A.box_bytes / sizeof(int4);
       const int4* src = reinterpret_cast<const int4*>(stack + (size_t)spill * A.box_bytes);
       int4* dst = reinterpret_cast<int4*>(stack);
-      const size_t total = (size_t)(top - spill) * words;  // <= spill * words: no overlap
-      for (size_t w = lane; w < total; w += 32) dst[w] = src[w];
+      // (top - spill) <= spill boxes: source and destination do not overlap
+      warp_copy16(dst, src, (size_t)(top - spill) * words);
       __syncwarp();
       top -= spill;
       continue;
@@ -758,8 +790,19 @@ __device__ int search_task(const SearchArgs& A, const DevSet& D, int pid, const 
     __syncwarp();
     top = base + ctot;
     const int nleaf = __popc(leafmask);
-    for (int l = 0; l < nleaf; ++l)
+    bool late = false;
+    for (int l = 0; l < nleaf; ++l) {
+      // past the deadline the remaining leaves are not enumerated (the
+      // problem is undecided): one step never runs long over the budget
+      int lt = 0;
+      if (lane == 0 && l > 0) lt = globaltimer_ns() > deadline_ns;
+      if (__shfl_sync(FULL, lt, 0)) {
+        late = true;
+        break;
+      }
       warp_enumerate<V, V, CAPV, CAPR, SH>(D, pid, p, box_at(leaves, A.box_bytes, l), st);
+    }
+    if (late) return TASK_ABORT;
     int ctlw = 0;
     if (lane == 0) {
       unsigned long long now = globaltimer_ns();
@@ -832,8 +875,7 @@ __global__ void __launch_bounds__(SEARCH_THREADS, MinBlocks<V>::value)
         if (pid >= 0) {
           const int4* src = reinterpret_cast<const int4*>(
               box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - t - len)));
-          int4* dst = reinterpret_cast<int4*>(stack);
-          for (size_t w = lane; w < words * (size_t)len; w += 32) dst[w] = src[w];
+          warp_copy16(reinterpret_cast<int4*>(stack), src, words * (size_t)len);
           __syncwarp();
           if (!dump_stack(A, D, stack, len) && lane == 0) atomicExch(&D.inc[pid].err, 1);
           __syncwarp();
@@ -841,20 +883,18 @@ __global__ void __launch_bounds__(SEARCH_THREADS, MinBlocks<V>::value)
         t += len;
         continue;
       }
-      {
-        const int4* src = reinterpret_cast<const int4*>(
-            box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - t - len)));
-        int4* dst = reinterpret_cast<int4*>(stack);
-        for (size_t w = lane; w < words * (size_t)len; w += 32) dst[w] = src[w];
-      }
-      __syncwarp();
+      const size_t first = (size_t)(A.ntasks - t - len);
       t += len;
       if (pid < 0) continue;  // holes left by a dump that did not fit
-      const mk_problem p = D.probs[pid];
       if (globaltimer_ns() > t_start + A.budget_ns) {
         if (lane == 0 && !A.dive) A.pending[pid] = 1;
         continue;
       }
+      warp_copy16(reinterpret_cast<int4*>(stack),
+                  reinterpret_cast<const int4*>(box_at(const_cast<void*>(A.tasks), A.box_bytes, first)),
+                  words * (size_t)len);
+      __syncwarp();
+      const mk_problem p = D.probs[pid];
       int r;
       if constexpr (!MkNum<V>::kWide) {
         if (is_shreg(p)) r = search_task<V, SMALL_V, SH_R, 1>(A, D, pid, p, stack, leaves, t_start, st, len);
@@ -1246,6 +1286,10 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   char* leaves = wb + w_leaves;
   void* cub_tmp = wb + w_cub;
   int* d_stop = reinterpret_cast<int*>(wb + w_stop);
+  // device stamp of the run's start (the pre-split leaves' wall budget)
+  unsigned long long* run_stamp = reinterpret_cast<unsigned long long*>(d_stop + 2);
+  k_stamp<<<1, 1, 0, s>>>(run_stamp);
+  ++launches;
   ClassRun cls[2];
   for (int c = 0; c < 2; ++c) {
     cls[c].tasks = wb + w_cls[c][0];
@@ -1534,7 +1578,8 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     bb_ms += ms;
     if (nleaf > 0) {
       CK(cudaEventRecord(ctx->ev[2], s));
-      k_leaf<<<(unsigned)((nleaf + 3) / 4), 128, 0, s>>>(D, leaves, (int)nleaf, d_st);
+      k_leaf<<<(unsigned)((nleaf + 3) / 4), 128, 0, s>>>(
+          D, leaves, (int)nleaf, d_st, run_stamp, (unsigned long long)(max_seconds * 1e9), d_pend);
       ++launches;
       CK(cudaGetLastError());
       CK(cudaEventRecord(ctx->ev[3], s));
@@ -1572,6 +1617,13 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     if (cls[0].ntasks < 0) budget_hit = true;
     else top = 0;
   }
+  const bool trace = getenv("MK_TRACE_RUN") != nullptr;
+  auto tr_el = [&]() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3;
+  };
+  if (trace)
+    fprintf(stderr, "[mk] presplit done %.2f ms rounds %lld tasks %lld/%lld\n", tr_el(),
+            (long long)rounds, cls[0].ntasks, cls[1].ntasks);
   CK(cudaEventRecord(ctx->ev[5], s));
   for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(ctx->side[c], ctx->ev[5], 0));
   while (!budget_hit && (cls[0].ntasks > 0 || cls[1].ntasks > 0)) {
@@ -1586,10 +1638,17 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     if (rc) return rc;
     search_ms += ms;
     ++search_launches;
+    if (trace)
+      fprintf(stderr, "[mk] search launch %d: %.2f ms (left %.2f ms) -> %.2f ms, next tasks %lld/%lld\n",
+              search_launches, ms, left * 1e3, tr_el(), cls[0].ntasks, cls[1].ntasks);
   }
   if (diving) {
     CK(cudaMemsetAsync(d_stop, 1, sizeof(int), s));
     for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(s, ctx->ev[8 + c], 0));
+    if (trace) {
+      CK(cudaStreamSynchronize(s));
+      fprintf(stderr, "[mk] dives joined %.2f ms\n", tr_el());
+    }
   }
   for (int c = 0; c < 2; ++c) {
     if (budget_hit && cls[c].ntasks > 0) {
