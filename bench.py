@@ -834,6 +834,11 @@ def run_b200(args):
                                         "frac": sass / int_peak if sass else None,
                                         "per_unit": per_unit,
                                         "source": f"profiles/ncu_{args.workload}_summary.json",
+                                        "calibrated_on": "the workload's full-presolve problem "
+                                                         "set, resident, deterministic limits "
+                                                         "(tools/profile_step.py): the budgeted "
+                                                         "first tier depends on wall time, which "
+                                                         "ncu's replay dilates",
                                         "ncu_issue_active_pct":
                                             cal.get("k_search_issue_active_pct")}},
             "cpu_baseline": side.pop("cpu_baseline", None),
