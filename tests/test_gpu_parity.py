@@ -66,3 +66,49 @@ def test_tiny_stacks_spill_without_loss(checker):
     ref = eng.solve(probs, {"max_seconds": 600.0})
     tiny = eng.solve(probs, {"max_seconds": 600.0, "unit_stack": 600})
     assert tiny == ref
+
+
+def test_budget_holds_on_a_hard_set(checker):
+    """A wall budget bounds the whole call: config3's light problems (many
+    of them undecidable in that time) searched with 20 and 50 ms budgets end
+    within a few milliseconds of them -- no spill, leaf enumeration or task
+    sweep runs on past the deadline -- and every problem the budget cut is
+    reported undecided, never decided wrongly."""
+    import sys
+    import os
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import entries, load_sites
+    from paper_2603_24595_b200.engine import compile_all
+
+    qs = load_sites(entries("config3"))[1]
+    light = [c for c, _ in compile_all(qs, light=True) if c is not None]
+    packed, _ = checker.pack(light)
+    rs = checker.engine.upload(packed)
+    try:
+        rs.run({"max_seconds": 0.02})                      # warm
+        for budget in (0.02, 0.05):
+            st = rs.run({"max_seconds": budget})
+            assert st["seconds"] < budget + 0.008, (budget, st["seconds"])
+    finally:
+        rs.free()
+
+
+def test_task_grouping_is_exact(checker):
+    """One task per grab and the default grouped grabs (runs of one
+    problem's tasks share a unit's stack) give identical verdicts and
+    optima."""
+    import os
+
+    from paper_2603_24595_b200.engine import compile_all
+
+    doc = load("paged_attention_v2_long_b16")
+    probs = [p for c, _ in compile_all(queries(doc)) if c for p in c.problems]
+    eng = checker.engine
+    ref = eng.solve(probs, {"max_seconds": 600.0})
+    os.environ["MK_TASK_GROUP"] = "1"
+    try:
+        one = eng.solve(probs, {"max_seconds": 600.0})
+    finally:
+        del os.environ["MK_TASK_GROUP"]
+    assert one == ref
