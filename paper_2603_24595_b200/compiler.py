@@ -819,9 +819,18 @@ class _Presolve:
         """Replace every symbol of ``m`` at once; the replacements must not
         mention each other's symbols (constants, say)."""
         memo: Dict[Node, Node] = {}
-        self.atoms = [ir.substitute(a, m, memo) for a in self.atoms]
+        # only nodes that mention a replaced symbol are rewritten (symbol
+        # sets are memoised per node for the query, so unchanged atoms cost
+        # one lookup per pass)
+        def sub(e: Node) -> Node:
+            syms = ir.symbols_of(e)
+            if not any(n in syms for n in m):
+                return e
+            return ir.substitute(e, m, memo)
+
+        self.atoms = [sub(a) for a in self.atoms]
         for k in list(self.defs):
-            self.defs[k] = ir.substitute(self.defs[k], m, memo)
+            self.defs[k] = sub(self.defs[k])
         self.defs.update(m)
 
     def _eliminate(self, name: str, e: Node) -> None:
