@@ -8,12 +8,12 @@ from bench import entries, load_sites
 from paper_2603_24595_b200.engine import SiteChecker, BatchStats
 qs = load_sites(entries("config3"))[1]
 chk = SiteChecker(device=0)
-for t1 in [(0.001, 0.002, 0.02), (0.0002, 0.001, 0.005)]:
+for t1 in [(0.001, 0.002, 0.02), (0.0005, 0.002, 0.01), (0.0002, 0.001, 0.005)]:
     chk.TIER1_S = t1
     for _ in range(2):
         chk.check_queries(qs)
     walls = []
-    for _ in range(4):
+    for _ in range(6):
         chk.stats = BatchStats()
         t = time.perf_counter()
         res = chk.check_queries(qs)
