@@ -690,6 +690,8 @@ class _Presolve:
         # (the atom list keeps its objects across passes; hashing the nested
         # tuples for every memo lookup dominated the pass)
         self._norm_by_id: Dict[int, Tuple[Node, Node]] = {}
+        # atom -> (normalised form key, factor), constant (or None): _form_bounds
+        self._form_memo: Dict[Node, Tuple] = {}
         self.cuts: Set[Node] = set()
         self._lin_memo = _Lin(self.widths)
 
@@ -711,6 +713,7 @@ class _Presolve:
         q.agg_done = set(self.agg_done)
         q._canon_memo = {}
         q._norm_by_id = {}
+        q._form_memo = {}
         q.cuts = set()         # a fresh cut budget for the branch's own rows
         q._lin_memo = _Lin(q.widths)
         return q
@@ -1227,14 +1230,18 @@ class _Presolve:
         """Bounds that single rows state on a normalised linear form
         (gcd-reduced, first coefficient positive)."""
         out: Dict[Tuple, List] = {}
+        memo = self._form_memo
         for a in self.atoms:
             if a[0] != "p" or a[1] not in ("le", "eq"):
                 continue
-            lf = self._lin_of_atom(lin, a)
-            if lf is None or not lf[0]:
+            got = memo.get(a)
+            if got is None:
+                lf = self._lin_of_atom(lin, a)
+                got = memo[a] = (None,) if lf is None or not lf[0] else \
+                    (_form_key(lf[0]), lf[1])
+            if got[0] is None:
                 continue
-            key, f = _form_key(lf[0])
-            c = lf[1]
+            (key, f), c = got
             ent = out.setdefault(key, [None, None])
             # f*F0 + c <= 0
             if f > 0:
@@ -1515,14 +1522,17 @@ class _Presolve:
 
     def _fbbt(self, lin: _Lin, rounds: int = 8) -> bool:
         any_change = False
+        # the rows do not change inside the sweeps, only the bounds do
+        rows = []
+        for a in self.atoms:
+            lf = self._lin_of_atom(lin, a)
+            if lf is None or a[1] == "ne":
+                continue
+            rows.append((a, lf[0], lf[1]))
         for _ in range(rounds):
             ivl = _Ivl(self.bounds)
             changed = False
-            for a in self.atoms:
-                lf = self._lin_of_atom(lin, a)
-                if lf is None or a[1] == "ne":
-                    continue
-                terms, c = lf
+            for a, terms, c in rows:
                 parts = []
                 # activity range of the row: finite sums plus the number of
                 # unbounded contributions, so each term's residual range is
