@@ -22,7 +22,7 @@ for t1 in [(0.001, 0.002, 0.02), (0.0005, 0.002, 0.01), (0.0002, 0.001, 0.005)]:
     st.pop("device", None)
     print(json.dumps({"tier1": t1, "wall_ms": walls, "stats": st,
                       "verdicts": {v: sum(1 for r in res if r.status == v) for v in ("sat", "unsat", "unknown")}}), flush=True)
-chk.TIER1_S = (0.001, 0.002, 0.02)
+chk.TIER1_S = SiteChecker.TIER1_S
 chk.trace = []
 chk.check_queries(qs)
 json.dump(chk.trace, open("gpurun_out/e2e_trace.json", "w"))
