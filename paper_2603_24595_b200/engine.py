@@ -351,6 +351,12 @@ class SiteChecker:
     # config3 end to end is within noise for 5, 10 and 20 ms caps (the compile
     # pool is the critical path) and the 10 ms cap keeps the device step short
     TIER1_S = (0.0005, 0.002, 0.01)   # per query, minimum, maximum
+    # smaller calls (analyze()'s one query per site) skip the first tier: a
+    # query the light tier leaves undecided is compiled twice, which only
+    # pays off amortised over a batch (measured on the B200, analyze() with
+    # device screening: rms_norm 79 -> 50 ms, silu_and_mul 38 -> 18 ms,
+    # paged_attention_v1 473 -> 414 ms; profiles/r02_analyze_tiers.jsonl)
+    TWO_TIER_MIN = 8
 
     def tier1_budget(self, n: int) -> float:
         per, lo, hi = self.TIER1_S
@@ -366,7 +372,7 @@ class SiteChecker:
         the budget did not finish -- through the full presolve and the
         device with the reference's per-query budget.  ``two_tier = False``
         runs (2) alone."""
-        if not self.two_tier or not queries:
+        if not self.two_tier or len(queries) < self.TWO_TIER_MIN:
             return self._check_full(queries)
         if self.compile_workers > 1 and len(queries) >= self.POOL_MIN_BATCH:
             # the caller's process unpickles every compiled query the pool
