@@ -147,8 +147,15 @@ MK_HD V mk_max(V a, V b) { return a > b ? a : b; }
 // truncating quotient, one division: a 32-bit division when both operands
 // fit (the common case for the contraction rows' bounds and coefficients;
 // a 64-bit division is a ~70-instruction sequence on the GPU)
-MK_HD i128 mk_tquot(i128 a, i128 b) { return a / b; }
+// (unit divisors -- most contraction-row coefficients -- need no division)
+MK_HD i128 mk_tquot(i128 a, i128 b) {
+  if (b == 1) return a;
+  if (b == -1) return -a;
+  return a / b;
+}
 MK_HD int64_t mk_tquot(int64_t a, int64_t b) {
+  if (b == 1) return a;
+  if (b == -1) return -a;
   if (a == (int64_t)(int32_t)a && b == (int64_t)(int32_t)b && !(a == INT32_MIN && b == -1))
     return (int64_t)((int32_t)a / (int32_t)b);
   return a / b;
