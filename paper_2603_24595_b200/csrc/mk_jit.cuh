@@ -146,6 +146,16 @@ inline void emit_path(std::ostringstream& s, const mk_problem& p, const mk_insn*
 // isotonic): such registers are 32-bit locals and an operation whose
 // operands and result are all 32-bit runs on the 32-bit pipe; everything
 // else is exact int64 (the narrow class).
+// instances per thread of the compacting generator's tile (256 threads)
+inline int gc_items() {
+  static const int v = [] {
+    const char* e = getenv("MK_GC_ITEMS");
+    const int x = e ? atoi(e) : 32;
+    return x >= 4 && x <= 64 && x % 4 == 0 ? x : 32;   // a multiple of 4 (the count scan)
+  }();
+  return v;
+}
+
 inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
                                    const mk_i128* consts, int n_outer, int off_reg, int shared,
                                    const int id_var[6], const int64_t* lo, const int64_t* hi,
@@ -278,6 +288,93 @@ inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
        " models += __shfl_down_sync(0xffffffffu, models, o); }\n"
        "  if ((threadIdx.x & 31) == 0) { if (done) atomicAdd(evaluated, done);"
        " if (models) atomicAdd(count, models); }\n}\n";
+  // compacting generator (sort path): each CTA takes the next tile of
+  // 256 x 8 instances in order (tile counter), evaluates them (item j of
+  // thread t is instance base + 256 j + t), counts the accesses per (item,
+  // warp), gets the tile's output offset by a decoupled look-back over the
+  // tiles before it and writes only the accesses, in instance order -- the
+  // separate compaction's full read and write of every tuple never happens
+  s << "__device__ __forceinline__ u64 gc_ld(const u64* p) { u64 v; asm volatile(\"ld.volatile.global.u64 %0, [%1];\""
+       " : \"=l\"(v) : \"l\"(p)); return v; }\n"
+       "__device__ __forceinline__ void gc_st(u64* p, u64 v) { asm volatile(\"st.volatile.global.u64 [%0], %1;\""
+       " :: \"l\"(p), \"l\"(v)); }\n"
+       "#define GC_ITEMS " << gc_items() << "\n"
+       "#define GC_AGG (1ull << 32)\n#define GC_INCL (2ull << 32)\n"
+       "extern \"C\" __global__ void __launch_bounds__(256) mk_race_genc_jit(unsigned long long vol, "
+    << KT << "* keys, unsigned int* vals, unsigned long long* count, unsigned long long* evaluated,"
+       " u64* lookback, unsigned int* tile_ctr, unsigned long long epoch) {\n"
+       "  __shared__ unsigned tile_s;\n  __shared__ unsigned cnt[GC_ITEMS * 8];\n"
+       "  __shared__ u64 prefix_s;\n"
+       "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
+       "  if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);\n  __syncthreads();\n"
+       "  const unsigned tile = tile_s;\n"
+       "  const unsigned long long base = (unsigned long long)tile * (256ull * GC_ITEMS);\n"
+       "  unsigned long long idx = base + threadIdx.x;\n"
+    << odometer_init("idx", "256ull", 256)
+    << "  unsigned long long done = 0, models = 0;\n"
+       "  " << KT << " key[GC_ITEMS];\n  unsigned keep[GC_ITEMS];\n"
+       "#pragma unroll\n"
+       "  for (int j = 0; j < GC_ITEMS; ++j) {\n"
+       "    " << KT << " k = 0;\n    bool hit = false;\n"
+       "    if (idx < vol) {\n"
+       << (count_inner ? "" : "      ++done;\n") <<
+       "      hit = mk_acc(" << call_args() << "done, k);\n"
+       "    }\n"
+       "    if (hit) ++models;\n"
+       "    key[j] = k;\n"
+       "    keep[j] = __ballot_sync(0xffffffffu, hit);\n"
+       "    if (lane == 0) cnt[j * 8 + warp] = __popc(keep[j]);\n"
+       "    idx += 256;\n"
+    << odometer_step()
+    << "  }\n  __syncthreads();\n"
+       "  if (warp == 0) {\n"
+       "    constexpr int E = GC_ITEMS / 4;   // (item, warp) counts per lane, in order\n"
+       "    unsigned loc[E], sum = 0;\n"
+       "#pragma unroll\n"
+       "    for (int e = 0; e < E; ++e) { loc[e] = cnt[lane * E + e]; sum += loc[e]; }\n"
+       "    unsigned incl = sum;\n"
+       "    for (int o = 1; o < 32; o <<= 1) { const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);"
+       " if (lane >= o) incl += y; }\n"
+       "    unsigned run = incl - sum;\n"
+       "#pragma unroll\n"
+       "    for (int e = 0; e < E; ++e) { cnt[lane * E + e] = run; run += loc[e]; }\n"
+       "    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);\n"
+       "    const u64 tag = epoch << 34;\n"
+       "    u64 prefix = 0;\n"
+       "    if (tile == 0) {\n      if (lane == 0) gc_st(lookback, tag | GC_INCL | total);\n"
+       "    } else {\n"
+       "      if (lane == 0) gc_st(lookback + tile, tag | GC_AGG | total);\n"
+       "      long long p = (long long)tile - 1;\n"
+       "      while (p >= 0) {\n"
+       "        const long long q = p - (long long)lane;\n"
+       "        u64 e = q >= 0 ? gc_ld(lookback + q) : (tag | GC_INCL);\n"
+       "        while ((e >> 34) != epoch || (e & (3ull << 32)) == 0) e = gc_ld(lookback + q);\n"
+       "        const unsigned inc = __ballot_sync(0xffffffffu, (e & GC_INCL) != 0);\n"
+       "        const unsigned upto = inc ? (unsigned)(__ffs(inc) - 1) : 31u;\n"
+       "        u64 c = ((unsigned)lane <= upto && q >= 0) ? (e & 0xffffffffull) : 0ull;\n"
+       "        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);\n"
+       "        prefix += c;\n"
+       "        if (inc) break;\n"
+       "        p -= 32;\n"
+       "      }\n"
+       "      if (lane == 0) gc_st(lookback + tile, tag | GC_INCL | (prefix + total));\n"
+       "    }\n"
+       "    if (lane == 0) prefix_s = prefix;\n"
+       "  }\n  __syncthreads();\n"
+       "  const u64 pre = prefix_s;\n"
+       "  const unsigned lt = (1u << lane) - 1u;\n"
+       "  idx = base + threadIdx.x;\n"
+       "#pragma unroll\n"
+       "  for (int j = 0; j < GC_ITEMS; ++j) {\n"
+       "    if ((keep[j] >> lane) & 1u) {\n"
+       "      const u64 o = pre + cnt[j * 8 + warp] + __popc(keep[j] & lt);\n"
+       "      keys[o] = key[j];\n      vals[o] = (unsigned int)idx;\n"
+       "    }\n"
+       "    idx += 256;\n"
+       "  }\n"
+       "  for (int o = 16; o > 0; o >>= 1) { done += __shfl_down_sync(0xffffffffu, done, o);"
+       " models += __shfl_down_sync(0xffffffffu, models, o); }\n"
+       "  if (lane == 0) { if (done) atomicAdd(evaluated, done); if (models) atomicAdd(count, models); }\n}\n";
   // one warp step of the fused pass over instances b0 .. b0 + 31 (lane l
   // holds b0 + l); `guarded`: the tail step, lanes past the range idle
   auto step = [&](bool guarded) {

@@ -368,7 +368,7 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   const int grid = ctx->sms * 8;
   const K sentinel = (K)(bits >= (int)(8 * sizeof(K)) ? ~(K)0 : (((K)1 << bits) - 1));
   // specialised generator (NVRTC) when available, else the interpreter
-  cudaKernel_t jk = nullptr;
+  cudaKernel_t jk = nullptr, jkc = nullptr;
   std::string src;
   if (!getenv("MK_NO_JIT")) {
     const mk_problem_set& set = prog->set;
@@ -385,6 +385,10 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
       }
     }
     jk = mkjit::get_kernel(ctx->jit, src, ctx->device);
+    // the compacting generator of the same source (MK_RACE_SEPARATE_COMPACT:
+    // dense generation + k_compact, measurement)
+    if (jk && !getenv("MK_RACE_SEPARATE_COMPACT"))
+      jkc = mkjit::get_kernel(ctx->jit, src, ctx->device, "mk_race_genc_jit");
   }
   out->jit = jk != nullptr;
   // fast path: the fused ordered pass (no per-instance HBM traffic).  When
@@ -475,7 +479,24 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
     return MK_OK;
   }
   CK(cudaEventRecord(ctx->ev[0], s));
-  if (jk) {
+  bool compacted = false;
+  if (jkc) {
+    // generation and compaction in one pass: only the accesses are written
+    mksort::Workspace gw = mksort::carve(wb + o_ws);
+    CK(cudaMemsetAsync(gw.tile_ctr + 14, 0, sizeof(unsigned), s));
+    unsigned long long a_vol = vol, a_epoch = mksort::next_epoch();
+    K* a_keys = k0;
+    uint32_t* a_vals = v0;
+    unsigned long long* a_cnt = ctr + 0;
+    unsigned long long* a_eval = ctr + 3;
+    unsigned long long* a_lb = gw.lookback;
+    unsigned* a_tc = gw.tile_ctr + 14;
+    void* args[] = {&a_vol, &a_keys, &a_vals, &a_cnt, &a_eval, &a_lb, &a_tc, &a_epoch};
+    const unsigned long long per = 256ull * (unsigned long long)mkjit::gc_items();
+    const unsigned long long tiles = (vol + per - 1) / per;
+    CK(cudaLaunchKernel((const void*)jkc, dim3((unsigned)tiles), dim3(RACE_THREADS), args, 0, s));
+    compacted = true;
+  } else if (jk) {
     unsigned long long a_vol = vol, a_nb = R.nblocks;
     K a_sent = sentinel;
     K* a_keys = k0;
@@ -507,8 +528,8 @@ static int race_run(mk_ctx* ctx, const RaceDev& R, unsigned long long vol, int b
   K* ko = k1;
   uint32_t* vc = v0;
   uint32_t* vo = v1;
-  if (h[0] == vol) {
-    CK(cudaMemcpyAsync(ctr + 5, &vol, sizeof(vol), cudaMemcpyHostToDevice, s));
+  if (compacted || h[0] == vol) {
+    CK(cudaMemcpyAsync(ctr + 5, &h[0], sizeof(h[0]), cudaMemcpyHostToDevice, s));
   } else {
     CK((mksort::compact<K, uint32_t>(k0, v0, k1, v1, vol, sentinel, wb + o_ws, ctr + 5, s)));
     kc = k1;
