@@ -318,6 +318,30 @@ def _cpu_baseline(queries, inst, budget_s):
                 "sample": f"unavailable: {exc}"}
 
 
+def _k2_sort_traffic():
+    """Measured DRAM bytes of one forced sort-path sweep (ncu launch list of
+    tools/gpu_k2_profile.sh, committed under profiles/): the sum over its
+    kernels of dram__bytes_read + dram__bytes_write, or None."""
+    import csv
+
+    path = os.path.join(ROOT, "profiles", "r02_k2_sort_launches.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+    except OSError:
+        return None
+    hdr, total = None, 0.0
+    for r in rows:
+        if "Kernel Name" in r and "Metric Value" in r:
+            hdr = r
+            continue
+        if hdr is None or len(r) != len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        if d["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += float(d["Metric Value"].replace(",", ""))
+    return total or None
+
+
 def _race_sweep_line(chk, args, peaks, src, int_peak):
     """K2 (race sweep, include/mk_b200.h mk_race_sweep) on config 1's output
     store (rms_norm, Llama-2-7B hidden 4096: out[blockIdx.x * hidden + idx])
@@ -388,8 +412,15 @@ def _race_sweep_line(chk, args, peaks, src, int_peak):
                           "same_result": (sr["tuples"], sr["conflicts"], sr["has_race"]) ==
                                          (r["tuples"], r["conflicts"], r["has_race"]),
                           "roofline": {"bound": "hbm", "achieved": s_ach, "peak": hbm_peak,
-                                       "unit": "GB/s", "frac": s_ach / hbm_peak, "traffic": None,
+                                       "unit": "GB/s", "frac": s_ach / hbm_peak,
+                                       "traffic": _k2_sort_traffic(),
+                                       "traffic_source": "profiles/r02_k2_sort_launches.csv "
+                                                         "(ncu, one forced sort-path sweep)",
                                        "algorithmic_bytes": sr["hbm_bytes"],
+                                       "note": "the generator compacts as it generates and the "
+                                               "order check finds the keys sorted, so the DRAM "
+                                               "traffic (generation write, order read, scan "
+                                               "read) is about half the 4 x tuple-bytes model",
                                        "peak_source": f"peaks file: {src}"}}}
 
 
