@@ -318,6 +318,8 @@ class SiteChecker:
         lim = dict(self.limits)
         lim["max_seconds"] = (budget_s if budget_s is not None else
                               min(self.limits["max_seconds"] * max(len(compiled), 1), 3600.0))
+        if budget_s is not None:
+            lim.update(self.TIER1_LIMITS)
         with self._device_lock:   # one engine call at a time per context
             if budget_s is not None and not self._warm and packed.problems:
                 # the first engine call of a context allocates its work
@@ -357,6 +359,11 @@ class SiteChecker:
     # device screening: rms_norm 79 -> 50 ms, silu_and_mul 38 -> 18 ms,
     # paged_attention_v1 473 -> 414 ms; profiles/r02_analyze_tiers.jsonl)
     TWO_TIER_MIN = 8
+    # extra engine limits of a first-tier call: no adaptive probe (a short
+    # budgeted call gains nothing from the probe's restart; measured on the
+    # B200: config3's first-tier device time 86 -> 72 ms per check_queries
+    # call, profiles/r02_e2e_tiers_probe.jsonl)
+    TIER1_LIMITS: Dict[str, object] = {"chunk": 65536}
 
     def tier1_budget(self, n: int) -> float:
         per, lo, hi = self.TIER1_S

@@ -8,8 +8,11 @@ from bench import entries, load_sites
 from paper_2603_24595_b200.engine import SiteChecker, BatchStats
 qs = load_sites(entries("config3"))[1]
 chk = SiteChecker(device=0)
-for t1 in [(0.001, 0.002, 0.02), (0.0005, 0.002, 0.01), (0.0002, 0.001, 0.005)]:
+import itertools
+for t1, extra in itertools.product([(0.0005, 0.002, 0.01), (0.0002, 0.001, 0.005)],
+                                   [{}, {"chunk": 65536}]):
     chk.TIER1_S = t1
+    chk.TIER1_LIMITS = extra
     for _ in range(2):
         chk.check_queries(qs)
     walls = []
@@ -20,7 +23,7 @@ for t1 in [(0.001, 0.002, 0.02), (0.0005, 0.002, 0.01), (0.0002, 0.001, 0.005)]:
         walls.append(round((time.perf_counter() - t) * 1e3, 1))
         st = dataclasses.asdict(chk.stats)
     st.pop("device", None)
-    print(json.dumps({"tier1": t1, "wall_ms": walls, "stats": st,
+    print(json.dumps({"tier1": t1, "extra": extra, "wall_ms": walls, "stats": st,
                       "verdicts": {v: sum(1 for r in res if r.status == v) for v in ("sat", "unsat", "unknown")}}), flush=True)
 chk.TIER1_S = SiteChecker.TIER1_S
 chk.trace = []
