@@ -1617,7 +1617,8 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
     if (cls[0].ntasks < 0) budget_hit = true;
     else top = 0;
   }
-  const bool trace = getenv("MK_TRACE_RUN") != nullptr;
+  const char* trace_env = getenv("MK_TRACE_RUN");
+  const bool trace = trace_env && *trace_env && *trace_env != '0';
   auto tr_el = [&]() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3;
   };
