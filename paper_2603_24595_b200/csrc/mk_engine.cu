@@ -191,8 +191,19 @@ __device__ __forceinline__ V ldv_volatile(const volatile mk_i128* p) {
 }
 
 // 64-bit lexicographic key of a point (see Incumbent::key)
+// the best corner of a box in witness order, read in place (the corner never
+// exists as an array: a materialised copy was one more local-memory array per
+// box evaluation)
 template <typename V>
-__device__ unsigned long long lex_key(const DevSet& D, const mk_problem& p, const V* x) {
+struct BoxCorner {
+  const V* lo;
+  const V* hi;
+  uint64_t maxmask;
+  __device__ __forceinline__ V operator[](int i) const { return ((maxmask >> i) & 1) ? hi[i] : lo[i]; }
+};
+
+template <typename V, typename X>
+__device__ unsigned long long lex_key(const DevSet& D, const mk_problem& p, const X& x) {
   typedef typename MkNum<V>::U U;
   unsigned long long key = 0;
   int left = 64;
@@ -216,8 +227,8 @@ __device__ unsigned long long lex_key(const DevSet& D, const mk_problem& p, cons
 
 // incumbent test: true when the box cannot hold anything better than the
 // current incumbent (its best corner is not strictly better)
-template <typename V>
-__device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, const V* corner) {
+template <typename V, typename X>
+__device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, const X& corner) {
   Incumbent* I = D.inc + pid;
   {
     unsigned long long kmin = *((volatile unsigned long long*)&I->key);
@@ -246,8 +257,8 @@ __device__ bool inc_dominates(const DevSet& D, int pid, const mk_problem& p, con
   return dominated;
 }
 
-template <typename V>
-__device__ void inc_offer(const DevSet& D, int pid, const mk_problem& p, const V* x) {
+template <typename V, typename X>
+__device__ void inc_offer(const DevSet& D, int pid, const mk_problem& p, const X& x) {
   Incumbent* I = D.inc + pid;
   // lock-free filter: a candidate whose key prefix is worse than the best
   // offered key loses without touching the lock
@@ -375,11 +386,10 @@ __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo,
   a.m = 0;
   a.sv2 = -1;
   a.m2 = 1;
-  V c[CAPV];
+  const BoxCorner<V> c{lo, hi, p.maxmask};
   st.boxes++;
   for (int v = 0; v < nv; ++v)
     if (lo[v] > hi[v]) return a;  // an empty root (k_root_contract)
-  mk_corner(lo, hi, nv, p.maxmask, c);
   const double vol0 = mk_volume_f(lo, hi, nv);
   if (inc_dominates<V>(D, pid, p, c)) {
     st.covered += vol0;
@@ -403,8 +413,7 @@ __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo,
     return a;
   }
   if (v.all_true) {
-    mk_corner(lo, hi, nv, p.maxmask, c);
-    inc_offer<V>(D, pid, p, c);
+    inc_offer<V>(D, pid, p, c);   // the contracted box's best corner
     st.covered += vol0;
     return a;
   }
