@@ -59,6 +59,15 @@ namespace {
 #define MK_SHREG_PATH 0
 #endif
 
+// bound-contraction sweeps per box (each ends early once nothing changes).
+// One: a box's children inherit its contracted bounds and are contracted
+// again, so further sweeps on the parent mostly repeat work (measured on the
+// B200, full sets: config3 15.4 -> 13.2 ms, moe_align 6.4 -> 6.0,
+// paged_attention_v2 long 12.6 -> 12.0 at 1 vs 4; profiles/r02_contract_sweeps.jsonl)
+#ifndef MK_CONTRACT_SWEEPS
+#define MK_CONTRACT_SWEEPS 1
+#endif
+
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SMALL_V = 8;    // free symbols of a "small" problem
 constexpr int SMALL_R = 64;   // registers of a "small" problem
@@ -395,7 +404,7 @@ __device__ Act process_box(const DevSet& D, int pid, const mk_problem& p, V* lo,
     st.covered += vol0;
     return a;
   }
-  if (!mk_contract(P, lo, hi, 4)) {
+  if (!mk_contract(P, lo, hi, MK_CONTRACT_SWEEPS)) {
     st.covered += vol0;
     return a;
   }
