@@ -1193,10 +1193,11 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   int64_t max_rounds = lim && lim->max_rounds > 0 ? lim->max_rounds : 200000;
   int64_t max_boxes = lim && lim->max_boxes > 0 ? lim->max_boxes : (int64_t)4e9;
   double max_seconds = lim && lim->max_seconds > 0 ? lim->max_seconds : 30.0;
-  // split arity, measured on the B200 (profiles/r02_split_k_*.jsonl): the
-  // whole golden corpus sums to 117 ms of resident steps at 16, 86 at 8, 80
-  // at 12; the config3 headline set takes 135 ms at 16, 80 at 12, 39 at 8
-  int K = 8;
+  // split arity, measured on the B200 (profiles/r02_split_knobs_after_kernel_work.jsonl,
+  // r02_split_k_final.jsonl): 8 was best with four contraction sweeps per
+  // box; with one sweep, 12 (full sets: config3 13.6 -> 9.1 ms, paged
+  // attention v2 long 12.0 -> 10.4, moe_align equal)
+  int K = 12;
   if (const char* e = getenv("MK_SPLIT_K")) K = atoi(e) > 1 ? atoi(e) : K;
   // widen the splits of shallow stacks (measured: config3 40 -> 32 ms,
   // racy 8.7 -> 4.6 ms, the rest within noise; profiles/r02_adapt_k.jsonl)
