@@ -362,8 +362,10 @@ class SiteChecker:
     # extra engine limits of a first-tier call: no adaptive probe (a short
     # budgeted call gains nothing from the probe's restart; measured on the
     # B200: config3's first-tier device time 86 -> 72 ms per check_queries
-    # call, profiles/r02_e2e_tiers_probe.jsonl)
-    TIER1_LIMITS: Dict[str, object] = {"chunk": 65536}
+    # call, profiles/r02_e2e_tiers_probe.jsonl) and split arity 8: on the
+    # light problems a 10 ms budget leaves 60 undecided at 8, 78 at the full
+    # problems' 12 (profiles/r02_tier1_split_k.jsonl)
+    TIER1_LIMITS: Dict[str, object] = {"chunk": 65536, "split_k": 8}
 
     def tier1_budget(self, n: int) -> float:
         per, lo, hi = self.TIER1_S
