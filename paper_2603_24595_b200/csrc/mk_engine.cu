@@ -881,13 +881,18 @@ __global__ void __launch_bounds__(SEARCH_THREADS, MinBlocks<V>::value)
     // ntasks-1-t for task t, so the run's boxes are contiguous, worst first,
     // exactly the stack order -- which fills the warp's lanes from the
     // first step instead of one root box per unit
+    // the grab's problem ids, one per lane, read in parallel (G <= 32)
+    const int cnt = tend - task;
+    int my_pid = -2;
+    if (lane < cnt)
+      my_pid = box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - 1 - task - lane))->prob;
     for (int t = task; t < tend;) {
-      const Box* tb = box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - 1 - t));
-      const int pid = tb->prob;
-      int len = 1;
-      while (t + len < tend &&
-             box_at(const_cast<void*>(A.tasks), A.box_bytes, (size_t)(A.ntasks - 1 - t - len))->prob == pid)
-        ++len;
+      const int off = t - task;
+      const int pid = __shfl_sync(FULL, my_pid, off);
+      // the run: consecutive lanes from `off` holding the same problem
+      const unsigned same = __ballot_sync(FULL, lane >= off && lane < cnt && my_pid == pid);
+      const unsigned rest = ~(same >> off);
+      const int len = rest ? __ffs(rest) - 1 : 32 - off;
       if (dumped) {
         // this unit's launch ended: the rest of its grab goes to the dump
         if (pid >= 0) {
@@ -1206,6 +1211,7 @@ static int run_set(mk_ctx* ctx, mk_dset* ds, const mk_limits* lim, int32_t* stat
   // most tasks a unit grabs at once (k_search; 1 = one root per grab)
   long long group_cap = 16;   // measured: profiles/r02_task_group.jsonl
   if (const char* e = getenv("MK_TASK_GROUP")) group_cap = atoi(e) > 0 ? atoi(e) : 1;
+  if (group_cap > 32) group_cap = 32;   // one task per lane when a grab is scanned
   if (lim && lim->split_k > 1) K = lim->split_k;
   int chunk = lim && lim->chunk > 0 ? lim->chunk : 65536;
   long long leaf_volume = lim && lim->leaf_volume > 0 ? lim->leaf_volume : 4096;
