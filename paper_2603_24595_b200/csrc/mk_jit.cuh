@@ -156,6 +156,17 @@ inline int gc_items() {
   return v;
 }
 
+// ", N": the compacting generator asks for N resident 256-thread CTAs per SM
+// (a register cap).  Default 5, measured on the B200 (config 1's forced sort
+// path: uncapped 115 registers, 2 CTAs per SM, generation 3.38 ms; 5 CTAs
+// 2.47 ms; 4: 2.67; 6: 2.59; 8: 3.19; profiles/r02_k2_genc_minb.jsonl).
+// MK_GC_MINB=0 leaves the registers uncapped.
+inline std::string gc_minb() {
+  const char* e = getenv("MK_GC_MINB");
+  const int x = e ? atoi(e) : 5;
+  return x > 0 && x <= 8 ? ", " + std::to_string(x) : std::string();
+}
+
 inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
                                    const mk_i128* consts, int n_outer, int off_reg, int shared,
                                    const int id_var[6], const int64_t* lo, const int64_t* hi,
@@ -300,7 +311,7 @@ inline std::string race_gen_source(const mk_problem& p, const mk_insn* insns,
        " :: \"l\"(p), \"l\"(v)); }\n"
        "#define GC_ITEMS " << gc_items() << "\n"
        "#define GC_AGG (1ull << 32)\n#define GC_INCL (2ull << 32)\n"
-       "extern \"C\" __global__ void __launch_bounds__(256) mk_race_genc_jit(unsigned long long vol, "
+       "extern \"C\" __global__ void __launch_bounds__(256" << gc_minb() << ") mk_race_genc_jit(unsigned long long vol, "
     << KT << "* keys, unsigned int* vals, unsigned long long* count, unsigned long long* evaluated,"
        " u64* lookback, unsigned int* tile_ctr, unsigned long long epoch) {\n"
        "  __shared__ unsigned tile_s;\n  __shared__ unsigned cnt[GC_ITEMS * 8];\n"
