@@ -413,6 +413,10 @@ def _race_sweep_line(chk, args, peaks, src, int_peak):
                                          (r["tuples"], r["conflicts"], r["has_race"]),
                           "roofline": {"bound": "hbm", "achieved": s_ach, "peak": hbm_peak,
                                        "unit": "GB/s", "frac": s_ach / hbm_peak,
+                                       "achieved_on_measured_traffic":
+                                           (_k2_sort_traffic() or 0) / (sms_ / 1e3) / 1e9,
+                                       "frac_on_measured_traffic":
+                                           (_k2_sort_traffic() or 0) / (sms_ / 1e3) / 1e9 / hbm_peak,
                                        "traffic": _k2_sort_traffic(),
                                        "traffic_source": "profiles/r02_k2_sort_launches.csv "
                                                          "(ncu, one forced sort-path sweep)",
